@@ -1,0 +1,299 @@
+#!/usr/bin/env python
+"""Benchmark of the fused ensemble step (arXiv 2101.09059 hot path) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W --config c2 --kernel assembled|matrix_free]
+    python bench.py --impl reference ...        # the CPU oracle, timed on the host cores
+
+One "step" = one explicit central-difference step of all N_s realisations (S2 load +
+S3 ensemble SpMM + S4 update, one fused kernel launch).  Metric (BASELINE.json):
+ensemble DOF-updates/s = N_s * 3V * steps / time, plus the fused step's HBM GB/s against
+the measured peak.  Multi-GPU (torchrun): ensemble sharding, N_s per GPU fixed (weak
+scaling), no collective on the data path; timing = max over ranks (CUDA events).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("ensemble DOF-updates/s (N_s×DOF×steps/s) and fused-step HBM GB/s vs peak")
+FALLBACK_HBM_GBS = 6650.0      # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def _workload_desc(cfg, n_s_total, world):
+    m = cfg.mesh
+    return (f"{cfg.name}: ideal cylinder D=4 L=30 cm, {m.meta['n_circ']}x{m.meta['n_axial']} rings "
+            f"(V={m.n_nodes}, F={m.n_tris}), N_s={n_s_total} ({cfg.n_s}/GPU), "
+            + ("steady 13 mmHg" if cfg.traction.n_tab == 0 else "pulsatile 13+27 mmHg")
+            + (f", mode-1 damping {cfg.c_d:g}/s" if cfg.damping == 1 else ", undamped"))
+
+
+def _peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons during the timed region."""
+
+    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+             "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
+
+    def __init__(self, device_index: int, period_s: float = 0.02):
+        self.samples, self.reasons = [], set()
+        self.period = period_s
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.NAMES.items():
+                    if r & getattr(nv, attr, 0):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _cpu_baseline(cfg, budget_s: float = 12.0, max_steps: int = 40):
+    """The oracle as it stands (oracle/oracle.c), timed on this host's cores on a bounded
+    sample of the same workload: the same mesh and all N_s realisations, a few steps."""
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    import oracle
+    m = cfg.mesh
+    om = oracle.OracleModel(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=cfg.rho, nu=cfg.nu,
+                            k_shear=cfg.k_shear, damping=cfg.damping, c_d=cfg.c_d)
+    tr = cfg.traction
+    om.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    om.run(1)
+    n, t0 = 0, time.perf_counter()
+    while n < max_steps and time.perf_counter() - t0 < budget_s:
+        om.run(1)
+        n += 1
+    el = time.perf_counter() - t0
+    return {"value": cfg.n_s * 3 * m.n_nodes * n / el, "unit": "DOF-updates/s",
+            "cores": int(os.environ.get("OMP_NUM_THREADS", cores)), "kind": "oracle",
+            "sample": f"{cfg.name} mesh, all {cfg.n_s} realisations, {n} steps ({el:.1f} s)",
+            "s_per_step": el / n}
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    from paper_2101_09059_b200.inputs import configs
+    cfg = configs.make(args.config, n_s=args.n_s)
+    # each "step" of this arm is one oracle time step on the full workload (bounded: the
+    # oracle steps a few hundred ms per step on 16 cores)
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    import oracle
+    m = cfg.mesh
+    om = oracle.OracleModel(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=cfg.rho, nu=cfg.nu,
+                            k_shear=cfg.k_shear, damping=cfg.damping, c_d=cfg.c_d)
+    tr = cfg.traction
+    om.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    om.run(args.warmup)
+    t0 = time.perf_counter()
+    om.run(args.steps)
+    el = time.perf_counter() - t0
+    value = cfg.n_s * 3 * m.n_nodes * args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "DOF-updates/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": _workload_desc(cfg, cfg.n_s, 1), "impl_detail": "oracle/oracle.c, OpenMP over realisations"},
+            "cpu_baseline": {"value": value, "unit": "DOF-updates/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
+                             "kind": "oracle", "sample": f"{cfg.name}, all {cfg.n_s} realisations, {args.steps} steps"},
+            "e2e": {"value": value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5000)
+    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--n-s", type=int, default=None, help="realisations per GPU (default: the config's)")
+    ap.add_argument("--kernel", default="assembled", choices=["assembled", "matrix_free"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-windows", type=int, default=10)
+    ap.add_argument("--obs-every", type=int, default=100)
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        if args.steps > 50:          # the driver's K for our arm; the oracle is ~10^3x slower
+            args.steps, args.warmup = 5, 1
+        return run_reference(args)
+
+    import torch
+    world, rank, local = _dist()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2101_09059_b200 import solver
+    from paper_2101_09059_b200.inputs import configs
+    base = configs.make(args.config, n_s=args.n_s, n_circ=None)
+    n_s = base.n_s
+    cfg = configs.make(args.config, n_s=n_s, s_begin=rank * n_s) if world > 1 else base
+    m = cfg.mesh
+    stream = torch.cuda.current_stream()
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=cfg.rho, nu=cfg.nu,
+                          k_shear=cfg.k_shear, damping=cfg.damping, c_d=cfg.c_d, kernel=args.kernel,
+                          dist="ensemble" if world > 1 else "single", s_begin=cfg.s_begin,
+                          rank=rank, world=world, device=local)
+    tr = cfg.traction
+    ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    info = ens.info()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    ens.step(max(3, args.warmup))
+    ens.sync()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        ens.step(args.steps)
+        e1.record(stream)
+        e1.synchronize()
+    barrier()
+    ens.sync()                                   # raises on divergence
+    el = e0.elapsed_time(e1) / 1e3
+    el_max = el
+    if world > 1:
+        t = torch.tensor([el], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        el_max = float(t.item())
+    dof_updates = world * n_s * 3 * m.n_nodes * args.steps
+    value = dof_updates / el_max
+    per_launch = el / args.steps
+    peak, peak_src = _peak_hbm()
+    achieved = info["bytes_per_step"] / per_launch / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tj = json.load(f)
+        key = f"{args.config}/{args.kernel}/{n_s}"
+        traffic = tj.get(key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # end to end through the public API with host buffers: per observation window of
+    # obs_every steps, H2D of the traction (pinned) + the steps + D2H of u_n (pinned)
+    Fp = torch.from_numpy(np.ascontiguousarray(tr.F)).pin_memory()
+    out = torch.empty((n_s, m.n_nodes, 3), dtype=torch.float64).pin_memory()
+    win = args.obs_every
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_windows):
+        ens.set_traction(Fp.numpy(), tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+        ens.step(win)
+        ens.get_state(u_n=out, want_prev=False)
+    e2e_el = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_el], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_el = float(t.item())
+    e2e_value = world * n_s * 3 * m.n_nodes * win * args.e2e_windows / e2e_el
+    h2d = Fp.numel() * 8 + tr.tab_t.size * 8 + tr.tab_g.size * 8
+    d2h = out.numel() * 8
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = _cpu_baseline(base)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "DOF-updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": _workload_desc(cfg, world * n_s, world), "kernel": args.kernel,
+                       "n_s_per_gpu": n_s, "V": m.n_nodes, "F": m.n_tris, "nnzb": info["nnzb"],
+                       "dt": info["dt"], "parallelism": f"ensemble-shard x{world}",
+                       "l2": f"inputs larger than L2: {info['bytes_per_step'] / 1e9:.3f} GB streamed per step vs 126 MB L2 (no flush)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "k_step_assembled" if args.kernel == "assembled" else "k_step_matrix_free",
+                         "algorithmic_bytes_per_launch": info["bytes_per_step"]},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "DOF-updates/s", "h2d_bytes_per_step": h2d / win,
+                    "d2h_bytes_per_step": d2h / win,
+                    "window": f"{win} steps + ens_set_traction (H2D {h2d} B) + ens_get_state u_n (D2H {d2h} B)"},
+            "gpu_launches": args.steps + 1,
+            "clocks": clk.summary(),
+            "paper_best_context": {"value": 7.27e8, "unit": "DOF-updates/s",
+                                   "hardware": "4x RTX 2080 Ti, OpenCL, 131,552-tri cylinder, 500 realisations (PAPER.md:665)"},
+        }
+        print(json.dumps(line), flush=True)
+    ens.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,213 @@
+/*
+ * ens.h -- C ABI of the B200-native ensemble explicit shell solver (arXiv 2101.09059).
+ *
+ * The hot path is one explicit central-difference step of N_s wall realisations at once
+ * (PAPER.md = the paper's LaTeX source):
+ *
+ *   (M~ + dt/2 C~) u_{n+1} = dt^2 f_n - (dt^2 K - 2M) u_n - (M - dt/2 C) u_{n-1}
+ *                                                (Eq. 22)
+ *
+ * with K = K(theta_s) the 3-dof linear membrane + transverse-shear shell stiffness of
+ * realisation s (Eqs. 7-10), M~ the lumped diagonal mass and C~ the
+ * diagonal damping, f_n the prescribed wall traction of the one-way
+ * coupled fluid solve, applied to all realisations at once ("solving
+ * multiple realizations ... at the same time"; "no approximation
+ * introduced").  The product K_s u_s is an ensemble sparse
+ * matrix-multi-vector product on one shared block-CSR pattern with 9 N_s values per
+ * block ("dense coefficient entries of size 9 n_s") or its matrix-free
+ * element form scaled by E*zeta at the Gauss points.
+ *
+ * Conventions (all calls)
+ *   - Units CGS: cm, g, s, Ba = dyn/cm^2.
+ *   - Host arrays passed IN are read during the call and never retained: the library
+ *     copies everything it needs before returning (ownership stays with the caller).
+ *   - Ensemble arrays crossing the ABI are realisation-OUTERMOST in the caller's node
+ *     numbering: u[n_s][n_nodes][3], E[n_s][n_nodes], h[n_s][n_nodes].  Inside, the
+ *     device layout is realisation-innermost in RCM order.
+ *   - Return value: ENS_OK (0) or a negative ENS_E_* code; ens_last_error() gives a
+ *     message naming the offending argument / element / edge / step.
+ *   - A context is not thread-safe; distinct contexts are independent.
+ *   - Device memory is owned by the context, obtained through opt->dev_alloc (the
+ *     PyTorch caching allocator in the Python binding) or cudaMallocAsync if NULL.
+ *   - Every floating-point quantity is IEEE fp64.
+ */
+#ifndef ENS_H_
+#define ENS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ENS_ABI_VERSION 1
+
+enum {
+    ENS_OK = 0,
+    ENS_E_ARG = -1,         /* invalid argument (n_s < 1, E <= 0, h <= 0, rho <= 0, nu not in [0, 0.5], bad dt ...) */
+    ENS_E_MESH = -2,        /* invalid mesh: node index out of range, repeated node, degenerate triangle,
+                               edge shared by > 2 triangles */
+    ENS_E_OOM = -3,         /* device allocation failed */
+    ENS_E_CUDA = -4,        /* CUDA runtime error (no device, launch failure, ...) */
+    ENS_E_NCCL = -5,        /* NCCL error (node-partitioned mode) */
+    ENS_E_DIVERGED = -6,    /* a non-finite displacement appeared (step and realisation in the message) */
+    ENS_E_STATE = -7,       /* context latched after divergence: call ens_set_state first */
+    ENS_E_UNSUPPORTED = -8  /* option combination not built */
+};
+
+/* Bits of ens_mesh.fixed[i]: bit c set => displacement component c (x, y, z) of node i is
+ * held at zero (fully fixed ends: value 7). */
+#define ENS_FIX_X 1
+#define ENS_FIX_Y 2
+#define ENS_FIX_Z 4
+
+typedef struct {
+    int64_t n_nodes;        /* V >= 1 */
+    int64_t n_tris;         /* F >= 1 */
+    const double* xyz;      /* [V][3] node coordinates, cm */
+    const int32_t* tris;    /* [F][3] 0-based node ids, counter-clockwise about the outward normal */
+    const uint8_t* fixed;   /* [V] Dirichlet bitmask (ENS_FIX_*), or NULL = none fixed */
+} ens_mesh;
+
+typedef struct {
+    int32_t n_s;            /* number of realisations held by this context (>= 1) */
+    const double* E;        /* [n_s][V] nodal Young's modulus, Ba (> 0)  (Eq. 11) */
+    const double* h;        /* [n_s][V] nodal wall thickness zeta, cm (> 0) */
+    double rho;             /* wall density, g/cm^3 (> 0); 1.06 */
+    double nu;              /* Poisson ratio in [0, 0.5] (Eq. 9; not stated in the paper) */
+    double k_shear;         /* transverse shear factor k (> 0), 5/6 */
+    int32_t s_begin;        /* global index of realisation 0 of this context (ensemble shards);
+                               used only in diagnostics */
+} ens_materials;
+
+enum { ENS_DAMP_NONE = 0, ENS_DAMP_MASS = 1, ENS_DAMP_IDENTITY = 2 };
+enum { ENS_KERNEL_ASSEMBLED = 0, ENS_KERNEL_MATRIX_FREE = 1 };
+enum { ENS_DIST_SINGLE = 0, ENS_DIST_NODE = 1, ENS_DIST_ENSEMBLE = 2 };
+
+typedef struct {
+    double dt;              /* time step, s; <= 0 => cfl_safety * l_min / sqrt(E_max / rho) */
+    double cfl_safety;      /* 0 => 0.9 */
+    double c_d;             /* damping coefficient */
+    int32_t damping;        /* ENS_DAMP_*: NONE C~ = 0; MASS C~ = c_d M~ (1/s); IDENTITY C~ = c_d I (g/s) */
+    int32_t kernel;         /* ENS_KERNEL_*: ASSEMBLED (per-realisation block-CSR values) or MATRIX_FREE */
+    int32_t dist;           /* ENS_DIST_*; ENSEMBLE = this rank holds realisations [s_begin, s_begin + n_s) */
+    int32_t rank, world;    /* process-group position (dist != SINGLE) */
+    void* nccl_comm;        /* ncclComm_t for ENS_DIST_NODE (torch ProcessGroupNCCL), else NULL */
+    void* stream;           /* cudaStream_t all work is enqueued on (NULL = legacy default stream) */
+    void* (*dev_alloc)(size_t bytes, void* user);    /* optional device allocator */
+    void (*dev_free)(void* ptr, void* user);
+    void* alloc_user;
+    int32_t device;         /* CUDA device ordinal; < 0 => current device */
+} ens_options;
+
+typedef struct ens_ctx ens_ctx;
+
+typedef struct {
+    double dt, dt_cfl;
+    int64_t n_nodes, n_tris, nnzb;      /* nnzb: 3x3 blocks of the pattern (= V + 2 #edges) */
+    int32_t n_s, kernel, damping, dist;
+    int64_t step;                       /* steps taken since t = 0 (t = step * dt) */
+    int64_t bytes_per_step;             /* algorithmic HBM bytes of one fused step */
+    int64_t flops_per_step;             /* algorithmic fp64 flops of one fused step */
+    int64_t device_bytes;               /* device memory held by the context */
+    int32_t rcm_bandwidth;              /* max |i - j| over the pattern in RCM order */
+    int32_t launches_per_step;          /* kernels enqueued per ens_step step */
+} ens_info;
+
+/* Create a context: validate the mesh, build the RCM-ordered block-CSR pattern, the
+ * element stiffnesses K^_e (E = 1, unit thickness, global frame), the Gauss-point
+ * material scalings alpha_{e,s} = sum_g w_g E_g zeta_g, the lumped
+ * masses, the central-difference coefficients and dt; upload; assemble the values on
+ * the device (kernel = ASSEMBLED).  State starts at rest: u_0 = u_{-1} = 0, t = 0.
+ * Traction starts at zero.  On error *out = NULL.  Collective when dist = NODE. */
+int ens_create(const ens_mesh* mesh, const ens_materials* mat, const ens_options* opt, ens_ctx** out);
+
+/* Prescribed wall traction, identical for all realisations (one-way coupling with a
+ * rigid-wall fluid; loads applied as nodal forces):
+ *   f(t) = ramp(t) * sum_k g_k(t) F_k,   ramp(t) = sin(pi t / (2 ramp_T)) for t < ramp_T, else 1
+ *   (PAPER.md:512, 571), g_k = linear interpolation of tab_g[k][:] at tau = t mod period
+ *   (period <= 0: no wrap), clamped to the end values; n_tab = 0 => g_k = 1.
+ * F: [n_fields][V][3] nodal forces (dyn) in the caller's numbering, 1 <= n_fields <= 4.
+ * tab_t: [n_tab] strictly increasing (s); tab_g: [n_fields][n_tab].  Copied. */
+int ens_set_traction(ens_ctx* ctx, int32_t n_fields, const double* F, int32_t n_tab,
+                     const double* tab_t, const double* tab_g, double period, double ramp_T);
+
+/* Enqueue n >= 0 fused steps on the context stream and return without waiting.  Each
+ * step reads u_n, u_{n-1}, writes u_{n+1} over u_{n-1} and evaluates f at t_n = n dt.
+ * A non-finite result sets a device flag that the next synchronising call
+ * (ens_get_state / ens_sync) reports as ENS_E_DIVERGED; afterwards the context returns
+ * ENS_E_STATE until ens_set_state. */
+int ens_step(ens_ctx* ctx, int64_t n);
+
+/* Wait for the enqueued work; report a pending divergence. */
+int ens_sync(ens_ctx* ctx);
+
+/* Copy the state to caller-owned HOST buffers (either may be NULL):
+ * u_n, u_nm1: [n_s][V][3] in the caller's node numbering.  t, step may be NULL.
+ * Synchronises the context stream. */
+int ens_get_state(ens_ctx* ctx, double* u_n, double* u_nm1, double* t, int64_t* step);
+
+/* Overwrite the state (checkpoint / resume; clears the divergence latch).
+ * u_n, u_nm1: [n_s][V][3] host, caller's numbering; NULL => zeros. */
+int ens_set_state(ens_ctx* ctx, const double* u_n, const double* u_nm1, double t, int64_t step);
+
+/* Diagnostic: y_s = K_s u_s for all s with the hot kernel's own product (same inner loop
+ * and summation order as ens_step).  u, y: [n_s][V][3] host, caller's numbering. */
+int ens_apply_stiffness(ens_ctx* ctx, const double* u, double* y);
+
+/* Sizes, dt and algorithmic traffic of the context. */
+int ens_query(const ens_ctx* ctx, ens_info* info);
+
+/* Destroy (NULL is a no-op).  Synchronises the stream first. */
+void ens_destroy(ens_ctx* ctx);
+
+/* Message of the last error on ctx (or, for ctx = NULL, of the last failed call on this
+ * thread).  Valid until the next call on the same context / thread. */
+const char* ens_last_error(const ens_ctx* ctx);
+
+/* ---- host-side setup maps (no device needed; used by the CPU tests) ------------------ */
+
+/* Mesh validation as in ens_create.  Returns ENS_OK or ENS_E_MESH; *bad = element (or the
+ * first node of the offending edge).  *code: 1 index, 2 repeated node, 3 degenerate, 4 edge. */
+int ens_host_validate(int64_t n_nodes, int64_t n_tris, const double* xyz, const int32_t* tris,
+                      int32_t* code, int64_t* bad);
+
+/* RCM permutation and block-CSR pattern exactly as ens_create builds them.
+ * perm[V] (perm[new] = old), row_ptr[V+1], col[col_cap]; *nnzb = blocks written.
+ * Returns ENS_E_ARG if col_cap is too small (*nnzb then holds the needed size). */
+int ens_host_pattern(int64_t n_nodes, int64_t n_tris, const int32_t* tris, int32_t* perm,
+                     int64_t* row_ptr, int32_t* col, int64_t col_cap, int64_t* nnzb);
+
+/* Node-partition bounds (bounds[P+1]) of an RCM-ordered pattern, balanced by blocks. */
+int ens_host_partition(int64_t n_nodes, const int64_t* row_ptr, int32_t n_parts, int64_t* bounds);
+
+/* Ghost rows of part [lo, hi): sorted columns outside the range.  ghosts[cap]; *n = count. */
+int ens_host_ghosts(int64_t n_nodes, const int64_t* row_ptr, const int32_t* col, int64_t lo,
+                    int64_t hi, int32_t* ghosts, int64_t cap, int64_t* n);
+
+/* Element stiffness K^_e (E = 1, unit thickness, global frame) and area, as ens_create
+ * computes them.  Khat: [F][9][9]; area: [F]. */
+int ens_host_element_stiffness(int64_t n_nodes, int64_t n_tris, const double* xyz,
+                               const int32_t* tris, double nu, double k_shear, double* Khat,
+                               double* area);
+
+/* Gauss-point scaling alpha [n_s][F], lumped mass m [n_s][V] and CFL dt, as ens_create
+ * computes them. */
+int ens_host_materials(int64_t n_nodes, int64_t n_tris, const double* xyz, const int32_t* tris,
+                       int32_t n_s, const double* E, const double* h, double rho,
+                       double cfl_safety, double* alpha, double* mass, double* dt_cfl);
+
+/* ---- test-only: synthetic operators (kernel unit tests, not the user contract) ----- */
+
+/* A context on a caller-given block-CSR pattern (any numbering, used as is) and values:
+ * row_ptr[V+1], col[nnzb], Kval[n_s][nnzb][9], c1/c2/c3 [n_s][V] (u_{n+1} =
+ * c1 (f - K u) + c2 u_n - c3 u_{n-1}), fixed[V] or NULL. */
+int ens_create_csr(int64_t n_nodes, const int64_t* row_ptr, const int32_t* col, int32_t n_s,
+                   const double* Kval, const double* c1, const double* c2, const double* c3,
+                   const uint8_t* fixed, double dt, const ens_options* opt, ens_ctx** out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ENS_H_ */

@@ -1,0 +1,72 @@
+// device.hpp -- launchers of the sm_100a kernels (kernels.cu).  Device layout (DESIGN.md
+// "HBM layout"): rows in RCM order, realisation innermost:
+//   u      [V][3][n_s]      two ping-pong buffers; u_{n+1} overwrites u_{n-1}
+//   Kval   [nnzb][9][n_s]   9 = (c, d) of the 3x3 node block, row-major
+//   c1     [V][n_s]         (+ c2a, c3a [V][n_s] for damping = IDENTITY)
+//   alpha  [F][n_s], Khat [F][81], etri [F][3] (RCM ids)
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime_api.h>
+
+namespace ens {
+
+constexpr int kMaxFields = 4;
+
+struct StepArgs {
+    int64_t V = 0;            // rows handled by this launch: rows [row0, row0 + V)
+    int64_t row0 = 0;
+    int64_t V_total = 0;      // rows of the state arrays (owned + ghost)
+    int32_t n_s = 0;
+    const int32_t* row_ptr = nullptr;   // [V_total + 1] (int32: nnzb < 2^31)
+    const int32_t* col = nullptr;
+    const double* Kval = nullptr;
+    // matrix-free operands
+    const int32_t* inc_ptr = nullptr;   // [V + 1] incidences of each row, ascending element
+    const int32_t* inc = nullptr;       // element * 4 + local index
+    const int32_t* etri = nullptr;      // [F][3] RCM node ids
+    const double* Khat = nullptr;       // [F][81]
+    const double* alpha = nullptr;      // [F][n_s]
+    // update coefficients
+    const double* c1 = nullptr;
+    const double* c2a = nullptr;        // null => scalars c2, c3
+    const double* c3a = nullptr;
+    double c2 = 2.0, c3 = 1.0;
+    const uint8_t* fixed = nullptr;     // [V_total]
+    // load f(t) = ramp(t) sum_k g_k(t) F_k
+    int32_t n_fields = 0;
+    const double* Fk = nullptr;         // [n_fields][V_total][3]
+    int32_t n_tab = 0;
+    const double* tab_t = nullptr;      // device [n_tab]
+    const double* tab_g = nullptr;      // device [n_fields][n_tab]
+    double period = 0.0, ramp_T = 0.0, dt = 0.0;
+    // time index: step = *step_base + step_off; u_n = buf[step & 1]
+    const int64_t* step_base = nullptr;
+    int64_t step_off = 0;
+    double* ubuf0 = nullptr;
+    double* ubuf1 = nullptr;
+    unsigned long long* flag = nullptr; // min over (step << 24 | s) of non-finite results
+    int32_t s_global0 = 0;
+    // diagnostic mode: y = K u_n written to y_out ([V][3][n_s]), no update
+    double* y_out = nullptr;
+};
+
+// Fused step (S2 load + S3 ensemble SpMM + S4 central-difference update) on the
+// assembled values: one launch advances rows [row0, row0+V) by one step.
+cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st);
+// Same on the matrix-free element form (alpha_{e,s} K^_e gathered per node).
+cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st);
+// *step_base += n (after n steps were enqueued)
+cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st);
+
+// F0: Kval[b][k][s] = sum_{(e, a, b') in contrib[b]} alpha[e][s] Khat[e][3a+c][3b'+d]
+cudaError_t launch_assemble(int64_t nnzb, int32_t n_s, const int32_t* contrib_ptr, const int32_t* contrib,
+                            const double* alpha, const double* Khat, double* Kval, cudaStream_t st);
+
+// F4: ABI [n_s][V][3] (caller numbering) <-> device [V][3][n_s] (RCM numbering)
+cudaError_t launch_abi_to_dev(int64_t V, int32_t n_s, const int32_t* perm, const double* src, double* dst,
+                              cudaStream_t st);
+cudaError_t launch_dev_to_abi(int64_t V, int32_t n_s, const int32_t* perm, const double* src, double* dst,
+                              cudaStream_t st);
+
+}  // namespace ens

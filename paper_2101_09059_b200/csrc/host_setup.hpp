@@ -1,0 +1,52 @@
+// host_setup.hpp -- one-time host setup of the ensemble shell solver (C++17).
+//
+// Everything the north star lists under "Host setup (done once)": mesh validation,
+// mesh -> block-CSR pattern with RCM reordering, element stiffness K^_e, Gauss-point
+// material scaling alpha_{e,s}, lumped mass, CFL step, node partition / halo maps.
+// Independent of oracle/ (no shared code); integer maps are specified exactly in
+// DESIGN.md "Pattern" so both reach the same bits.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace ens {
+
+struct MeshView {
+    int64_t V = 0, F = 0;
+    const double* xyz = nullptr;    // [V][3]
+    const int32_t* tris = nullptr;  // [F][3]
+};
+
+// 0 ok; 1 index out of range; 2 repeated node; 3 degenerate; 4 edge shared by > 2 triangles.
+int validate_mesh(const MeshView& m, int64_t* bad);
+
+struct Pattern {
+    std::vector<int32_t> perm;      // perm[new] = old
+    std::vector<int32_t> iperm;     // iperm[old] = new
+    std::vector<int64_t> row_ptr;   // [V+1], RCM order
+    std::vector<int32_t> col;       // [nnzb], ascending per row, diagonal included
+    int32_t bandwidth = 0;
+};
+
+// Neighbour lists (sorted, unique, no self) of the triangulation's edge graph.
+void edge_graph(const MeshView& m, std::vector<int64_t>& ptr, std::vector<int32_t>& adj);
+std::vector<int32_t> rcm_order(int64_t V, const std::vector<int64_t>& ptr, const std::vector<int32_t>& adj);
+Pattern build_pattern(const MeshView& m);
+
+// K^_e for E = 1 and unit thickness in the global frame (81 doubles) + area.
+void element_stiffness(const double* X1, const double* X2, const double* X3, double nu,
+                       double k_shear, double* Khat, double* area);
+
+// alpha[s][e] (closed form of the 3-point Gauss rule on P1 fields), mass[s][v], CFL dt.
+void materials(const MeshView& m, int32_t n_s, const double* E, const double* h, double rho,
+               double* alpha, double* mass);
+double cfl_dt(const MeshView& m, int32_t n_s, const double* E, double rho, double safety);
+
+// Node partition of the RCM rows balanced by blocks, and ghost rows.
+std::vector<int64_t> partition_bounds(const std::vector<int64_t>& row_ptr, int32_t P);
+std::vector<int32_t> ghost_rows(const std::vector<int64_t>& row_ptr, const std::vector<int32_t>& col,
+                                int64_t lo, int64_t hi);
+
+}  // namespace ens

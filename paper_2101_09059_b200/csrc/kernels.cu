@@ -1,0 +1,426 @@
+// kernels.cu -- sm_100a kernels of the ensemble explicit shell step (arXiv 2101.09059).
+//
+// Hot path (north star): r = f_ext - K(theta_s) u_s over N_s realisations, fused with the
+// central-difference update (Eq. 22).  fp64 throughout, CUDA cores:
+// this is a sparse streaming product, not a dense contraction, so no tensor cores.
+//
+// Thread mapping (assembled kernel): thread = (row i, realisation group g), VEC
+// consecutive realisations per thread, groups of one row on consecutive lanes, so that
+// every (block, entry) segment Kval[b][k][0..n_s) — n_s*8 contiguous bytes — is read by
+// consecutive lanes with 16 B (VEC = 2) or 32 B (VEC = 4) vector loads.  Each thread
+// accumulates its realisations sequentially in CSR block order then d = 0,1,2 with explicit
+// fma(): the per-realisation arithmetic is identical whatever N_s, VEC or the launch
+// geometry, which makes ensemble runs bit-identical to single-realisation runs.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device.hpp"
+
+namespace ens {
+namespace {
+
+constexpr int kThreads = 256;
+
+struct d4 { double x, y, z, w; };
+
+template <int VEC> struct Vec;
+template <> struct Vec<1> { double v[1]; };
+template <> struct Vec<2> { double v[2]; };
+template <> struct Vec<4> { double v[4]; };
+
+// ---- loads -----------------------------------------------------------------------------
+// Kval is streamed exactly once per step: no L1 allocation, L2 evict-first (createpolicy /
+// the 256-bit EFL2 form), so the u_n gather working set stays resident in the 126 MB L2.
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ld_stream(const double* p, uint64_t pol);
+
+template <>
+__device__ __forceinline__ Vec<1> ld_stream<1>(const double* p, uint64_t pol) {
+    Vec<1> r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(r.v[0]) : "l"(p), "l"(pol));
+    return r;
+}
+template <>
+__device__ __forceinline__ Vec<2> ld_stream<2>(const double* p, uint64_t pol) {
+    Vec<2> r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p), "l"(pol));
+    return r;
+}
+template <>
+__device__ __forceinline__ Vec<4> ld_stream<4>(const double* p, uint64_t) {
+    Vec<4> r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
+    return r;
+}
+
+// u_n and the coefficient arrays: read-only within a launch, re-used across rows via L1/L2.
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ld_ro(const double* p) {
+    Vec<VEC> r;
+    if constexpr (VEC == 1) {
+        r.v[0] = __ldg(p);
+    } else if constexpr (VEC == 2) {
+        double2 t = __ldg(reinterpret_cast<const double2*>(p));
+        r.v[0] = t.x; r.v[1] = t.y;
+    } else {
+        asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                     : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
+    }
+    return r;
+}
+
+// u_{n-1}: read then overwritten in place by the same thread (plain coherent accesses).
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ld_rw(const double* p) {
+    Vec<VEC> r;
+    if constexpr (VEC == 1) {
+        r.v[0] = *p;
+    } else if constexpr (VEC == 2) {
+        double2 t = *reinterpret_cast<const double2*>(p);
+        r.v[0] = t.x; r.v[1] = t.y;
+    } else {
+        asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+                     : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
+    }
+    return r;
+}
+
+template <int VEC>
+__device__ __forceinline__ void st_vec(double* p, const Vec<VEC>& x) {
+    if constexpr (VEC == 1) {
+        *p = x.v[0];
+    } else if constexpr (VEC == 2) {
+        *reinterpret_cast<double2*>(p) = make_double2(x.v[0], x.v[1]);
+    } else {
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};"
+                     :: "l"(p), "d"(x.v[0]), "d"(x.v[1]), "d"(x.v[2]), "d"(x.v[3]) : "memory");
+    }
+}
+
+// ---- load coefficients coef_k = ramp(t) g_k(t)  (ens_set_traction contract) ------------
+__device__ void load_coeffs(const StepArgs& a, double t, double* coef) {
+    double ramp = 1.0;
+    if (a.ramp_T > 0.0 && t < a.ramp_T) ramp = sin(3.141592653589793 * t / (2.0 * a.ramp_T));
+    double tau = t;
+    if (a.period > 0.0) tau = t - a.period * floor(t / a.period);
+    for (int k = 0; k < a.n_fields; ++k) {
+        double g = 1.0;
+        if (a.n_tab > 0) {
+            const double* G = a.tab_g + int64_t(k) * a.n_tab;
+            if (tau <= a.tab_t[0]) {
+                g = G[0];
+            } else if (tau >= a.tab_t[a.n_tab - 1]) {
+                g = G[a.n_tab - 1];
+            } else {
+                int lo = 0, hi = a.n_tab - 1;          // tab_t[lo] <= tau < tab_t[hi]
+                while (hi - lo > 1) {
+                    int mid = (lo + hi) >> 1;
+                    if (a.tab_t[mid] <= tau) lo = mid; else hi = mid;
+                }
+                g = G[lo] + (G[lo + 1] - G[lo]) * (tau - a.tab_t[lo]) / (a.tab_t[lo + 1] - a.tab_t[lo]);
+            }
+        }
+        coef[k] = ramp * g;
+    }
+}
+
+struct StepCtx {
+    int64_t step;
+    const double* un;
+    double* uo;       // u_{n-1} in, u_{n+1} out
+};
+
+__device__ __forceinline__ StepCtx step_ctx(const StepArgs& a) {
+    StepCtx c;
+    c.step = *a.step_base + a.step_off;
+    c.un = (c.step & 1) ? a.ubuf1 : a.ubuf0;
+    c.uo = (c.step & 1) ? a.ubuf0 : a.ubuf1;
+    return c;
+}
+
+// S2 + S4: r = f - y; u_{n+1} = c1 r + c2 u_n - c3 u_{n-1}; Dirichlet; non-finite flag.
+template <int VEC>
+__device__ __forceinline__ void cd_update(const StepArgs& a, const StepCtx& sc, const double* coef,
+                                          int64_t i, int s0, const double (&y)[3][VEC]) {
+    const int n_s = a.n_s;
+    const uint8_t fx = a.fixed ? __ldg(a.fixed + i) : uint8_t(0);
+    Vec<VEC> c1 = ld_ro<VEC>(a.c1 + i * n_s + s0);
+    Vec<VEC> c2, c3;
+    if (a.c2a) {
+        c2 = ld_ro<VEC>(a.c2a + i * n_s + s0);
+        c3 = ld_ro<VEC>(a.c3a + i * n_s + s0);
+    } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) { c2.v[v] = a.c2; c3.v[v] = a.c3; }
+    }
+    unsigned bad = 0;   // bit v: realisation s0 + v produced a non-finite value
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double f = 0.0;
+        for (int k = 0; k < a.n_fields; ++k) f = fma(coef[k], __ldg(a.Fk + (int64_t(k) * a.V_total + i) * 3 + c), f);
+        const int64_t off = (i * 3 + c) * n_s + s0;
+        Vec<VEC> un = ld_ro<VEC>(sc.un + off);
+        Vec<VEC> uo = ld_rw<VEC>(sc.uo + off);
+        Vec<VEC> out;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            double r = f - y[c][v];
+            double t = fma(c2.v[v], un.v[v], -(c3.v[v] * uo.v[v]));
+            double w = fma(c1.v[v], r, t);
+            if ((fx >> c) & 1) w = 0.0;
+            bad |= unsigned(!isfinite(w)) << v;
+            out.v[v] = w;
+        }
+        st_vec<VEC>(sc.uo + off, out);
+    }
+    if (bad) {
+        for (int v = 0; v < VEC; ++v)
+            if ((bad >> v) & 1) {
+                unsigned long long code = (unsigned long long)(sc.step) << 24 | (unsigned long long)(a.s_global0 + s0 + v);
+                atomicMin(a.flag, code);
+            }
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void store_y(const StepArgs& a, int64_t i, int s0, const double (&y)[3][VEC]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        Vec<VEC> o;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) o.v[v] = y[c][v];
+        st_vec<VEC>(a.y_out + (i * 3 + c) * a.n_s + s0, o);
+    }
+}
+
+// ---- F1: fused step on the assembled per-realisation block values ----------------------
+template <int VEC, bool APPLY>
+__global__ void __launch_bounds__(kThreads)
+k_step_assembled(const StepArgs a) {
+    __shared__ double s_coef[kMaxFields];
+    const StepCtx sc = step_ctx(a);
+    if (!APPLY && threadIdx.x == 0) load_coeffs(a, double(sc.step) * a.dt, s_coef);
+    if (!APPLY) __syncthreads();
+
+    const int P = a.n_s / VEC;                       // realisation groups per row
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= a.V * P) return;
+    const int64_t i = a.row0 + tid / P;
+    const int s0 = int(tid % P) * VEC;
+    const int n_s = a.n_s;
+
+    uint64_t pol = 0;
+    if constexpr (VEC < 4) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+
+    double y[3][VEC];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) y[c][v] = 0.0;
+
+    const int32_t b_end = __ldg(a.row_ptr + i + 1);
+#pragma unroll 2
+    for (int32_t b = __ldg(a.row_ptr + i); b < b_end; ++b) {
+        const int64_t j = __ldg(a.col + b);
+        const double* kp = a.Kval + int64_t(b) * 9 * n_s + s0;
+        const double* up = sc.un + j * 3 * n_s + s0;
+        Vec<VEC> u[3], k[9];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) u[d] = ld_ro<VEC>(up + d * n_s);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) k[e] = ld_stream<VEC>(kp + e * n_s, pol);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) y[c][v] = fma(k[3 * c + d].v[v], u[d].v[v], y[c][v]);
+    }
+    if constexpr (APPLY) store_y<VEC>(a, i, s0, y);
+    else cd_update<VEC>(a, sc, s_coef, i, s0, y);
+}
+
+// ---- F2: fused step on the matrix-free element form ------------------------------------
+// y[i][c][s] = sum_{(e, a) incident to i, ascending e} alpha[e][s] * sum_{b, d}
+//              Khat[e][3a+c][3b+d] u[etri[e][b]][d][s]
+template <int VEC, bool APPLY>
+__global__ void __launch_bounds__(kThreads)
+k_step_matrix_free(const StepArgs a) {
+    __shared__ double s_coef[kMaxFields];
+    const StepCtx sc = step_ctx(a);
+    if (!APPLY && threadIdx.x == 0) load_coeffs(a, double(sc.step) * a.dt, s_coef);
+    if (!APPLY) __syncthreads();
+
+    const int P = a.n_s / VEC;
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= a.V * P) return;
+    const int64_t i = a.row0 + tid / P;
+    const int s0 = int(tid % P) * VEC;
+    const int n_s = a.n_s;
+
+    double y[3][VEC];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) y[c][v] = 0.0;
+
+    const int32_t k_end = __ldg(a.inc_ptr + i + 1);
+    for (int32_t k = __ldg(a.inc_ptr + i); k < k_end; ++k) {
+        const int32_t code = __ldg(a.inc + k);
+        const int64_t e = code >> 2;
+        const int la = code & 3;
+        const double* Kh = a.Khat + e * 81 + 27 * la;
+        Vec<VEC> al = ld_ro<VEC>(a.alpha + e * n_s + s0);
+        double t[3][VEC];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) t[c][v] = 0.0;
+#pragma unroll
+        for (int nb = 0; nb < 3; ++nb) {
+            const int64_t node = __ldg(a.etri + e * 3 + nb);
+            Vec<VEC> u[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) u[d] = ld_ro<VEC>(sc.un + (node * 3 + d) * n_s + s0);
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const double kv = __ldg(Kh + 9 * c + 3 * nb + d);
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) t[c][v] = fma(kv, u[d].v[v], t[c][v]);
+                }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) y[c][v] = fma(al.v[v], t[c][v], y[c][v]);
+    }
+    if constexpr (APPLY) store_y<VEC>(a, i, s0, y);
+    else cd_update<VEC>(a, sc, s_coef, i, s0, y);
+}
+
+__global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
+
+// ---- F0: device assembly of the per-realisation block values ---------------------------
+__global__ void __launch_bounds__(kThreads)
+k_assemble(int64_t nnzb, int32_t n_s, const int32_t* __restrict__ cptr, const int32_t* __restrict__ contrib,
+           const double* __restrict__ alpha, const double* __restrict__ Khat, double* __restrict__ Kval) {
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= nnzb * n_s) return;
+    const int64_t b = tid / n_s;
+    const int s = int(tid % n_s);
+    double acc[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc[k] = 0.0;
+    for (int32_t q = cptr[b]; q < cptr[b + 1]; ++q) {
+        const int32_t code = contrib[q];
+        const int64_t e = code / 9;
+        const int ab = code % 9, la = ab / 3, lb = ab % 3;
+        const double al = alpha[e * n_s + s];
+        const double* K = Khat + e * 81;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) acc[3 * c + d] = fma(al, K[9 * (3 * la + c) + 3 * lb + d], acc[3 * c + d]);
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Kval[(b * 9 + k) * n_s + s] = acc[k];
+}
+
+// ---- F4: layout transposes (ABI <-> device), off the hot path --------------------------
+__global__ void k_abi_to_dev(int64_t V, int32_t n_s, const int32_t* __restrict__ perm,
+                             const double* __restrict__ src, double* __restrict__ dst) {
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= V * 3 * n_s) return;
+    const int s = int(tid % n_s);
+    const int64_t ic = tid / n_s;
+    const int64_t i = ic / 3;
+    const int c = int(ic % 3);
+    dst[tid] = src[(int64_t(s) * V + perm[i]) * 3 + c];
+}
+
+__global__ void k_dev_to_abi(int64_t V, int32_t n_s, const int32_t* __restrict__ perm,
+                             const double* __restrict__ src, double* __restrict__ dst) {
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= V * 3 * n_s) return;
+    const int s = int(tid % n_s);
+    const int64_t ic = tid / n_s;
+    const int64_t i = ic / 3;
+    const int c = int(ic % 3);
+    dst[(int64_t(s) * V + perm[i]) * 3 + c] = src[tid];
+}
+
+inline unsigned grid_for(int64_t n) { return unsigned((n + kThreads - 1) / kThreads); }
+
+}  // namespace
+
+template <int VEC, bool APPLY>
+static cudaError_t launch_a1(const StepArgs& a, cudaStream_t st) {
+    const int64_t n = a.V * (a.n_s / VEC);
+    if (n == 0) return cudaSuccess;
+    k_step_assembled<VEC, APPLY><<<grid_for(n), kThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int VEC, bool APPLY>
+static cudaError_t launch_a2(const StepArgs& a, cudaStream_t st) {
+    const int64_t n = a.V * (a.n_s / VEC);
+    if (n == 0) return cudaSuccess;
+    k_step_matrix_free<VEC, APPLY><<<grid_for(n), kThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+static int pick_vec(int32_t n_s) { return (n_s % 4 == 0 && n_s >= 128) ? 4 : (n_s % 2 == 0 ? 2 : 1); }
+
+cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st) {
+    const bool apply = a.y_out != nullptr;
+    switch (pick_vec(a.n_s)) {
+        case 4: return apply ? launch_a1<4, true>(a, st) : launch_a1<4, false>(a, st);
+        case 2: return apply ? launch_a1<2, true>(a, st) : launch_a1<2, false>(a, st);
+        default: return apply ? launch_a1<1, true>(a, st) : launch_a1<1, false>(a, st);
+    }
+}
+
+cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
+    const bool apply = a.y_out != nullptr;
+    switch (pick_vec(a.n_s)) {
+        case 4: return apply ? launch_a2<4, true>(a, st) : launch_a2<4, false>(a, st);
+        case 2: return apply ? launch_a2<2, true>(a, st) : launch_a2<2, false>(a, st);
+        default: return apply ? launch_a2<1, true>(a, st) : launch_a2<1, false>(a, st);
+    }
+}
+
+cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st) {
+    k_advance<<<1, 1, 0, st>>>(step_base, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_assemble(int64_t nnzb, int32_t n_s, const int32_t* contrib_ptr, const int32_t* contrib,
+                            const double* alpha, const double* Khat, double* Kval, cudaStream_t st) {
+    const int64_t n = nnzb * n_s;
+    if (n == 0) return cudaSuccess;
+    k_assemble<<<grid_for(n), kThreads, 0, st>>>(nnzb, n_s, contrib_ptr, contrib, alpha, Khat, Kval);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_abi_to_dev(int64_t V, int32_t n_s, const int32_t* perm, const double* src, double* dst,
+                              cudaStream_t st) {
+    const int64_t n = V * 3 * n_s;
+    if (n == 0) return cudaSuccess;
+    k_abi_to_dev<<<grid_for(n), kThreads, 0, st>>>(V, n_s, perm, src, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dev_to_abi(int64_t V, int32_t n_s, const int32_t* perm, const double* src, double* dst,
+                              cudaStream_t st) {
+    const int64_t n = V * 3 * n_s;
+    if (n == 0) return cudaSuccess;
+    k_dev_to_abi<<<grid_for(n), kThreads, 0, st>>>(V, n_s, perm, src, dst);
+    return cudaGetLastError();
+}
+
+}  // namespace ens

@@ -1,0 +1,247 @@
+"""Python binding of the C ABI (include/ens.h): argument marshalling only.
+
+Every step of the hot path runs in libens.so's sm_100a kernels.  PyTorch supplies the
+device memory (its caching allocator, through the ABI's dev_alloc/dev_free callbacks)
+and the CUDA stream; nothing here computes any part of the method.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _ffi
+from ._ffi import EnsError, check, lib
+
+DAMPING = {"none": 0, "mass": 1, "identity": 2, 0: 0, 1: 1, 2: 2}
+KERNEL = {"assembled": 0, "matrix_free": 1, 0: 0, 1: 1}
+DIST = {"single": 0, "node": 1, "ensemble": 2, 0: 0, 1: 1, 2: 2}
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class _TorchAllocator:
+    """dev_alloc / dev_free callbacks backed by torch's CUDA caching allocator."""
+
+    def __init__(self, device):
+        import torch
+        self.torch = torch
+        self.device = device
+        self.live = {}
+        self.alloc_cb = _ffi.DEV_ALLOC(self._alloc)
+        self.free_cb = _ffi.DEV_FREE(self._free)
+
+    def _alloc(self, nbytes, _user):
+        try:
+            t = self.torch.empty(int(nbytes), dtype=self.torch.uint8, device=self.device)
+        except Exception:     # OOM -> NULL -> ENS_E_OOM
+            return None
+        self.live[t.data_ptr()] = t
+        return t.data_ptr()
+
+    def _free(self, ptr, _user):
+        self.live.pop(ptr, None)
+
+
+class Ensemble:
+    """N_s realisations of the wall, advanced together by the fused sm_100a step.
+
+    Arrays crossing this API are realisation-outermost in the caller's node numbering:
+    E, h: [n_s][V]; u: [n_s][V][3]; F: [K][V][3].
+    """
+
+    def __init__(self, xyz, tris, fixed, E, h, *, rho, nu, k_shear=5.0 / 6.0, dt=0.0,
+                 cfl_safety=0.9, c_d=0.0, damping="none", kernel="assembled", dist="single",
+                 s_begin=0, rank=0, world=1, device=None, stream=None, torch_alloc=True,
+                 _ctx=None):
+        self._ctx = None
+        self._alloc = None
+        if _ctx is not None:                      # from_csr
+            self._ctx, self._alloc, self.n_s, self.V = _ctx
+            return
+        xyz, tris = _c(xyz, np.float64), _c(tris, np.int32)
+        E, h = _c(E, np.float64), _c(h, np.float64)
+        fixed = None if fixed is None else _c(fixed, np.uint8)
+        self.V, self.n_s = xyz.shape[0], E.shape[0]
+        mesh = _ffi.EnsMesh(self.V, tris.shape[0], _p(xyz), _p(tris), _p(fixed))
+        mat = _ffi.EnsMaterials(self.n_s, _p(E), _p(h), rho, nu, k_shear, s_begin)
+        opt, self._alloc = _options(dt, cfl_safety, c_d, damping, kernel, dist, rank, world,
+                                    device, stream, torch_alloc)
+        ctx = C.c_void_p()
+        check(lib().ens_create(C.byref(mesh), C.byref(mat), C.byref(opt), C.byref(ctx)))
+        self._ctx = ctx
+
+    @classmethod
+    def from_csr(cls, row_ptr, col, Kval, c1, c2, c3, fixed=None, dt=1.0, *, device=None,
+                 stream=None, torch_alloc=True):
+        """Test-only: synthetic operator (ens_create_csr).  Kval [n_s][nnzb][9], c* [n_s][V]."""
+        row_ptr, col = _c(row_ptr, np.int64), _c(col, np.int32)
+        Kval = _c(Kval, np.float64)
+        c1, c2, c3 = _c(c1, np.float64), _c(c2, np.float64), _c(c3, np.float64)
+        fixed = None if fixed is None else _c(fixed, np.uint8)
+        V, n_s = len(row_ptr) - 1, Kval.shape[0]
+        opt, alloc = _options(dt, 0.9, 0.0, 0, 0, 0, 0, 1, device, stream, torch_alloc)
+        ctx = C.c_void_p()
+        check(lib().ens_create_csr(V, _p(row_ptr), _p(col), n_s, _p(Kval), _p(c1), _p(c2), _p(c3),
+                                   _p(fixed), float(dt), C.byref(opt), C.byref(ctx)))
+        return cls(None, None, None, None, None, rho=0, nu=0, _ctx=(ctx, alloc, n_s, V))
+
+    # ---- lifecycle ------------------------------------------------------------------
+    def close(self):
+        if self._ctx:
+            lib().ens_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- the ABI calls --------------------------------------------------------------
+    def set_traction(self, F, tab_t=None, tab_g=None, period=0.0, ramp_T=0.0):
+        F = _c(F, np.float64)
+        K = F.shape[0]
+        tab_t = np.zeros(0) if tab_t is None else _c(tab_t, np.float64)
+        tab_g = np.zeros((K, 0)) if tab_g is None else _c(tab_g, np.float64)
+        check(lib().ens_set_traction(self._ctx, K, _p(F), len(tab_t), _p(tab_t), _p(tab_g),
+                                     float(period), float(ramp_T)), self._ctx)
+
+    def step(self, n: int = 1):
+        check(lib().ens_step(self._ctx, int(n)), self._ctx)
+
+    def sync(self):
+        check(lib().ens_sync(self._ctx), self._ctx)
+
+    def get_state(self, u_n=None, u_nm1=None, want_prev=True):
+        """Returns (u_n, u_nm1, t, step); fills the given host buffers if provided."""
+        shape = (self.n_s, self.V, 3)
+        if u_n is None:
+            u_n = np.empty(shape)
+        if want_prev and u_nm1 is None:
+            u_nm1 = np.empty(shape)
+        t = C.c_double()
+        st = C.c_int64()
+        check(lib().ens_get_state(self._ctx, _ptr(u_n), _ptr(u_nm1), C.byref(t), C.byref(st)), self._ctx)
+        return u_n, u_nm1, t.value, st.value
+
+    def set_state(self, u_n=None, u_nm1=None, step=0):
+        u_n = None if u_n is None else _c(u_n, np.float64)
+        u_nm1 = None if u_nm1 is None else _c(u_nm1, np.float64)
+        check(lib().ens_set_state(self._ctx, _p(u_n), _p(u_nm1), 0.0, int(step)), self._ctx)
+
+    def apply_stiffness(self, u):
+        u = _c(u, np.float64)
+        y = np.empty_like(u)
+        check(lib().ens_apply_stiffness(self._ctx, _p(u), _p(y)), self._ctx)
+        return y
+
+    def info(self) -> dict:
+        inf = _ffi.EnsInfo()
+        check(lib().ens_query(self._ctx, C.byref(inf)), self._ctx)
+        return {k: getattr(inf, k) for k, _ in _ffi.EnsInfo._fields_}
+
+
+def _ptr(a):
+    """Host pointer of a numpy array or a (pinned) CPU torch tensor."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags.c_contiguous and a.dtype == np.float64
+        return a.ctypes.data_as(C.c_void_p)
+    assert a.is_contiguous() and a.device.type == "cpu"
+    return C.c_void_p(a.data_ptr())
+
+
+def _options(dt, cfl_safety, c_d, damping, kernel, dist, rank, world, device, stream, torch_alloc):
+    opt = _ffi.EnsOptions()
+    opt.dt = float(dt or 0.0)
+    opt.cfl_safety = float(cfl_safety)
+    opt.c_d = float(c_d)
+    opt.damping = DAMPING[damping]
+    opt.kernel = KERNEL[kernel]
+    opt.dist = DIST[dist]
+    opt.rank, opt.world = int(rank), int(world)
+    opt.device = -1 if device is None else int(device)
+    alloc = None
+    if stream is not None:
+        opt.stream = C.c_void_p(int(stream))
+    if torch_alloc:
+        import torch
+        if torch.cuda.is_available():
+            dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+            if stream is None:
+                opt.stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+            alloc = _TorchAllocator(dev)
+            opt.dev_alloc = alloc.alloc_cb
+            opt.dev_free = alloc.free_cb
+    return opt, alloc
+
+
+# ---- host-side maps (no GPU) ----------------------------------------------------------
+
+def host_validate(xyz, tris):
+    xyz, tris = _c(xyz, np.float64), _c(tris, np.int32)
+    code, bad = C.c_int32(), C.c_int64()
+    lib().ens_host_validate(xyz.shape[0], tris.shape[0], _p(xyz), _p(tris), C.byref(code), C.byref(bad))
+    return code.value, bad.value
+
+
+def host_pattern(V, tris):
+    """(perm, row_ptr, col) exactly as ens_create builds them."""
+    tris = _c(tris, np.int32)
+    perm = np.zeros(V, np.int32)
+    row_ptr = np.zeros(V + 1, np.int64)
+    cap = V + 6 * tris.shape[0]
+    col = np.zeros(cap, np.int32)
+    n = C.c_int64()
+    check(lib().ens_host_pattern(V, tris.shape[0], _p(tris), _p(perm), _p(row_ptr), _p(col), cap, C.byref(n)))
+    return perm, row_ptr, col[:n.value].copy()
+
+
+def host_partition(row_ptr, P):
+    row_ptr = _c(row_ptr, np.int64)
+    b = np.zeros(P + 1, np.int64)
+    check(lib().ens_host_partition(len(row_ptr) - 1, _p(row_ptr), P, _p(b)))
+    return b
+
+
+def host_ghosts(row_ptr, col, lo, hi):
+    row_ptr, col = _c(row_ptr, np.int64), _c(col, np.int32)
+    V = len(row_ptr) - 1
+    g = np.zeros(V, np.int32)
+    n = C.c_int64()
+    check(lib().ens_host_ghosts(V, _p(row_ptr), _p(col), int(lo), int(hi), _p(g), V, C.byref(n)))
+    return g[:n.value].copy()
+
+
+def host_element_stiffness(xyz, tris, nu, k_shear):
+    xyz, tris = _c(xyz, np.float64), _c(tris, np.int32)
+    F = tris.shape[0]
+    K = np.zeros((F, 9, 9))
+    A = np.zeros(F)
+    check(lib().ens_host_element_stiffness(xyz.shape[0], F, _p(xyz), _p(tris), nu, k_shear, _p(K), _p(A)))
+    return K, A
+
+
+def host_materials(xyz, tris, E, h, rho, cfl_safety=0.9):
+    xyz, tris, E, h = _c(xyz, np.float64), _c(tris, np.int32), _c(E, np.float64), _c(h, np.float64)
+    n_s, V, F = E.shape[0], xyz.shape[0], tris.shape[0]
+    alpha = np.zeros((n_s, F))
+    mass = np.zeros((n_s, V))
+    dt = C.c_double()
+    check(lib().ens_host_materials(V, F, _p(xyz), _p(tris), n_s, _p(E), _p(h), rho, cfl_safety,
+                                   _p(alpha), _p(mass), C.byref(dt)))
+    return alpha, mass, dt.value

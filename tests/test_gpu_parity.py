@@ -1,0 +1,247 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, on a B200 (-m gpu).
+
+Tolerances (north star): one SpMM <= 1e-12 relative L2 and
+|dy| <= 4 nnz_row eps (|K||u|) per entry; displacement after 10^4 steps <= 1e-9
+relative L2; ensemble equivalence, Dirichlet zeros, state round trips: bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+import oracle
+from paper_2101_09059_b200 import solver
+from paper_2101_09059_b200._ffi import ENS_E_DIVERGED, ENS_E_STATE, EnsError
+from paper_2101_09059_b200.inputs import configs, fields, loads, mesh as meshmod
+
+pytestmark = pytest.mark.gpu
+EPS = np.finfo(np.float64).eps
+RHO, NU, KS = 1.06, 0.5, 5.0 / 6.0
+
+
+def _mats(m, n_s, seed, s_begin=0):
+    E, h, _ = fields.sample_materials(m.xyz, m.tris, n_s, E_mean=7e6, E_std=7e5, h_mean=0.4,
+                                      h_std=0.04, rho_corr=3.7, seed=seed, s_begin=s_begin)
+    return E, h
+
+
+def _pair(m, E, h, kernel="assembled", **kw):
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, kernel=kernel, **kw)
+    om = oracle.OracleModel(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS,
+                            damping=solver.DAMPING[kw.get("damping", 0)], c_d=kw.get("c_d", 0.0),
+                            dt=ens.info()["dt"])
+    return ens, om
+
+
+def _check_spmm(ens, om, u):
+    y = ens.apply_stiffness(u)
+    yo = om.spmm(u)
+    assert np.linalg.norm(y - yo) <= 1e-12 * np.linalg.norm(yo)
+    # per entry: 4 * nnz_row * eps * (|K| |u|)_i
+    absKu = oracle.spmm(om.row_ptr, om.col, np.abs(om.Kval), np.abs(u))
+    nnz_row = np.diff(om.row_ptr).max() * 3
+    assert np.all(np.abs(y - yo) <= 4 * nnz_row * EPS * absKu + 1e-300)
+
+
+@pytest.mark.parametrize("kernel", ["assembled", "matrix_free"])
+@pytest.mark.parametrize("n_s", [1, 3, 4, 6, 64, 128])
+def test_spmm_parity(kernel, n_s):
+    """Several tiles and a ragged tail: 40 x 51 rings, V = 2,040, N_s odd/even/x4."""
+    m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(40, 51), 0.02, 1), 1)
+    E, h = _mats(m, n_s, 11)
+    ens, om = _pair(m, E, h, kernel=kernel)
+    rng = np.random.default_rng(n_s)
+    _check_spmm(ens, om, rng.uniform(-1, 1, (n_s, m.n_nodes, 3)))
+    ens.close()
+
+
+def _crit_dt(om):
+    """Exact stability threshold 2 / sqrt(lambda_max(M^-1/2 K_ff M^-1/2)), min over s."""
+    free = np.repeat(om.fixed == 0, 3)
+    best = np.inf
+    for s in range(om.n_s):
+        K = om.K_sparse(s).toarray()[np.ix_(free, free)]
+        d = 1.0 / np.sqrt(np.repeat(om.m[s], 3)[free])
+        lam = sla.eigvalsh(d[:, None] * K * d[None, :], subset_by_index=[K.shape[0] - 1, K.shape[0] - 1])
+        best = min(best, 2.0 / math.sqrt(lam[-1]))
+    return best
+
+
+def test_c1_1e4_steps_parity():
+    """Config c1 (12 x 23 rings, N_s = 4, steady 13 mmHg, undamped), 10^4 steps at
+    0.9 dt_crit: relative L2 <= 1e-9 at step 10^4."""
+    cfg = configs.make("c1")
+    m = cfg.mesh
+    om0 = oracle.OracleModel(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS)
+    dt = 0.9 * _crit_dt(om0)
+    ens, om = _pair(m, cfg.E, cfg.h, dt=dt)
+    tr = cfg.traction
+    ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    om.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    for chunk in (1, 99, 900, 9000):
+        ens.step(chunk)
+        om.run(chunk)
+        u, up, t, step = ens.get_state()
+        assert step == om.step
+        for a, b in ((u, om.u_n), (up, om.u_nm1)):
+            assert np.linalg.norm(a - b) <= 1e-9 * np.linalg.norm(b)
+    assert t == pytest.approx(1e4 * dt, rel=1e-15)
+    ens.close()
+
+
+@pytest.mark.parametrize("damping,c_d", [("mass", 250.0), ("identity", 0.5)])
+def test_pulsatile_damped_parity(damping, c_d):
+    """Pulsatile table + sine ramp + period wrap + both damping forms, 3,000 steps."""
+    m = meshmod.cylinder(16, 31)
+    E, h = _mats(m, 6, 21)
+    tr = loads.pulsatile(m.xyz, m.tris, period=0.05, systole=0.02, n_tab=51, ramp_T=0.03)
+    ens, om = _pair(m, E, h, damping=damping, c_d=c_d)
+    ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    om.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    ens.step(3000)
+    om.run(3000)
+    u, up, _, _ = ens.get_state()
+    assert np.linalg.norm(u - om.u_n) <= 1e-9 * np.linalg.norm(om.u_n)
+    ens.close()
+
+
+@pytest.mark.parametrize("kernel", ["assembled", "matrix_free"])
+def test_ensemble_equivalence_bitexact(kernel):
+    """N_s = 8 together (VEC = 2 lanes) == each realisation alone (VEC = 1): bit for bit."""
+    m = meshmod.cylinder(24, 40)
+    E, h = _mats(m, 8, 31)
+    tr = loads.pulsatile(m.xyz, m.tris, period=0.01, systole=0.004, ramp_T=0.003)
+    kw = dict(rho=RHO, nu=NU, k_shear=KS, kernel=kernel, dt=5e-5, damping="identity", c_d=0.3)
+    allr = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, **kw)
+    allr.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    allr.step(500)
+    u_all, up_all, _, _ = allr.get_state()
+    for s in (0, 3, 7):
+        one = solver.Ensemble(m.xyz, m.tris, m.fixed, E[s:s + 1], h[s:s + 1], **kw)
+        one.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+        one.step(500)
+        u1, up1, _, _ = one.get_state()
+        assert np.array_equal(u1[0], u_all[s]) and np.array_equal(up1[0], up_all[s])
+        one.close()
+    # and an N_s = 128 run (VEC = 4) whose first 8 realisations are the same fields
+    E2 = np.concatenate([E] * 16)
+    h2 = np.concatenate([h] * 16)
+    big = solver.Ensemble(m.xyz, m.tris, m.fixed, E2, h2, **kw)
+    big.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    big.step(500)
+    ub, _, _, _ = big.get_state(want_prev=False)
+    for r in range(16):
+        assert np.array_equal(ub[8 * r:8 * r + 8], u_all)
+    big.close()
+    allr.close()
+
+
+def test_dirichlet_zero_load_and_state_roundtrip():
+    m = meshmod.cylinder(16, 21)
+    E, h = _mats(m, 4, 41)
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS)
+    ens.step(100)
+    u, up, _, _ = ens.get_state()
+    assert not u.any() and not up.any()            # zero load from rest => zero
+    tr = loads.steady(m.xyz, m.tris)
+    ens.set_traction(tr.F)
+    ens.step(137)
+    u, up, _, step = ens.get_state()
+    fixed = m.fixed == 7
+    assert not u[:, fixed].any() and not up[:, fixed].any() and u[:, ~fixed].any()
+    ens.step(50)
+    ref, _, _, _ = ens.get_state()
+    # resume from the checkpoint in a fresh context: bit-identical continuation
+    ens2 = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS)
+    ens2.set_traction(tr.F)
+    ens2.set_state(u, up, step)
+    ens2.step(50)
+    got, _, _, step2 = ens2.get_state()
+    assert step2 == step + 50 and np.array_equal(got, ref)
+    ens.close(); ens2.close()
+
+
+def test_divergence_detected_and_latched():
+    m = meshmod.cylinder(12, 23)
+    E, h = _mats(m, 2, 51)
+    om0 = oracle.OracleModel(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS)
+    dt = 3.0 * _crit_dt(om0)
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, dt=dt)
+    ens.set_traction(loads.steady(m.xyz, m.tris).F)
+    ens.step(3000)
+    with pytest.raises(EnsError) as ei:
+        ens.sync()
+    assert ei.value.code == ENS_E_DIVERGED and "step" in str(ei.value)
+    with pytest.raises(EnsError) as ei:
+        ens.step(1)
+    assert ei.value.code == ENS_E_STATE
+    ens.set_state(None, None, 0)
+    ens.step(1)
+    ens.sync()
+    ens.close()
+
+
+def test_sdof_closed_form_on_gpu():
+    """ens_create_csr with one 3x3 diagonal block: the kernel reproduces the closed-form
+    solution of the central-difference recurrence (same pin as the oracle's)."""
+    m_, k, f = 2.0, 50.0, 3.0
+    dt = 0.9 * 2.0 / math.sqrt(k / m_)
+    c1, c2, c3 = oracle.coeffs(np.array([[m_]]), dt, 0, 0.0)
+    ens = solver.Ensemble.from_csr([0, 1], [0], np.diag([k] * 3).reshape(1, 1, 9), c1, c2, c3, dt=dt)
+    ens.set_traction(np.array([[[f, 0.0, -f]]]))
+    n = 10_000
+    ens.step(n)
+    u, _, _, _ = ens.get_state()
+    L = np.longdouble
+    th = np.arccos(1 - L(c1[0, 0]) * L(k) / 2)
+    ref = (L(f) / L(k)) * (1 - np.cos(L(n) * th) + np.tan(th / 2) * np.sin(L(n) * th))
+    assert abs(L(u[0, 0, 0]) - ref) <= 1e-12 * (f / k) * 3
+    assert u[0, 0, 2] == -u[0, 0, 0] and u[0, 0, 1] == 0.0
+    ens.close()
+
+
+def test_c2_full_size_sampled_realisations():
+    """Config c2 at full size (96 x 262, N_s = 64, mode-1 damping 250/s) in the bench's
+    launch configuration; the oracle recomputes a sample of realisations one by one."""
+    cfg = configs.make("c2")
+    m = cfg.mesh
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS,
+                          damping="mass", c_d=cfg.c_d)
+    dt = ens.info()["dt"]
+    tr = cfg.traction
+    ens.set_traction(tr.F)
+    ens.step(1000)
+    u, _, _, _ = ens.get_state(want_prev=False)
+    for s in (0, 17, 63):
+        om = oracle.OracleModel(m.xyz, m.tris, m.fixed, cfg.E[s:s + 1], cfg.h[s:s + 1], rho=RHO,
+                                nu=NU, k_shear=KS, damping=1, c_d=cfg.c_d, dt=dt)
+        om.set_traction(tr.F, tr.tab_t, tr.tab_g, 0.0, 0.0)
+        om.run(1000)
+        assert np.linalg.norm(u[s] - om.u_n[0]) <= 1e-9 * np.linalg.norm(om.u_n[0])
+    ens.close()
+
+
+def test_c2_laplace_law_on_gpu():
+    """BASELINE config 2: steady pressure to static equilibrium, 10^4 steps; the
+    homogeneous member s = 0 matches the Laplace law with the fixed-end correction."""
+    cfg = configs.make("c2")
+    m = cfg.mesh
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS,
+                          damping="mass", c_d=cfg.c_d)
+    ens.set_traction(cfg.traction.F)
+    ens.step(10_000)
+    u, up, _, _ = ens.get_state()
+    assert np.linalg.norm(u - up) <= 1e-10 * np.linalg.norm(u)    # at rest
+    ring = 131
+    nodes = np.arange(ring * 96, (ring + 1) * 96)
+    rhat = m.xyz[nodes, :2] / np.linalg.norm(m.xyz[nodes, :2], axis=1, keepdims=True)
+    ur = np.mean(np.einsum("ij,ij->i", u[0, nodes, :2], rhat))
+    R, L, p = 2.0, 30.0, loads.P_SUPERPOSED
+    ell = R * math.sqrt(KS / (2 * (1 + NU)))
+    ref = (1 - NU ** 2) * p * R * R / (7e6 * 0.4) / (1 - 2 * NU ** 2 * ell / L)
+    assert ur == pytest.approx(ref, rel=1e-3)
+    # realisations with random fields: displacement spread around the homogeneous value
+    urs = np.mean(np.einsum("sij,ij->si", u[:, nodes, :2], rhat), axis=1)
+    assert np.all(np.abs(urs / ref - 1) < 0.5)
+    ens.close()

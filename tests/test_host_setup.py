@@ -1,0 +1,133 @@
+"""CPU tests of the product's host setup (libens.so ens_host_* entry points) against the
+oracle: integer maps bit-exact, floating-point setup within rounding (-m "not gpu")."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2101_09059_b200 import _ffi, solver
+from paper_2101_09059_b200.inputs import mesh as meshmod
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "ens.h")).read()
+    declared = set(re.findall(r"\b(ens_[a-z_]+)\s*\(", header))
+    declared -= {"ens_ctx"}
+    L = _ffi.lib()
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+    assert declared == set(_ffi.EXPORTS)
+
+
+MESHES = [
+    lambda: meshmod.cylinder(12, 23),
+    lambda: meshmod.shuffle_nodes(meshmod.cylinder(12, 23), 1),
+    lambda: meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(17, 11), 0.05, 2), 2),
+    lambda: meshmod.shuffle_nodes(meshmod.cylinder(96, 40), 3),
+]
+
+
+@pytest.mark.parametrize("mk", MESHES)
+def test_pattern_bitexact_vs_oracle(mk):
+    m = mk()
+    perm, row_ptr, col = solver.host_pattern(m.n_nodes, m.tris)
+    operm = oracle.rcm(m.n_nodes, m.tris)
+    orow, ocol = oracle.csr(m.n_nodes, m.tris, operm)
+    assert np.array_equal(perm, operm)
+    assert np.array_equal(row_ptr, orow)
+    assert np.array_equal(col, ocol)
+
+
+def test_pattern_two_components_bitexact():
+    a = meshmod.cylinder(5, 4)
+    b = meshmod.cylinder(6, 3)
+    tris = np.concatenate([b.tris + a.n_nodes, a.tris])
+    V = a.n_nodes + b.n_nodes
+    perm, row_ptr, col = solver.host_pattern(V, tris)
+    assert np.array_equal(perm, oracle.rcm(V, tris))
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+def test_partition_and_ghosts_bitexact(P):
+    m = meshmod.shuffle_nodes(meshmod.cylinder(24, 30), 7)
+    perm, row_ptr, col = solver.host_pattern(m.n_nodes, m.tris)
+    b = solver.host_partition(row_ptr, P)
+    ob, ogh, _ = oracle.halo_maps(row_ptr, col, P)
+    assert np.array_equal(b, ob)
+    for p in range(P):
+        assert np.array_equal(solver.host_ghosts(row_ptr, col, b[p], b[p + 1]), ogh[p])
+
+
+def test_validate_codes_match_oracle():
+    m = meshmod.cylinder(6, 3)
+    cases = []
+    t = m.tris.copy(); t[3, 1] = m.n_nodes; cases.append((m.xyz, t))
+    t = m.tris.copy(); t[4, 2] = t[4, 0]; cases.append((m.xyz, t))
+    x = m.xyz.copy(); x[m.tris[5, 2]] = x[m.tris[5, 0]] + 0.5 * (x[m.tris[5, 1]] - x[m.tris[5, 0]])
+    cases.append((x, m.tris))
+    cases.append((m.xyz, np.concatenate([m.tris, m.tris[:1]])))
+    cases.append((m.xyz, m.tris))
+    for xyz, tris in cases:
+        assert solver.host_validate(xyz, tris) == oracle.validate_mesh(xyz, tris)
+
+
+def test_element_stiffness_vs_oracle():
+    m = meshmod.perturb(meshmod.cylinder(16, 12), 0.1, 5)
+    for nu in (0.0, 0.3, 0.5):
+        K, A = solver.host_element_stiffness(m.xyz, m.tris, nu, 5 / 6)
+        Ko, Ao = oracle.all_khat(m.xyz, m.tris, nu, 5 / 6)
+        scale = np.abs(Ko).max(axis=(1, 2), keepdims=True)
+        assert np.max(np.abs(K - Ko) / scale) < 1e-13
+        np.testing.assert_allclose(A, Ao, rtol=1e-14)
+        assert np.array_equal(K, np.transpose(K, (0, 2, 1)))
+
+
+def test_materials_vs_oracle():
+    m = meshmod.perturb(meshmod.cylinder(16, 12), 0.1, 6)
+    rng = np.random.default_rng(0)
+    E = rng.uniform(5e6, 9e6, (3, m.n_nodes))
+    h = rng.uniform(0.3, 0.5, (3, m.n_nodes))
+    al, ms, dt = solver.host_materials(m.xyz, m.tris, E, h, 1.06, 0.9)
+    np.testing.assert_allclose(al, oracle.alpha(m.n_nodes, m.tris, E, h), rtol=1e-14)
+    np.testing.assert_allclose(ms, oracle.mass(m.xyz, m.tris, h, 1.06), rtol=1e-13)
+    assert dt == pytest.approx(oracle.cfl(m.xyz, m.tris, E, 1.06, 0.9), rel=1e-14)
+
+
+def test_create_without_gpu_fails_loudly():
+    """On a box without a device, ens_create must fail with ENS_E_CUDA — never fall back."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    m = meshmod.cylinder(6, 3)
+    E = np.full((1, m.n_nodes), 7e6)
+    h = np.full((1, m.n_nodes), 0.4)
+    with pytest.raises(_ffi.EnsError) as ei:
+        solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=1.06, nu=0.5)
+    assert ei.value.code in (_ffi.ENS_E_CUDA, _ffi.ENS_E_OOM)
+
+
+@pytest.mark.parametrize("bad", ["E", "h", "nu", "rho", "mesh"])
+def test_create_argument_errors(bad):
+    m = meshmod.cylinder(6, 3)
+    E = np.full((1, m.n_nodes), 7e6)
+    h = np.full((1, m.n_nodes), 0.4)
+    kw = dict(rho=1.06, nu=0.5)
+    tris = m.tris
+    if bad == "E":
+        E[0, 3] = -1
+    elif bad == "h":
+        h[0, 2] = 0
+    elif bad == "nu":
+        kw["nu"] = 0.7
+    elif bad == "rho":
+        kw["rho"] = 0.0
+    else:
+        tris = m.tris.copy(); tris[0, 0] = 999
+    with pytest.raises(_ffi.EnsError) as ei:
+        solver.Ensemble(m.xyz, tris, m.fixed, E, h, torch_alloc=False, **kw)
+    assert ei.value.code == (_ffi.ENS_E_MESH if bad == "mesh" else _ffi.ENS_E_ARG)
