@@ -33,7 +33,7 @@ def _workload_desc(cfg, n_s_total, world):
     m = cfg.mesh
     return (f"{cfg.name}: ideal cylinder D=4 L=30 cm, {m.meta['n_circ']}x{m.meta['n_axial']} rings "
             f"(V={m.n_nodes}, F={m.n_tris}), N_s={n_s_total} ({cfg.n_s}/GPU), "
-            + ("steady 13 mmHg" if cfg.traction.n_tab == 0 else "pulsatile 13+27 mmHg")
+            + ("steady 13 mmHg" if len(cfg.traction.tab_t) == 0 else "pulsatile 13+27 mmHg")
             + (f", mode-1 damping {cfg.c_d:g}/s" if cfg.damping == 1 else ", undamped"))
 
 
