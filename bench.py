@@ -100,6 +100,15 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def _launch_count(n: int, G: int) -> int:
+    """Kernels ens_step(n) enqueues: n fused steps + one counter advance per graph replay
+    (G steps each) and one for the directly launched remainder."""
+    if G > 0 and n >= G:
+        q, r = divmod(n, G)
+        return q * (G + 1) + (r + 1 if r else 0)
+    return n + (1 if n else 0)
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -283,7 +292,7 @@ def main(argv=None):
             "e2e": {"value": e2e_value, "unit": "DOF-updates/s", "h2d_bytes_per_step": h2d / win,
                     "d2h_bytes_per_step": d2h / win,
                     "window": f"{win} steps + ens_set_traction (H2D {h2d} B) + ens_get_state u_n (D2H {d2h} B)"},
-            "gpu_launches": args.steps + 1,
+            "gpu_launches": _launch_count(args.steps, info.get("graph_steps", 0)),
             "clocks": clk.summary(),
             "paper_best_context": {"value": 7.27e8, "unit": "DOF-updates/s",
                                    "hardware": "4x RTX 2080 Ti, OpenCL, 131,552-tri cylinder, 500 realisations (PAPER.md:665)"},

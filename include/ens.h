@@ -112,7 +112,9 @@ typedef struct {
     int64_t flops_per_step;             /* algorithmic fp64 flops of one fused step */
     int64_t device_bytes;               /* device memory held by the context */
     int32_t rcm_bandwidth;              /* max |i - j| over the pattern in RCM order */
-    int32_t launches_per_step;          /* kernels enqueued per ens_step step */
+    int32_t launches_per_step;          /* fused-step kernels per time step (1) */
+    int32_t graph_steps;                /* ens_step replays a CUDA graph of this many steps + 1 counter
+                                           advance (env ENS_GRAPH_STEPS; 0 = direct launches) */
 } ens_info;
 
 /* Create a context: validate the mesh, build the RCM-ordered block-CSR pattern, the

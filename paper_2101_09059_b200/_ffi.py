@@ -45,7 +45,7 @@ class EnsInfo(C.Structure):
                 ("kernel", C.c_int32), ("damping", C.c_int32), ("dist", C.c_int32),
                 ("step", C.c_int64), ("bytes_per_step", C.c_int64), ("flops_per_step", C.c_int64),
                 ("device_bytes", C.c_int64), ("rcm_bandwidth", C.c_int32),
-                ("launches_per_step", C.c_int32)]
+                ("launches_per_step", C.c_int32), ("graph_steps", C.c_int32)]
 
 
 EXPORTS = [

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -47,8 +48,10 @@ struct ens_ctx {
     double *d_Kval = nullptr, *d_c1 = nullptr, *d_c2a = nullptr, *d_c3a = nullptr;
     double c2 = 2.0, c3 = 1.0;
     uint8_t* d_fixed = nullptr;
-    int32_t *d_inc_ptr = nullptr, *d_inc = nullptr, *d_etri = nullptr;
-    double *d_Khat = nullptr, *d_alpha = nullptr;
+    int32_t* d_inc_ptr = nullptr;
+    int4* d_fan = nullptr;
+    double *d_Krow = nullptr, *d_Khat = nullptr, *d_alpha = nullptr;
+    int32_t mf_rows = 1, mf_groups = 1, mf_smem_inc = 0;
     double *d_u0 = nullptr, *d_u1 = nullptr, *d_stage = nullptr;
     double *d_scratch_u = nullptr, *d_scratch_y = nullptr;
     unsigned long long* d_flag = nullptr;
@@ -60,6 +63,11 @@ struct ens_ctx {
 
     int64_t step = 0;       // host mirror of *d_step once the stream drains
     bool latched = false;
+
+    // CUDA graph of graph_steps fused steps + one counter advance, replayed by ens_step
+    int32_t graph_steps = 64;
+    cudaGraphExec_t graph = nullptr;
+    bool graph_dirty = true;
 };
 
 namespace {
@@ -186,10 +194,12 @@ ens::StepArgs step_args(const ens_ctx* c) {
     a.col = c->d_col;
     a.Kval = c->d_Kval;
     a.inc_ptr = c->d_inc_ptr;
-    a.inc = c->d_inc;
-    a.etri = c->d_etri;
-    a.Khat = c->d_Khat;
+    a.fan = c->d_fan;
+    a.Krow = c->d_Krow;
     a.alpha = c->d_alpha;
+    a.mf_rows = c->mf_rows;
+    a.mf_groups = c->mf_groups;
+    a.mf_smem_inc = c->mf_smem_inc;
     a.c1 = c->d_c1;
     a.c2a = c->d_c2a;
     a.c3a = c->d_c3a;
@@ -257,18 +267,28 @@ int build_device_operator(ens_ctx* c, const ens::MeshView& m, const ens::Pattern
         dfree(c, c->d_alpha);       // the assembled path needs only Kval from here on
         dfree(c, c->d_Khat);
     } else {
-        std::vector<int32_t> etri(size_t(3 * F)), iptr(size_t(c->V) + 1, 0), inc(size_t(3 * F));
-        for (int64_t e = 0; e < F; ++e)
-            for (int a = 0; a < 3; ++a) {
-                etri[size_t(3 * e + a)] = pat.iperm[size_t(m.tris[3 * e + a])];
-                iptr[size_t(etri[size_t(3 * e + a)]) + 1]++;
+        ens::Fans fans = ens::build_fans(m, pat.iperm, Khat);
+        dfree(c, c->d_Khat);                      // Krow holds K^ in gather order
+        // CTA geometry: G threads per row (one realisation group each), R rows per CTA
+        const int P = c->n_s / ens::pick_vec(c->n_s);
+        c->mf_groups = std::min(P, 256);
+        c->mf_rows = std::max(1, std::min(256 / c->mf_groups, 32));
+        for (;;) {
+            int32_t mx = 0;
+            for (int64_t r0 = 0; r0 < c->V; r0 += c->mf_rows) {
+                int64_t r1 = std::min<int64_t>(r0 + c->mf_rows, c->V);
+                mx = std::max(mx, fans.ptr[size_t(r1)] - fans.ptr[size_t(r0)]);
             }
-        for (size_t k = 1; k < iptr.size(); ++k) iptr[k] += iptr[k - 1];
-        std::vector<int32_t> fillp(iptr.begin(), iptr.end() - 1);
-        for (int64_t e = 0; e < F; ++e)
-            for (int a = 0; a < 3; ++a) inc[size_t(fillp[size_t(etri[size_t(3 * e + a)])]++)] = int32_t(4 * e + a);
-        if ((rc = upload(c, &c->d_etri, etri.data(), etri.size())) ||
-            (rc = upload(c, &c->d_inc_ptr, iptr.data(), iptr.size())) || (rc = upload(c, &c->d_inc, inc.data(), inc.size())))
+            c->mf_smem_inc = mx;
+            if (int64_t(mx) * 240 <= 96 * 1024 || c->mf_rows == 1) break;
+            c->mf_rows = std::max(1, c->mf_rows / 2);
+        }
+        if (int64_t(c->mf_smem_inc) * 240 > 200 * 1024)
+            return fail(c, ENS_E_UNSUPPORTED, "a node has too many incident elements for the matrix-free kernel");
+        static_assert(sizeof(ens::FanRec) == sizeof(int4), "FanRec layout");
+        if ((rc = upload(c, &c->d_inc_ptr, fans.ptr.data(), fans.ptr.size())) ||
+            (rc = upload(c, &c->d_fan, reinterpret_cast<const int4*>(fans.rec.data()), fans.rec.size())) ||
+            (rc = upload(c, &c->d_Krow, fans.Krow.data(), fans.Krow.size())))
             return rc;
     }
     return ENS_OK;
@@ -278,7 +298,39 @@ int finish_create(ens_ctx* c, ens_ctx** out) {
     int rc = alloc_state(c);
     if (rc) return rc;
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (const char* g = std::getenv("ENS_GRAPH_STEPS")) c->graph_steps = std::max(0, std::atoi(g));
     *out = c;
+    return ENS_OK;
+}
+
+void drop_graph(ens_ctx* c) {
+    if (c->graph) cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+    c->graph_dirty = true;
+}
+
+// Capture graph_steps launches (step_off = 0..G-1) + the counter advance on a private
+// stream (the caller's stream may be the legacy default stream, which cannot capture).
+int build_graph(ens_ctx* c) {
+    drop_graph(c);
+    cudaStream_t cap = nullptr;
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    ens::StepArgs a = step_args(c);
+    cudaError_t err = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    for (int32_t k = 0; err == cudaSuccess && k < c->graph_steps; ++k) {
+        a.step_off = k;
+        err = c->kernel == ENS_KERNEL_MATRIX_FREE ? ens::launch_step_matrix_free(a, cap)
+                                                  : ens::launch_step_assembled(a, cap);
+    }
+    if (err == cudaSuccess) err = ens::launch_advance(c->d_step, c->graph_steps, cap);
+    cudaGraph_t g = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(cap, &g);
+    if (err == cudaSuccess) err = e2;
+    if (err == cudaSuccess) err = cudaGraphInstantiate(&c->graph, g, 0);
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(cap);
+    if (err != cudaSuccess) return cuda_fail(c, err, "CUDA graph capture of the step loop");
+    c->graph_dirty = false;
     return ENS_OK;
 }
 
@@ -455,6 +507,7 @@ int ens_set_traction(ens_ctx* c, int32_t n_fields, const double* F, int32_t n_ta
             for (int d = 0; d < 3; ++d) Fd[size_t((k * V + i) * 3 + d)] = F[(k * V + c->perm[size_t(i)]) * 3 + d];
     // (re)allocate: sizes may change; keep previous buffers alive until the stream drains
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    drop_graph(c);
     dfree(c, c->d_Fk);
     dfree(c, c->d_tab_t);
     dfree(c, c->d_tab_g);
@@ -477,12 +530,20 @@ int ens_step(ens_ctx* c, int64_t n) {
     if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
     if (n < 0) return fail(c, ENS_E_ARG, "n must be >= 0");
     if (c->latched) return fail(c, ENS_E_STATE, "context diverged: call ens_set_state before stepping again");
+    int64_t left = n;
+    if (c->graph_steps > 0 && n >= c->graph_steps) {
+        if (c->graph_dirty) {
+            int rc = build_graph(c);
+            if (rc) return rc;
+        }
+        for (; left >= c->graph_steps; left -= c->graph_steps) CUDA_TRY(c, cudaGraphLaunch(c->graph, c->stream));
+    }
     ens::StepArgs a = step_args(c);
-    for (int64_t k = 0; k < n; ++k) {
+    for (int64_t k = 0; k < left; ++k) {
         a.step_off = k;
         CUDA_TRY(c, launch(c, a));
     }
-    if (n) CUDA_TRY(c, ens::launch_advance(c->d_step, n, c->stream));
+    if (left) CUDA_TRY(c, ens::launch_advance(c->d_step, left, c->stream));
     c->step += n;
     return ENS_OK;
 }
@@ -581,6 +642,7 @@ int ens_query(const ens_ctx* c, ens_info* info) {
     info->device_bytes = c->device_bytes;
     info->rcm_bandwidth = c->bandwidth;
     info->launches_per_step = 1;
+    info->graph_steps = c->graph_steps;
     // algorithmic bytes: values + state read/read/write + c1 (+ c2, c3)
     const int64_t ns = c->n_s, per_node_state = 3 * 8 * 3 + 8 + (c->d_c2a ? 16 : 0);
     if (c->kernel == ENS_KERNEL_ASSEMBLED) {
@@ -595,6 +657,8 @@ int ens_query(const ens_ctx* c, ens_info* info) {
 
 void ens_destroy(ens_ctx* c) {
     if (!c) return;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    drop_graph(c);
     free_all(c);
     delete c;
 }

@@ -21,12 +21,14 @@ struct StepArgs {
     const int32_t* row_ptr = nullptr;   // [V_total + 1] (int32: nnzb < 2^31)
     const int32_t* col = nullptr;
     const double* Kval = nullptr;
-    // matrix-free operands
-    const int32_t* inc_ptr = nullptr;   // [V + 1] incidences of each row, ascending element
-    const int32_t* inc = nullptr;       // element * 4 + local index
-    const int32_t* etri = nullptr;      // [F][3] RCM node ids
-    const double* Khat = nullptr;       // [F][81]
+    // matrix-free operands (host_setup.hpp "Fans")
+    const int32_t* inc_ptr = nullptr;   // [V_total + 1] incidence range of each row
+    const int4* fan = nullptr;          // [3F] {e, n_prev, n_next, restart}
+    const double* Krow = nullptr;       // [3F][28]
     const double* alpha = nullptr;      // [F][n_s]
+    int32_t mf_rows = 1;                // rows per CTA
+    int32_t mf_groups = 1;              // realisation groups (threads) per row per CTA
+    int32_t mf_smem_inc = 0;            // max incidences staged by one CTA
     // update coefficients
     const double* c1 = nullptr;
     const double* c2a = nullptr;        // null => scalars c2, c3
@@ -56,6 +58,8 @@ struct StepArgs {
 cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st);
 // Same on the matrix-free element form (alpha_{e,s} K^_e gathered per node).
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st);
+// realisations per thread of the step kernels for a given N_s (4, 2 or 1)
+int pick_vec(int32_t n_s);
 // *step_base += n (after n steps were enqueued)
 cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st);
 

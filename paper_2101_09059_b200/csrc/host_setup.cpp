@@ -279,6 +279,80 @@ double cfl_dt(const MeshView& m, int32_t n_s, const double* E, double rho, doubl
 }
 
 // ------------------------------------------------------------------------------------
+// Fans for the matrix-free gather.  Element e = (t0, t1, t2) seen from its local node a
+// has the other nodes o1 = t[a+1], o2 = t[a+2] (cyclic, counter-clockwise about the
+// outward normal).  On a consistently oriented manifold the next element counter-
+// clockwise around the node has o1' = o2, so incidences chain by o2 -> o1.  Chains start
+// at an incidence whose o1 is no other incidence's o2 (open fan), else at the smallest
+// element; any mesh (even inconsistently oriented) is handled: a chain that cannot be
+// continued simply restarts.
+// ------------------------------------------------------------------------------------
+Fans build_fans(const MeshView& m, const std::vector<int32_t>& iperm, const std::vector<double>& Khat) {
+    const int64_t V = m.V, F = m.F;
+    Fans f;
+    f.ptr.assign(size_t(V) + 1, 0);
+    for (int64_t e = 0; e < F; ++e)
+        for (int a = 0; a < 3; ++a) f.ptr[size_t(iperm[size_t(m.tris[3 * e + a])]) + 1]++;
+    std::partial_sum(f.ptr.begin(), f.ptr.end(), f.ptr.begin());
+    // raw incidences per row, ascending element
+    std::vector<std::pair<int32_t, int32_t>> raw(size_t(3 * F));   // (e, a)
+    std::vector<int32_t> fill(f.ptr.begin(), f.ptr.end() - 1);
+    for (int64_t e = 0; e < F; ++e)
+        for (int a = 0; a < 3; ++a) raw[size_t(fill[size_t(iperm[size_t(m.tris[3 * e + a])])]++)] = {int32_t(e), a};
+    f.rec.resize(size_t(3 * F));
+    f.Krow.assign(size_t(3 * F) * 28, 0.0);
+    std::vector<char> used;
+    for (int64_t i = 0; i < V; ++i) {
+        const int32_t lo = f.ptr[size_t(i)], hi = f.ptr[size_t(i) + 1], n = hi - lo;
+        auto other = [&](int32_t k, int s) {          // s = 1 -> o1, 2 -> o2 (RCM ids)
+            auto [e, a] = raw[size_t(lo + k)];
+            return iperm[size_t(m.tris[3 * int64_t(e) + (a + s) % 3])];
+        };
+        used.assign(size_t(n), 0);
+        int32_t out = lo;
+        for (int32_t placed = 0; placed < n;) {
+            // chain start: an unused incidence whose o1 is not the o2 of another unused one
+            int32_t start = -1;
+            for (int32_t k = 0; k < n && start < 0; ++k) {
+                if (used[size_t(k)]) continue;
+                bool has_pred = false;
+                for (int32_t q = 0; q < n; ++q)
+                    if (q != k && !used[size_t(q)] && other(q, 2) == other(k, 1)) { has_pred = true; break; }
+                if (!has_pred) start = k;
+            }
+            if (start < 0)
+                for (int32_t k = 0; k < n; ++k)
+                    if (!used[size_t(k)]) { start = k; break; }
+            int32_t cur = start;
+            bool first = true;
+            while (cur >= 0) {
+                used[size_t(cur)] = 1;
+                ++placed;
+                auto [e, a] = raw[size_t(lo + cur)];
+                FanRec& r = f.rec[size_t(out)];
+                r.e = e;
+                r.n_prev = other(cur, 1);
+                r.n_next = other(cur, 2);
+                r.restart = first ? 1 : 0;
+                const int loc[3] = {a, (a + 1) % 3, (a + 2) % 3};
+                double* K = f.Krow.data() + size_t(out) * 28;
+                for (int c = 0; c < 3; ++c)
+                    for (int b = 0; b < 3; ++b)
+                        for (int d = 0; d < 3; ++d)
+                            K[9 * c + 3 * b + d] = Khat[size_t(e) * 81 + size_t(9 * (3 * a + c) + 3 * loc[b] + d)];
+                ++out;
+                first = false;
+                int32_t nxt = -1;
+                for (int32_t q = 0; q < n; ++q)
+                    if (!used[size_t(q)] && other(q, 1) == r.n_next) { nxt = q; break; }
+                cur = nxt;
+            }
+        }
+    }
+    return f;
+}
+
+// ------------------------------------------------------------------------------------
 // Partition: bounds[p] = min { r : P row_ptr[r] >= p nnzb }.
 // ------------------------------------------------------------------------------------
 std::vector<int64_t> partition_bounds(const std::vector<int64_t>& row_ptr, int32_t P) {

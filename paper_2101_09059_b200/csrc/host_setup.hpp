@@ -44,6 +44,22 @@ void materials(const MeshView& m, int32_t n_s, const double* E, const double* h,
                double* alpha, double* mass);
 double cfl_dt(const MeshView& m, int32_t n_s, const double* E, double rho, double safety);
 
+// Matrix-free operator arranged for the node-centric gather: for each
+// row i (RCM order) its incident elements as chains of a fan around i, so that consecutive
+// incidences (i, p_k, p_k+1), (i, p_k+1, p_k+2) share the node p_k+1.
+struct FanRec {
+    int32_t e;        // element (alpha row)
+    int32_t n_prev;   // p_k   (RCM id)
+    int32_t n_next;   // p_k+1 (RCM id)
+    int32_t restart;  // 1: first incidence of a chain (n_prev must be loaded)
+};
+struct Fans {
+    std::vector<int32_t> ptr;     // [V+1] incidence range of each row
+    std::vector<FanRec> rec;      // [3F]
+    std::vector<double> Krow;     // [3F][28]: K^_e rows 3a..3a+2, columns (own, p_k, p_k+1) x 3, + pad
+};
+Fans build_fans(const MeshView& m, const std::vector<int32_t>& iperm, const std::vector<double>& Khat);
+
 // Node partition of the RCM rows balanced by blocks, and ghost rows.
 std::vector<int64_t> partition_bounds(const std::vector<int64_t>& row_ptr, int32_t P);
 std::vector<int32_t> ghost_rows(const std::vector<int64_t>& row_ptr, const std::vector<int32_t>& col,

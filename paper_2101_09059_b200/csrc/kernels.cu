@@ -244,60 +244,113 @@ k_step_assembled(const StepArgs a) {
 }
 
 // ---- F2: fused step on the matrix-free element form ------------------------------------
-// y[i][c][s] = sum_{(e, a) incident to i, ascending e} alpha[e][s] * sum_{b, d}
-//              Khat[e][3a+c][3b+d] u[etri[e][b]][d][s]
+// y[i][c][s] = sum over the incidences (e, a) of row i of alpha[e][s] * sum_{b, d}
+//              K^_e[3a+c][3 loc(b) + d] u[node_b][d][s]
+// Incidences are walked as fans around i (host_setup.cpp build_fans): incidence k uses the
+// nodes (i, p_k, p_k+1) and the next one (i, p_k+1, p_k+2), so u[p_k+1] is loaded once and
+// carried in registers.  The CTA's rows are contiguous, hence so are their incidences: one
+// thread stages their K^ rows (224 B each) and fan records (16 B) into shared memory with
+// two 1-D TMA bulk copies completing on an mbarrier, while every thread loads its own u_i.
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done) : "r"(bar), "r"(phase) : "memory");
+    }
+}
+
 template <int VEC, bool APPLY>
 __global__ void __launch_bounds__(kThreads)
 k_step_matrix_free(const StepArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double s_coef[kMaxFields];
+    __shared__ __align__(8) uint64_t s_bar;
+
     const StepCtx sc = step_ctx(a);
-    if (!APPLY && threadIdx.x == 0) load_coeffs(a, double(sc.step) * a.dt, s_coef);
-    if (!APPLY) __syncthreads();
+    const int G = a.mf_groups, R = a.mf_rows;
+    const int64_t r0 = a.row0 + int64_t(blockIdx.x) * R;
+    const int64_t r1 = min(r0 + R, a.row0 + a.V);
+    const int32_t k0 = __ldg(a.inc_ptr + r0), k1 = __ldg(a.inc_ptr + r1);
+    const uint32_t n_inc = uint32_t(k1 - k0);
+    double* sK = reinterpret_cast<double*>(smem);
+    const int4* sRec = reinterpret_cast<const int4*>(smem + size_t(a.mf_smem_inc) * 224);
+    const uint32_t bar = uint32_t(__cvta_generic_to_shared(&s_bar));
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        if (n_inc) {
+            mbar_expect_tx(bar, n_inc * 240u);
+            tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sK)), a.Krow + size_t(k0) * 28, n_inc * 224u, bar);
+            tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sRec)), a.fan + k0, n_inc * 16u, bar);
+        }
+        if (!APPLY) load_coeffs(a, double(sc.step) * a.dt, s_coef);
+    }
+    __syncthreads();
 
     const int P = a.n_s / VEC;
-    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= a.V * P) return;
-    const int64_t i = a.row0 + tid / P;
-    const int s0 = int(tid % P) * VEC;
+    const int lr = int(threadIdx.x) / G;
+    const int g = int(blockIdx.y) * G + int(threadIdx.x) % G;
+    const int64_t i = r0 + lr;
+    const bool valid = lr < R && i < r1 && g < P;
     const int n_s = a.n_s;
+    const int s0 = g * VEC;
 
     double y[3][VEC];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int v = 0; v < VEC; ++v) y[c][v] = 0.0;
+    Vec<VEC> uo[3], up[3];
+    if (valid) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) uo[d] = ld_ro<VEC>(sc.un + (i * 3 + d) * n_s + s0);
+    }
+    if (n_inc) mbar_wait(bar, 0);
+    if (!valid) return;
 
-    const int32_t k_end = __ldg(a.inc_ptr + i + 1);
-    for (int32_t k = __ldg(a.inc_ptr + i); k < k_end; ++k) {
-        const int32_t code = __ldg(a.inc + k);
-        const int64_t e = code >> 2;
-        const int la = code & 3;
-        const double* Kh = a.Khat + e * 81 + 27 * la;
-        Vec<VEC> al = ld_ro<VEC>(a.alpha + e * n_s + s0);
-        double t[3][VEC];
+    const int32_t kb = __ldg(a.inc_ptr + i) - k0, ke = __ldg(a.inc_ptr + i + 1) - k0;
+    for (int32_t k = kb; k < ke; ++k) {
+        const int4 rec = sRec[k];
+        if (rec.w) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
+            for (int d = 0; d < 3; ++d) up[d] = ld_ro<VEC>(sc.un + (int64_t(rec.y) * 3 + d) * n_s + s0);
+        }
+        Vec<VEC> un[3];
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) t[c][v] = 0.0;
+        for (int d = 0; d < 3; ++d) un[d] = ld_ro<VEC>(sc.un + (int64_t(rec.z) * 3 + d) * n_s + s0);
+        const Vec<VEC> al = ld_ro<VEC>(a.alpha + int64_t(rec.x) * n_s + s0);
+        const double* K = sK + size_t(k) * 28;
 #pragma unroll
-        for (int nb = 0; nb < 3; ++nb) {
-            const int64_t node = __ldg(a.etri + e * 3 + nb);
-            Vec<VEC> u[3];
+        for (int c = 0; c < 3; ++c) {
+            double t[VEC];
 #pragma unroll
-            for (int d = 0; d < 3; ++d) u[d] = ld_ro<VEC>(sc.un + (node * 3 + d) * n_s + s0);
+            for (int v = 0; v < VEC; ++v) t[v] = 0.0;
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
+            for (int d = 0; d < 3; ++d) {
+                const double k_own = K[9 * c + d], k_prev = K[9 * c + 3 + d], k_next = K[9 * c + 6 + d];
 #pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const double kv = __ldg(Kh + 9 * c + 3 * nb + d);
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) t[c][v] = fma(kv, u[d].v[v], t[c][v]);
+                for (int v = 0; v < VEC; ++v) {
+                    t[v] = fma(k_own, uo[d].v[v], t[v]);
+                    t[v] = fma(k_prev, up[d].v[v], t[v]);
+                    t[v] = fma(k_next, un[d].v[v], t[v]);
                 }
+            }
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) y[c][v] = fma(al.v[v], t[v], y[c][v]);
         }
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) y[c][v] = fma(al.v[v], t[c][v], y[c][v]);
+        for (int d = 0; d < 3; ++d) up[d] = un[d];
     }
     if constexpr (APPLY) store_y<VEC>(a, i, s0, y);
     else cd_update<VEC>(a, sc, s_coef, i, s0, y);
@@ -368,13 +421,22 @@ static cudaError_t launch_a1(const StepArgs& a, cudaStream_t st) {
 
 template <int VEC, bool APPLY>
 static cudaError_t launch_a2(const StepArgs& a, cudaStream_t st) {
-    const int64_t n = a.V * (a.n_s / VEC);
-    if (n == 0) return cudaSuccess;
-    k_step_matrix_free<VEC, APPLY><<<grid_for(n), kThreads, 0, st>>>(a);
+    if (a.V == 0) return cudaSuccess;
+    const int P = a.n_s / VEC;
+    const size_t smem = size_t(a.mf_smem_inc) * 240;
+    static bool attr_set = false;      // per template instance
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free<VEC, APPLY>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    dim3 grid(unsigned((a.V + a.mf_rows - 1) / a.mf_rows), unsigned((P + a.mf_groups - 1) / a.mf_groups));
+    k_step_matrix_free<VEC, APPLY><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(a);
     return cudaGetLastError();
 }
 
-static int pick_vec(int32_t n_s) { return (n_s % 4 == 0 && n_s >= 128) ? 4 : (n_s % 2 == 0 ? 2 : 1); }
+int pick_vec(int32_t n_s) { return (n_s % 4 == 0 && n_s >= 128) ? 4 : (n_s % 2 == 0 ? 2 : 1); }
 
 cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st) {
     const bool apply = a.y_out != nullptr;
