@@ -91,9 +91,17 @@ typedef struct {
     double c_d;             /* damping coefficient */
     int32_t damping;        /* ENS_DAMP_*: NONE C~ = 0; MASS C~ = c_d M~ (1/s); IDENTITY C~ = c_d I (g/s) */
     int32_t kernel;         /* ENS_KERNEL_*: ASSEMBLED (per-realisation block-CSR values) or MATRIX_FREE */
-    int32_t dist;           /* ENS_DIST_*; ENSEMBLE = this rank holds realisations [s_begin, s_begin + n_s) */
-    int32_t rank, world;    /* process-group position (dist != SINGLE) */
-    void* nccl_comm;        /* ncclComm_t for ENS_DIST_NODE (torch ProcessGroupNCCL), else NULL */
+    int32_t dist;           /* ENS_DIST_*.  ENSEMBLE: this context holds realisations [s_begin, s_begin + n_s)
+                               of a sharded ensemble (no communication).  NODE: the RCM rows are split
+                               into `world` parts balanced by blocks, each advanced with a halo
+                               exchange of the N_s-wide interface rows per step:
+                               with nccl_comm != NULL this process holds part `rank` and exchanges with
+                               NCCL point-to-point; with nccl_comm == NULL this context holds all
+                               `world` parts on one device and exchanges by device copies (single-
+                               process emulation; results are bit-identical to ENS_DIST_SINGLE). */
+    int32_t rank, world;    /* process-group position (dist == NODE) */
+    void* nccl_comm;        /* ncclComm_t of this process group (torch ProcessGroupNCCL._comm_ptr()),
+                               resolved against the libnccl.so.2 already loaded in-process */
     void* stream;           /* cudaStream_t all work is enqueued on (NULL = legacy default stream) */
     void* (*dev_alloc)(size_t bytes, void* user);    /* optional device allocator */
     void (*dev_free)(void* ptr, void* user);
@@ -112,7 +120,9 @@ typedef struct {
     int64_t flops_per_step;             /* algorithmic fp64 flops of one fused step */
     int64_t device_bytes;               /* device memory held by the context */
     int32_t rcm_bandwidth;              /* max |i - j| over the pattern in RCM order */
-    int32_t launches_per_step;          /* fused-step kernels per time step (1) */
+    int64_t n_owned;                    /* rows advanced by this context (V unless NODE with NCCL) */
+    int64_t halo_bytes_per_step;        /* bytes sent + received by the halo exchange per step */
+    int32_t launches_per_step;          /* kernels per time step (1 without a halo) */
     int32_t graph_steps;                /* ens_step replays a CUDA graph of this many steps + 1 counter
                                            advance (env ENS_GRAPH_STEPS; 0 = direct launches) */
 } ens_info;
@@ -146,16 +156,22 @@ int ens_step(ens_ctx* ctx, int64_t n);
 int ens_sync(ens_ctx* ctx);
 
 /* Copy the state to caller-owned HOST buffers (either may be NULL):
- * u_n, u_nm1: [n_s][V][3] in the caller's node numbering.  t, step may be NULL.
- * Synchronises the context stream. */
+ * u_n, u_nm1: [n_s][R][3] with R = V in the caller's node numbering, except for a NODE
+ * context on NCCL, where R = the owned rows in the order ens_get_owned reports.
+ * t, step may be NULL.  Synchronises the context. */
 int ens_get_state(ens_ctx* ctx, double* u_n, double* u_nm1, double* t, int64_t* step);
 
+/* Rows of ens_get_state / ens_apply_stiffness outputs: *n = R; node_ids[R] (may be NULL)
+ * receives the caller node id of each row. */
+int ens_get_owned(const ens_ctx* ctx, int32_t* node_ids, int64_t* n);
+
 /* Overwrite the state (checkpoint / resume; clears the divergence latch).
- * u_n, u_nm1: [n_s][V][3] host, caller's numbering; NULL => zeros. */
+ * u_n, u_nm1: FULL [n_s][V][3] host arrays in the caller's numbering (every rank of a NODE
+ * group passes the full state: each takes its owned and ghost rows); NULL => zeros. */
 int ens_set_state(ens_ctx* ctx, const double* u_n, const double* u_nm1, double t, int64_t step);
 
 /* Diagnostic: y_s = K_s u_s for all s with the hot kernel's own product (same inner loop
- * and summation order as ens_step).  u, y: [n_s][V][3] host, caller's numbering. */
+ * and summation order as ens_step).  u: full [n_s][V][3]; y: [n_s][R][3] as ens_get_state. */
 int ens_apply_stiffness(ens_ctx* ctx, const double* u, double* y);
 
 /* Sizes, dt and algorithmic traffic of the context. */
@@ -187,6 +203,15 @@ int ens_host_partition(int64_t n_nodes, const int64_t* row_ptr, int32_t n_parts,
 /* Ghost rows of part [lo, hi): sorted columns outside the range.  ghosts[cap]; *n = count. */
 int ens_host_ghosts(int64_t n_nodes, const int64_t* row_ptr, const int32_t* col, int64_t lo,
                     int64_t hi, int32_t* ghosts, int64_t cap, int64_t* n);
+
+/* Halo plan of part `part` of n_parts (as ens_create builds it for ENS_DIST_NODE):
+ * lo_hi_b[5] = {lo, hi, b_lo, b_hi, n_ghost}: owned RCM rows [lo, hi); every row with a
+ * ghost column is among local rows [0, b_lo) or [hi-lo-b_hi, hi-lo).  peers[n_parts] and
+ * peer_info[n_parts][4] = {send_off, send_n, recv_row, recv_n} per neighbour (ascending
+ * rank); send_rows[cap] = local rows sent, concatenated per neighbour. */
+int ens_host_halo_plan(int64_t n_nodes, const int64_t* row_ptr, const int32_t* col, int32_t n_parts, int32_t part,
+                       int64_t* lo_hi_b, int32_t* peers, int64_t* peer_info, int32_t* send_rows, int64_t cap,
+                       int64_t* n_peers, int64_t* n_send);
 
 /* Element stiffness K^_e (E = 1, unit thickness, global frame) and area, as ens_create
  * computes them.  Khat: [F][9][9]; area: [F]. */

@@ -1,5 +1,7 @@
 // capi.cpp -- the C ABI of include/ens.h: context lifetime, host setup -> device upload,
-// step enqueue, state transfer.  Every step of the hot path runs in kernels.cu.
+// step enqueue (fused kernels + halo exchange), state transfer.  Every step of the hot
+// path runs in kernels.cu; the halo moves with NCCL (one part per process) or device
+// copies (all parts in one context: the single-process emulation used by the tests).
 #include "ens.h"
 
 #include <algorithm>
@@ -14,6 +16,7 @@
 
 #include "device.hpp"
 #include "host_setup.hpp"
+#include "nccl_dl.hpp"
 
 namespace {
 
@@ -24,12 +27,33 @@ struct DevBuf {
     size_t bytes = 0;
 };
 
+// One node partition held on this device: owned rows [lo, hi) of the RCM order, ghosts.
+struct Part {
+    ens::PartPlan plan;
+    int64_t n_own = 0, n_gh = 0;
+    int32_t *d_row_ptr = nullptr, *d_col = nullptr;
+    int32_t *d_map_own = nullptr, *d_map_all = nullptr;   // local row -> caller node id
+    int32_t* d_map_abi = nullptr;                          // owned row -> row of the ABI arrays
+    int32_t* d_send_rows = nullptr;
+    double *d_Kval = nullptr, *d_c1 = nullptr, *d_c2a = nullptr, *d_c3a = nullptr, *d_Fk = nullptr;
+    double *d_u0 = nullptr, *d_u1 = nullptr, *d_sendbuf = nullptr;
+    uint8_t* d_fixed = nullptr;
+    int32_t* d_inc_ptr = nullptr;
+    int4* d_fan = nullptr;
+    double *d_Krow = nullptr, *d_alpha = nullptr;
+    int32_t mf_rows = 1, mf_groups = 1, mf_smem_inc = 0;
+    double *d_scratch_u = nullptr, *d_scratch_y = nullptr;
+    std::vector<int32_t> map_own;                          // host copy (ens_get_owned)
+};
+
 }  // namespace
 
 struct ens_ctx {
     std::string err;
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_packed = nullptr, ev_halo = nullptr;
     void* (*dev_alloc)(size_t, void*) = nullptr;
     void (*dev_free)(void*, void*) = nullptr;
     void* alloc_user = nullptr;
@@ -38,36 +62,31 @@ struct ens_ctx {
 
     int64_t V = 0, F = 0, nnzb = 0;
     int32_t n_s = 0, s_begin = 0;
-    int32_t kernel = 0, damping = 0, dist = 0;
+    int32_t kernel = 0, damping = 0, dist = 0, rank = 0, world = 1;
     double dt = 0.0, dt_cfl = 0.0, c_d = 0.0;
-    int32_t bandwidth = 0;
-    std::vector<int32_t> perm, iperm;      // perm[new] = old
-
-    // device arrays (RCM order, realisation innermost)
-    int32_t *d_row_ptr = nullptr, *d_col = nullptr, *d_perm = nullptr;
-    double *d_Kval = nullptr, *d_c1 = nullptr, *d_c2a = nullptr, *d_c3a = nullptr;
     double c2 = 2.0, c3 = 1.0;
-    uint8_t* d_fixed = nullptr;
-    int32_t* d_inc_ptr = nullptr;
-    int4* d_fan = nullptr;
-    double *d_Krow = nullptr, *d_Khat = nullptr, *d_alpha = nullptr;
-    int32_t mf_rows = 1, mf_groups = 1, mf_smem_inc = 0;
-    double *d_u0 = nullptr, *d_u1 = nullptr, *d_stage = nullptr;
-    double *d_scratch_u = nullptr, *d_scratch_y = nullptr;
+    int32_t bandwidth = 0;
+    std::vector<int32_t> perm, iperm;       // perm[new] = old (global)
+
+    std::vector<Part> parts;                // 1 (single / ensemble / NCCL rank) or world (emulation)
+    const ens::Nccl* nccl = nullptr;
+    void* nccl_comm = nullptr;
+
+    double* d_stage = nullptr;              // [n_s][V][3] ABI staging
     unsigned long long* d_flag = nullptr;
     int64_t* d_step = nullptr;
-    // traction
     int32_t n_fields = 0, n_tab = 0;
-    double *d_Fk = nullptr, *d_tab_t = nullptr, *d_tab_g = nullptr;
+    double *d_tab_t = nullptr, *d_tab_g = nullptr;
     double period = 0.0, ramp_T = 0.0;
 
-    int64_t step = 0;       // host mirror of *d_step once the stream drains
+    int64_t step = 0;
     bool latched = false;
 
-    // CUDA graph of graph_steps fused steps + one counter advance, replayed by ens_step
-    int32_t graph_steps = 64;
+    int32_t graph_steps = 64;               // CUDA graph of this many steps (single part, no halo)
     cudaGraphExec_t graph = nullptr;
     bool graph_dirty = true;
+
+    bool has_halo() const { return parts.size() > 1 || nccl_comm != nullptr; }
 };
 
 namespace {
@@ -83,10 +102,16 @@ int cuda_fail(ens_ctx* c, cudaError_t e, const char* what) {
                 std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-#define CUDA_TRY(c, expr)                                   \
-    do {                                                    \
-        cudaError_t _e = (expr);                            \
+#define CUDA_TRY(c, expr)                                      \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
         if (_e != cudaSuccess) return cuda_fail(c, _e, #expr); \
+    } while (0)
+
+#define RC_TRY(expr)              \
+    do {                          \
+        int _rc = (expr);         \
+        if (_rc) return _rc;      \
     } while (0)
 
 template <typename T>
@@ -123,22 +148,32 @@ void dfree(ens_ctx* c, T*& p) {
 
 template <typename T>
 int upload(ens_ctx* c, T** out, const T* host, size_t count) {
-    int rc = dalloc(c, out, count);
-    if (rc) return rc;
+    RC_TRY(dalloc(c, out, count));
     if (count) CUDA_TRY(c, cudaMemcpyAsync(*out, host, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
-    // host staging vectors die at the end of ens_create: make the copy complete first
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));   // host staging vectors are temporaries
     return ENS_OK;
+}
+
+void drop_graph(ens_ctx* c) {
+    if (c->graph) cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+    c->graph_dirty = true;
 }
 
 void free_all(ens_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
+    drop_graph(c);
     for (auto& b : c->bufs) {
         if (c->dev_free) c->dev_free(b.p, c->alloc_user);
         else cudaFreeAsync(b.p, c->stream);
     }
     if (c->stream) cudaStreamSynchronize(c->stream);
     c->bufs.clear();
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->ev_packed) cudaEventDestroy(c->ev_packed);
+    if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+    c->comm_stream = nullptr;
+    c->ev_packed = c->ev_halo = nullptr;
 }
 
 int check_opts(const ens_options* opt) {
@@ -147,14 +182,18 @@ int check_opts(const ens_options* opt) {
     if (opt->damping < 0 || opt->damping > 2) return fail(nullptr, ENS_E_ARG, "opt->damping must be 0, 1 or 2");
     if (opt->kernel < 0 || opt->kernel > 1) return fail(nullptr, ENS_E_ARG, "opt->kernel must be 0 or 1");
     if (!(opt->c_d >= 0.0) || !std::isfinite(opt->c_d)) return fail(nullptr, ENS_E_ARG, "opt->c_d must be finite and >= 0");
-    if (opt->dist == ENS_DIST_NODE)
-        return fail(nullptr, ENS_E_UNSUPPORTED, "dist = ENS_DIST_NODE is not built in this version (use ENS_DIST_ENSEMBLE)");
     if (opt->dist < 0 || opt->dist > 2) return fail(nullptr, ENS_E_ARG, "opt->dist must be 0, 1 or 2");
+    if (opt->dist == ENS_DIST_NODE) {
+        if (opt->world < 1) return fail(nullptr, ENS_E_ARG, "opt->world must be >= 1");
+        if (opt->nccl_comm && (opt->rank < 0 || opt->rank >= opt->world))
+            return fail(nullptr, ENS_E_ARG, "opt->rank must lie in [0, world)");
+    }
     return ENS_OK;
 }
 
 int init_ctx(ens_ctx* c, const ens_options* opt) {
     ens_options def{};
+    def.device = -1;
     if (!opt) opt = &def;
     c->device = opt->device;
     if (opt->device >= 0) CUDA_TRY(c, cudaSetDevice(opt->device));
@@ -167,47 +206,45 @@ int init_ctx(ens_ctx* c, const ens_options* opt) {
     c->damping = opt->damping;
     c->dist = opt->dist;
     c->c_d = opt->c_d;
+    c->rank = opt->rank;
+    c->world = opt->world > 0 ? opt->world : 1;
+    c->nccl_comm = opt->dist == ENS_DIST_NODE ? opt->nccl_comm : nullptr;
+    if (c->nccl_comm) {
+        std::string why;
+        c->nccl = ens::nccl_load(&why);
+        if (!c->nccl) return fail(c, ENS_E_NCCL, why);
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+    }
+    if (const char* g = std::getenv("ENS_GRAPH_STEPS")) c->graph_steps = std::max(0, std::atoi(g));
     return ENS_OK;
 }
 
-int alloc_state(ens_ctx* c) {
-    const size_t n = size_t(c->V) * 3 * size_t(c->n_s);
-    int rc;
-    if ((rc = dalloc(c, &c->d_u0, n)) || (rc = dalloc(c, &c->d_u1, n)) || (rc = dalloc(c, &c->d_stage, n)) ||
-        (rc = dalloc(c, &c->d_flag, 1)) || (rc = dalloc(c, &c->d_step, 1)))
-        return rc;
-    CUDA_TRY(c, cudaMemsetAsync(c->d_u0, 0, n * sizeof(double), c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->d_u1, 0, n * sizeof(double), c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0xff, sizeof(unsigned long long), c->stream));
-    CUDA_TRY(c, cudaMemsetAsync(c->d_step, 0, sizeof(int64_t), c->stream));
-    c->step = 0;
-    return ENS_OK;
-}
-
-ens::StepArgs step_args(const ens_ctx* c) {
+ens::StepArgs part_args(const ens_ctx* c, const Part& p) {
     ens::StepArgs a;
-    a.V = c->V;
     a.row0 = 0;
-    a.V_total = c->V;
+    a.V = p.n_own;
+    a.fk_rows = p.n_own;
     a.n_s = c->n_s;
-    a.row_ptr = c->d_row_ptr;
-    a.col = c->d_col;
-    a.Kval = c->d_Kval;
-    a.inc_ptr = c->d_inc_ptr;
-    a.fan = c->d_fan;
-    a.Krow = c->d_Krow;
-    a.alpha = c->d_alpha;
-    a.mf_rows = c->mf_rows;
-    a.mf_groups = c->mf_groups;
-    a.mf_smem_inc = c->mf_smem_inc;
-    a.c1 = c->d_c1;
-    a.c2a = c->d_c2a;
-    a.c3a = c->d_c3a;
+    a.row_ptr = p.d_row_ptr;
+    a.col = p.d_col;
+    a.Kval = p.d_Kval;
+    a.inc_ptr = p.d_inc_ptr;
+    a.fan = p.d_fan;
+    a.Krow = p.d_Krow;
+    a.alpha = p.d_alpha;
+    a.mf_rows = p.mf_rows;
+    a.mf_groups = p.mf_groups;
+    a.mf_smem_inc = p.mf_smem_inc;
+    a.c1 = p.d_c1;
+    a.c2a = p.d_c2a;
+    a.c3a = p.d_c3a;
     a.c2 = c->c2;
     a.c3 = c->c3;
-    a.fixed = c->d_fixed;
+    a.fixed = p.d_fixed;
     a.n_fields = c->n_fields;
-    a.Fk = c->d_Fk;
+    a.Fk = p.d_Fk;
     a.n_tab = c->n_tab;
     a.tab_t = c->d_tab_t;
     a.tab_g = c->d_tab_g;
@@ -215,161 +252,279 @@ ens::StepArgs step_args(const ens_ctx* c) {
     a.ramp_T = c->ramp_T;
     a.dt = c->dt;
     a.step_base = c->d_step;
-    a.ubuf0 = c->d_u0;
-    a.ubuf1 = c->d_u1;
+    a.ubuf0 = p.d_u0;
+    a.ubuf1 = p.d_u1;
     a.flag = c->d_flag;
     a.s_global0 = c->s_begin;
     return a;
 }
 
-cudaError_t launch(const ens_ctx* c, const ens::StepArgs& a) {
-    return c->kernel == ENS_KERNEL_MATRIX_FREE ? ens::launch_step_matrix_free(a, c->stream)
-                                               : ens::launch_step_assembled(a, c->stream);
+cudaError_t launch_rows(const ens_ctx* c, ens::StepArgs a, int64_t row0, int64_t rows, cudaStream_t st) {
+    if (rows <= 0) return cudaSuccess;
+    a.row0 = row0;
+    a.V = rows;
+    return c->kernel == ENS_KERNEL_MATRIX_FREE ? ens::launch_step_matrix_free(a, st)
+                                               : ens::launch_step_assembled(a, st);
 }
 
-// Element -> node-block contributions for F0, ascending element within each block.
-int build_device_operator(ens_ctx* c, const ens::MeshView& m, const ens::Pattern& pat,
-                          const std::vector<double>& Khat, const std::vector<double>& alpha_se) {
-    const int64_t F = c->F, n_s = c->n_s;
-    // alpha in device layout [F][n_s]
-    std::vector<double> alpha_dev(size_t(F * n_s));
-    for (int64_t s = 0; s < n_s; ++s)
-        for (int64_t e = 0; e < F; ++e) alpha_dev[size_t(e * n_s + s)] = alpha_se[size_t(s * F + e)];
-    int rc;
-    if ((rc = upload(c, &c->d_alpha, alpha_dev.data(), alpha_dev.size()))) return rc;
-    if ((rc = upload(c, &c->d_Khat, Khat.data(), Khat.size()))) return rc;
-
-    if (c->kernel == ENS_KERNEL_ASSEMBLED) {
-        std::vector<int32_t> cnt(size_t(c->nnzb) + 1, 0), code(size_t(9 * F)), blk(size_t(9 * F));
-        for (int64_t e = 0; e < F; ++e)
-            for (int a = 0; a < 3; ++a)
-                for (int b = 0; b < 3; ++b) {
-                    int32_t i = pat.iperm[size_t(m.tris[3 * e + a])], j = pat.iperm[size_t(m.tris[3 * e + b])];
-                    auto first = pat.col.begin() + pat.row_ptr[size_t(i)];
-                    auto last = pat.col.begin() + pat.row_ptr[size_t(i) + 1];
-                    auto it = std::lower_bound(first, last, j);
-                    int32_t bi = int32_t(it - pat.col.begin());
-                    blk[size_t(9 * e + 3 * a + b)] = bi;
-                    cnt[size_t(bi) + 1]++;
-                }
-        for (size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
-        std::vector<int32_t> fillp(cnt.begin(), cnt.end() - 1);
-        for (int64_t e = 0; e < F; ++e)                 // ascending e => ascending within block
-            for (int ab = 0; ab < 9; ++ab) code[size_t(fillp[size_t(blk[size_t(9 * e + ab)])]++)] = int32_t(9 * e + ab);
-        int32_t *d_cptr = nullptr, *d_code = nullptr;
-        if ((rc = upload(c, &d_cptr, cnt.data(), cnt.size())) || (rc = upload(c, &d_code, code.data(), code.size())))
-            return rc;
-        if ((rc = dalloc(c, &c->d_Kval, size_t(c->nnzb) * 9 * size_t(n_s)))) return rc;
-        CUDA_TRY(c, ens::launch_assemble(c->nnzb, c->n_s, d_cptr, d_code, c->d_alpha, c->d_Khat, c->d_Kval, c->stream));
-        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-        dfree(c, d_cptr);
-        dfree(c, d_code);
-        dfree(c, c->d_alpha);       // the assembled path needs only Kval from here on
-        dfree(c, c->d_Khat);
-    } else {
-        ens::Fans fans = ens::build_fans(m, pat.iperm, Khat);
-        dfree(c, c->d_Khat);                      // Krow holds K^ in gather order
-        // CTA geometry: G threads per row (one realisation group each), R rows per CTA
-        const int P = c->n_s / ens::pick_vec(c->n_s);
-        c->mf_groups = std::min(P, 256);
-        c->mf_rows = std::max(1, std::min(256 / c->mf_groups, 32));
-        for (;;) {
-            int32_t mx = 0;
-            for (int64_t r0 = 0; r0 < c->V; r0 += c->mf_rows) {
-                int64_t r1 = std::min<int64_t>(r0 + c->mf_rows, c->V);
-                mx = std::max(mx, fans.ptr[size_t(r1)] - fans.ptr[size_t(r0)]);
-            }
-            c->mf_smem_inc = mx;
-            if (int64_t(mx) * 240 <= 96 * 1024 || c->mf_rows == 1) break;
-            c->mf_rows = std::max(1, c->mf_rows / 2);
-        }
-        if (int64_t(c->mf_smem_inc) * 240 > 200 * 1024)
-            return fail(c, ENS_E_UNSUPPORTED, "a node has too many incident elements for the matrix-free kernel");
-        static_assert(sizeof(ens::FanRec) == sizeof(int4), "FanRec layout");
-        if ((rc = upload(c, &c->d_inc_ptr, fans.ptr.data(), fans.ptr.size())) ||
-            (rc = upload(c, &c->d_fan, reinterpret_cast<const int4*>(fans.rec.data()), fans.rec.size())) ||
-            (rc = upload(c, &c->d_Krow, fans.Krow.data(), fans.Krow.size())))
-            return rc;
+// ---- one time step of every part (step index = ctx step + k) ---------------------------
+int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
+    const int64_t step = c->step + k;            // host mirror of *d_step + k
+    if (!c->has_halo()) {
+        ens::StepArgs a = part_args(c, c->parts[0]);
+        a.step_off = k;
+        CUDA_TRY(c, launch_rows(c, a, 0, c->parts[0].n_own, st));
+        return ENS_OK;
     }
+    // (1) boundary rows of every part (they read ghosts, and the neighbours need them)
+    for (Part& p : c->parts) {
+        ens::StepArgs a = part_args(c, p);
+        a.step_off = k;
+        CUDA_TRY(c, launch_rows(c, a, 0, p.plan.b_lo, st));
+        CUDA_TRY(c, launch_rows(c, a, p.n_own - p.plan.b_hi, p.plan.b_hi, st));
+        CUDA_TRY(c, ens::launch_pack(int64_t(p.plan.send_rows.size()), c->n_s, p.d_send_rows, c->d_step, k, p.d_u0,
+                                     p.d_u1, p.d_sendbuf, st));
+    }
+    const size_t w = size_t(3) * size_t(c->n_s);
+    auto unew = [&](Part& p) { return ((step + 1) & 1) ? p.d_u1 : p.d_u0; };
+    // (2) halo: u_{n+1} of the send rows -> the neighbours' ghost rows
+    if (c->nccl_comm) {
+        Part& p = c->parts[0];
+        CUDA_TRY(c, cudaEventRecord(c->ev_packed, st));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
+        const ens::Nccl& N = *c->nccl;
+        int r = N.group_start();
+        for (const auto& pe : p.plan.peers) {
+            if (r == 0 && pe.send_n)
+                r = N.send(p.d_sendbuf + size_t(pe.send_off) * w, size_t(pe.send_n) * w, ens::Nccl::kDouble, pe.q,
+                           c->nccl_comm, c->comm_stream);
+            if (r == 0 && pe.recv_n)
+                r = N.recv(unew(p) + size_t(pe.recv_row) * w, size_t(pe.recv_n) * w, ens::Nccl::kDouble, pe.q,
+                           c->nccl_comm, c->comm_stream);
+        }
+        int r2 = N.group_end();
+        if (r == 0) r = r2;
+        if (r != 0)
+            return fail(c, ENS_E_NCCL, std::string("halo exchange: ") + (N.error_string ? N.error_string(r) : "error"));
+        CUDA_TRY(c, cudaEventRecord(c->ev_halo, c->comm_stream));
+    } else {
+        for (Part& p : c->parts)
+            for (const auto& pe : p.plan.peers) {
+                if (!pe.recv_n) continue;
+                const Part& q = c->parts[size_t(pe.q)];
+                const auto it = std::find_if(q.plan.peers.begin(), q.plan.peers.end(),
+                                             [&](const ens::PartPlan::Peer& x) { return x.q == p.plan.p; });
+                CUDA_TRY(c, cudaMemcpyAsync(unew(p) + size_t(pe.recv_row) * w, q.d_sendbuf + size_t(it->send_off) * w,
+                                            size_t(pe.recv_n) * w * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            }
+    }
+    // (3) interior rows, overlapping the exchange on the comm stream
+    for (Part& p : c->parts) {
+        ens::StepArgs a = part_args(c, p);
+        a.step_off = k;
+        CUDA_TRY(c, launch_rows(c, a, p.plan.b_lo, p.n_own - p.plan.b_lo - p.plan.b_hi, st));
+    }
+    // (4) the next step's boundary rows read the ghosts: join the exchange
+    if (c->nccl_comm) CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
     return ENS_OK;
 }
 
-int finish_create(ens_ctx* c, ens_ctx** out) {
-    int rc = alloc_state(c);
-    if (rc) return rc;
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    if (const char* g = std::getenv("ENS_GRAPH_STEPS")) c->graph_steps = std::max(0, std::atoi(g));
-    *out = c;
-    return ENS_OK;
-}
-
-void drop_graph(ens_ctx* c) {
-    if (c->graph) cudaGraphExecDestroy(c->graph);
-    c->graph = nullptr;
-    c->graph_dirty = true;
-}
-
-// Capture graph_steps launches (step_off = 0..G-1) + the counter advance on a private
-// stream (the caller's stream may be the legacy default stream, which cannot capture).
+// Capture graph_steps steps + the counter advance on a private stream (the caller's stream
+// may be the legacy default stream, which cannot capture).
 int build_graph(ens_ctx* c) {
     drop_graph(c);
     cudaStream_t cap = nullptr;
     CUDA_TRY(c, cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-    ens::StepArgs a = step_args(c);
     cudaError_t err = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
-    for (int32_t k = 0; err == cudaSuccess && k < c->graph_steps; ++k) {
-        a.step_off = k;
-        err = c->kernel == ENS_KERNEL_MATRIX_FREE ? ens::launch_step_matrix_free(a, cap)
-                                                  : ens::launch_step_assembled(a, cap);
-    }
-    if (err == cudaSuccess) err = ens::launch_advance(c->d_step, c->graph_steps, cap);
+    int rc = ENS_OK;
+    for (int32_t k = 0; err == cudaSuccess && rc == ENS_OK && k < c->graph_steps; ++k) rc = enqueue_step(c, k, cap);
+    if (err == cudaSuccess && rc == ENS_OK) err = ens::launch_advance(c->d_step, c->graph_steps, cap);
     cudaGraph_t g = nullptr;
     cudaError_t e2 = cudaStreamEndCapture(cap, &g);
     if (err == cudaSuccess) err = e2;
-    if (err == cudaSuccess) err = cudaGraphInstantiate(&c->graph, g, 0);
+    if (err == cudaSuccess && rc == ENS_OK) err = cudaGraphInstantiate(&c->graph, g, 0);
     if (g) cudaGraphDestroy(g);
     cudaStreamDestroy(cap);
+    if (rc) return rc;
     if (err != cudaSuccess) return cuda_fail(c, err, "CUDA graph capture of the step loop");
     c->graph_dirty = false;
     return ENS_OK;
 }
 
-}  // namespace
+// ---- per-part device operator ---------------------------------------------------------
+struct Global {
+    const ens::MeshView* m;
+    const ens::Pattern* pat;
+    const std::vector<double>* Khat;       // [F][81]
+    const std::vector<double>* alpha;      // [n_s][F]
+    const std::vector<double>* mass;       // [n_s][V] caller numbering
+    const uint8_t* fixed;                  // caller numbering or null
+    const ens::Fans* fans;                 // matrix-free only
+    const std::vector<int32_t>* contrib_ptr;   // [nnzb + 1] (assembled only)
+    const std::vector<int32_t>* contrib;       // e * 9 + a * 3 + b
+};
 
-extern "C" {
+int build_part(ens_ctx* c, Part& P, const Global& G) {
+    const auto& pl = P.plan;
+    const auto& pat = *G.pat;
+    const int64_t n_s = c->n_s, lo = pl.lo, hi = pl.hi;
+    P.n_own = hi - lo;
+    P.n_gh = int64_t(pl.ghosts.size());
+    const int64_t n_loc = P.n_own + P.n_gh;
+    auto local = [&](int32_t g) -> int32_t {
+        if (g >= lo && g < hi) return int32_t(g - lo);
+        auto it = std::lower_bound(pl.ghosts.begin(), pl.ghosts.end(), g);
+        return int32_t(P.n_own + (it - pl.ghosts.begin()));
+    };
+    // maps local row -> caller node id
+    std::vector<int32_t> map_all(static_cast<size_t>(n_loc));
+    for (int64_t i = 0; i < P.n_own; ++i) map_all[size_t(i)] = pat.perm[size_t(lo + i)];
+    for (int64_t k = 0; k < P.n_gh; ++k) map_all[size_t(P.n_own + k)] = pat.perm[size_t(pl.ghosts[size_t(k)])];
+    P.map_own.assign(map_all.begin(), map_all.begin() + P.n_own);
+    // pattern of the owned rows, columns local, each row in its GLOBAL column order
+    const int64_t b0 = pat.row_ptr[size_t(lo)], b1 = pat.row_ptr[size_t(hi)];
+    std::vector<int32_t> rp(size_t(P.n_own) + 1), cl(size_t(b1 - b0));
+    for (int64_t i = 0; i <= P.n_own; ++i) rp[size_t(i)] = int32_t(pat.row_ptr[size_t(lo + i)] - b0);
+    for (int64_t b = b0; b < b1; ++b) cl[size_t(b - b0)] = local(pat.col[size_t(b)]);
+    // coefficients of the owned rows
+    std::vector<double> c1(size_t(P.n_own * n_s)), c2a, c3a;
+    if (c->damping == ENS_DAMP_IDENTITY) { c2a.resize(c1.size()); c3a.resize(c1.size()); }
+    const double dt = c->dt;
+    for (int64_t i = 0; i < P.n_own; ++i)
+        for (int64_t s = 0; s < n_s; ++s) {
+            const double mi = (*G.mass)[size_t(s * c->V + map_all[size_t(i)])];
+            const double cc = c->damping == ENS_DAMP_MASS ? c->c_d * mi : (c->damping == ENS_DAMP_IDENTITY ? c->c_d : 0.0);
+            const double D = mi + 0.5 * dt * cc;
+            c1[size_t(i * n_s + s)] = dt * dt / D;
+            if (c->damping == ENS_DAMP_IDENTITY) {
+                c2a[size_t(i * n_s + s)] = 2.0 * mi / D;
+                c3a[size_t(i * n_s + s)] = (mi - 0.5 * dt * cc) / D;
+            }
+        }
+    std::vector<uint8_t> fx(size_t(P.n_own), 0);
+    if (G.fixed)
+        for (int64_t i = 0; i < P.n_own; ++i) fx[size_t(i)] = G.fixed[map_all[size_t(i)]] & 7;
+    RC_TRY(upload(c, &P.d_row_ptr, rp.data(), rp.size()));
+    RC_TRY(upload(c, &P.d_col, cl.data(), cl.size()));
+    RC_TRY(upload(c, &P.d_map_own, map_all.data(), size_t(P.n_own)));
+    RC_TRY(upload(c, &P.d_map_all, map_all.data(), map_all.size()));
+    if (c->nccl_comm) {        // one part per process: owned rows in local order (ens_get_owned)
+        std::vector<int32_t> ident(size_t(P.n_own));
+        for (int64_t i = 0; i < P.n_own; ++i) ident[size_t(i)] = int32_t(i);
+        RC_TRY(upload(c, &P.d_map_abi, ident.data(), ident.size()));
+    } else {
+        P.d_map_abi = P.d_map_own;
+    }
+    RC_TRY(upload(c, &P.d_fixed, fx.data(), fx.size()));
+    RC_TRY(upload(c, &P.d_c1, c1.data(), c1.size()));
+    if (c->damping == ENS_DAMP_IDENTITY) {
+        RC_TRY(upload(c, &P.d_c2a, c2a.data(), c2a.size()));
+        RC_TRY(upload(c, &P.d_c3a, c3a.data(), c3a.size()));
+    }
+    if (!pl.send_rows.empty()) {
+        RC_TRY(upload(c, &P.d_send_rows, pl.send_rows.data(), pl.send_rows.size()));
+        RC_TRY(dalloc(c, &P.d_sendbuf, pl.send_rows.size() * 3 * size_t(n_s)));
+    }
+    // elements touching the owned rows -> local element ids
+    std::vector<int32_t> elems;
+    if (G.m->F) {
+        std::vector<char> mark(size_t(G.m->F), 0);
+        for (int64_t e = 0; e < G.m->F; ++e)
+            for (int a = 0; a < 3; ++a) {
+                int32_t g = pat.iperm[size_t(G.m->tris[3 * e + a])];
+                if (g >= lo && g < hi) mark[size_t(e)] = 1;
+            }
+        for (int64_t e = 0; e < G.m->F; ++e)
+            if (mark[size_t(e)]) elems.push_back(int32_t(e));
+    }
+    std::vector<int32_t> eloc(size_t(G.m->F), -1);
+    for (size_t k = 0; k < elems.size(); ++k) eloc[size_t(elems[k])] = int32_t(k);
+    const int64_t Fl = int64_t(elems.size());
+    std::vector<double> al(size_t(Fl * n_s));
+    for (int64_t k = 0; k < Fl; ++k)
+        for (int64_t s = 0; s < n_s; ++s) al[size_t(k * n_s + s)] = (*G.alpha)[size_t(s * G.m->F + elems[size_t(k)])];
+    if (c->kernel == ENS_KERNEL_ASSEMBLED) {
+        // F0 on the owned blocks: contributions re-indexed to local elements
+        std::vector<int32_t> cp(size_t(b1 - b0) + 1), cc;
+        const auto& gcp = *G.contrib_ptr;
+        const auto& gc = *G.contrib;
+        for (int64_t b = b0; b < b1; ++b) {
+            cp[size_t(b - b0)] = int32_t(cc.size());
+            for (int32_t q = gcp[size_t(b)]; q < gcp[size_t(b) + 1]; ++q)
+                cc.push_back(eloc[size_t(gc[size_t(q)] / 9)] * 9 + gc[size_t(q)] % 9);
+        }
+        cp[size_t(b1 - b0)] = int32_t(cc.size());
+        std::vector<double> kh(size_t(Fl) * 81);
+        for (int64_t k = 0; k < Fl; ++k)
+            std::copy_n(G.Khat->data() + size_t(elems[size_t(k)]) * 81, 81, kh.data() + size_t(k) * 81);
+        int32_t *d_cp = nullptr, *d_cc = nullptr;
+        double *d_al = nullptr, *d_kh = nullptr;
+        RC_TRY(upload(c, &d_cp, cp.data(), cp.size()));
+        RC_TRY(upload(c, &d_cc, cc.data(), cc.size()));
+        RC_TRY(upload(c, &d_al, al.data(), al.size()));
+        RC_TRY(upload(c, &d_kh, kh.data(), kh.size()));
+        RC_TRY(dalloc(c, &P.d_Kval, size_t(b1 - b0) * 9 * size_t(n_s)));
+        CUDA_TRY(c, ens::launch_assemble(b1 - b0, c->n_s, d_cp, d_cc, d_al, d_kh, P.d_Kval, c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        dfree(c, d_cp);
+        dfree(c, d_cc);
+        dfree(c, d_al);
+        dfree(c, d_kh);
+    } else {
+        const ens::Fans& fans = *G.fans;
+        const int32_t k0 = fans.ptr[size_t(lo)], k1 = fans.ptr[size_t(hi)];
+        std::vector<int32_t> ip(size_t(P.n_own) + 1);
+        for (int64_t i = 0; i <= P.n_own; ++i) ip[size_t(i)] = fans.ptr[size_t(lo + i)] - k0;
+        std::vector<ens::FanRec> rec(fans.rec.begin() + k0, fans.rec.begin() + k1);
+        for (auto& r : rec) {
+            r.e = eloc[size_t(r.e)];
+            r.n_prev = local(r.n_prev);
+            r.n_next = local(r.n_next);
+        }
+        const int Pg = c->n_s / ens::pick_vec_mf(c->n_s);
+        P.mf_groups = std::min(Pg, 256);
+        P.mf_rows = std::max(1, std::min(256 / P.mf_groups, 32));
+        for (;;) {
+            int32_t mx = 0;
+            for (int64_t r0 = 0; r0 < P.n_own; r0 += P.mf_rows) {
+                const int64_t r1 = std::min<int64_t>(r0 + P.mf_rows, P.n_own);
+                mx = std::max(mx, ip[size_t(r1)] - ip[size_t(r0)]);
+            }
+            P.mf_smem_inc = mx;
+            if (int64_t(mx) * 240 <= 96 * 1024 || P.mf_rows == 1) break;
+            P.mf_rows = std::max(1, P.mf_rows / 2);
+        }
+        if (int64_t(P.mf_smem_inc) * 240 > 200 * 1024)
+            return fail(c, ENS_E_UNSUPPORTED, "a node has too many incident elements for the matrix-free kernel");
+        static_assert(sizeof(ens::FanRec) == sizeof(int4), "FanRec layout");
+        RC_TRY(upload(c, &P.d_inc_ptr, ip.data(), ip.size()));
+        RC_TRY(upload(c, &P.d_fan, reinterpret_cast<const int4*>(rec.data()), rec.size()));
+        RC_TRY(upload(c, &P.d_Krow, fans.Krow.data() + size_t(k0) * 28, size_t(k1 - k0) * 28));
+        RC_TRY(upload(c, &P.d_alpha, al.data(), al.size()));
+    }
+    const size_t ns = size_t(n_loc) * 3 * size_t(n_s);
+    RC_TRY(dalloc(c, &P.d_u0, ns));
+    RC_TRY(dalloc(c, &P.d_u1, ns));
+    CUDA_TRY(c, cudaMemsetAsync(P.d_u0, 0, ns * sizeof(double), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(P.d_u1, 0, ns * sizeof(double), c->stream));
+    return ENS_OK;
+}
 
-int ens_create(const ens_mesh* mesh, const ens_materials* mat, const ens_options* opt, ens_ctx** out) {
-    if (!out) return fail(nullptr, ENS_E_ARG, "out is NULL");
-    *out = nullptr;
-    if (!mesh || !mat) return fail(nullptr, ENS_E_ARG, "mesh or materials is NULL");
-    if (mesh->n_nodes < 1 || mesh->n_tris < 1 || !mesh->xyz || !mesh->tris)
-        return fail(nullptr, ENS_E_ARG, "mesh needs n_nodes >= 1, n_tris >= 1, xyz and tris");
-    if (mesh->n_nodes >= (int64_t(1) << 31) || 3 * mesh->n_tris >= (int64_t(1) << 31))
-        return fail(nullptr, ENS_E_ARG, "mesh too large for 32-bit node / element ids");
-    if (mat->n_s < 1 || !mat->E || !mat->h) return fail(nullptr, ENS_E_ARG, "materials need n_s >= 1, E and h");
-    if (!(mat->rho > 0.0) || !std::isfinite(mat->rho)) return fail(nullptr, ENS_E_ARG, "rho must be > 0");
-    if (!(mat->nu >= 0.0 && mat->nu <= 0.5)) return fail(nullptr, ENS_E_ARG, "nu must lie in [0, 0.5]");
-    if (!(mat->k_shear > 0.0) || !std::isfinite(mat->k_shear)) return fail(nullptr, ENS_E_ARG, "k_shear must be > 0");
-    int rc = check_opts(opt);
-    if (rc) return rc;
+int finish_create(ens_ctx* c) {
+    RC_TRY(dalloc(c, &c->d_stage, size_t(c->V) * 3 * size_t(c->n_s)));
+    RC_TRY(dalloc(c, &c->d_flag, 1));
+    RC_TRY(dalloc(c, &c->d_step, 1));
+    CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0xff, sizeof(unsigned long long), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->d_step, 0, sizeof(int64_t), c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    c->step = 0;
+    return ENS_OK;
+}
+
+int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, const ens_options* opt) {
     const int64_t V = mesh->n_nodes, F = mesh->n_tris, NV = int64_t(mat->n_s) * V;
-    for (int64_t k = 0; k < NV; ++k) {
-        if (!(mat->E[k] > 0.0) || !std::isfinite(mat->E[k]))
-            return fail(nullptr, ENS_E_ARG, "E[" + std::to_string(k / V) + "][" + std::to_string(k % V) + "] must be finite and > 0");
-        if (!(mat->h[k] > 0.0) || !std::isfinite(mat->h[k]))
-            return fail(nullptr, ENS_E_ARG, "h[" + std::to_string(k / V) + "][" + std::to_string(k % V) + "] must be finite and > 0");
-    }
     ens::MeshView m{V, F, mesh->xyz, mesh->tris};
-    int64_t bad = -1;
-    int vcode = ens::validate_mesh(m, &bad);
-    if (vcode) {
-        static const char* what[] = {"", "node index out of range in element ", "repeated node in element ",
-                                     "degenerate (zero-area) element ", "edge shared by more than two triangles at node "};
-        return fail(nullptr, ENS_E_MESH, std::string(what[vcode]) + std::to_string(bad));
-    }
-
-    ens_ctx* c = new ens_ctx();
-    if ((rc = init_ctx(c, opt))) { delete c; return rc; }
+    RC_TRY(init_ctx(c, opt));
     c->V = V;
     c->F = F;
     c->n_s = mat->n_s;
@@ -381,9 +536,9 @@ int ens_create(const ens_mesh* mesh, const ens_materials* mat, const ens_options
     c->bandwidth = pat.bandwidth;
     c->perm = pat.perm;
     c->iperm = pat.iperm;
-    if (c->nnzb >= (int64_t(1) << 31)) { delete c; return fail(nullptr, ENS_E_ARG, "pattern exceeds 2^31 blocks"); }
+    if (c->nnzb >= (int64_t(1) << 31)) return fail(c, ENS_E_ARG, "pattern exceeds 2^31 blocks");
 
-    // S1: element stiffness, Gauss-point scaling, mass, CFL, coefficients
+    // S1: element stiffness, Gauss-point scaling, mass, CFL
     std::vector<double> Khat(size_t(81 * F)), area(static_cast<size_t>(F));
     for (int64_t e = 0; e < F; ++e)
         ens::element_stiffness(mesh->xyz + 3 * int64_t(mesh->tris[3 * e]), mesh->xyz + 3 * int64_t(mesh->tris[3 * e + 1]),
@@ -391,47 +546,108 @@ int ens_create(const ens_mesh* mesh, const ens_materials* mat, const ens_options
                                Khat.data() + 81 * e, area.data() + e);
     std::vector<double> alpha(size_t(mat->n_s * F)), mass(static_cast<size_t>(NV));
     ens::materials(m, mat->n_s, mat->E, mat->h, mat->rho, alpha.data(), mass.data());
-    double safety = (opt && opt->cfl_safety > 0.0) ? opt->cfl_safety : 0.9;
+    const double safety = (opt && opt->cfl_safety > 0.0) ? opt->cfl_safety : 0.9;
     c->dt_cfl = ens::cfl_dt(m, mat->n_s, mat->E, mat->rho, safety);
     c->dt = (opt && opt->dt > 0.0) ? opt->dt : c->dt_cfl;
-
-    const int64_t n_s = c->n_s;
-    const double dt = c->dt;
-    std::vector<double> c1(static_cast<size_t>(NV)), c2a, c3a;
-    if (c->damping == ENS_DAMP_IDENTITY) { c2a.resize(size_t(NV)); c3a.resize(size_t(NV)); }
-    for (int64_t i = 0; i < V; ++i)
-        for (int64_t s = 0; s < n_s; ++s) {
-            const double mi = mass[size_t(s * V + pat.perm[size_t(i)])];
-            double cc = c->damping == ENS_DAMP_MASS ? c->c_d * mi : (c->damping == ENS_DAMP_IDENTITY ? c->c_d : 0.0);
-            double D = mi + 0.5 * dt * cc;
-            c1[size_t(i * n_s + s)] = dt * dt / D;
-            if (c->damping == ENS_DAMP_IDENTITY) {
-                c2a[size_t(i * n_s + s)] = 2.0 * mi / D;
-                c3a[size_t(i * n_s + s)] = (mi - 0.5 * dt * cc) / D;
-            }
-        }
-    if (c->damping == ENS_DAMP_MASS) {      // C~ = c_d M~: c2, c3 independent of the node
-        double q = 0.5 * dt * c->c_d;
+    if (c->damping == ENS_DAMP_MASS) {       // C~ = c_d M~: c2, c3 independent of the node
+        const double q = 0.5 * c->dt * c->c_d;
         c->c2 = 2.0 / (1.0 + q);
         c->c3 = (1.0 - q) / (1.0 + q);
     }
-    std::vector<int32_t> rp32(pat.row_ptr.begin(), pat.row_ptr.end());
-    std::vector<uint8_t> fixed(size_t(V), 0);
-    if (mesh->fixed)
-        for (int64_t i = 0; i < V; ++i) fixed[size_t(i)] = mesh->fixed[pat.perm[size_t(i)]] & 7;
 
-    if ((rc = upload(c, &c->d_row_ptr, rp32.data(), rp32.size())) || (rc = upload(c, &c->d_col, pat.col.data(), pat.col.size())) ||
-        (rc = upload(c, &c->d_perm, pat.perm.data(), pat.perm.size())) || (rc = upload(c, &c->d_fixed, fixed.data(), fixed.size())) ||
-        (rc = upload(c, &c->d_c1, c1.data(), c1.size())) ||
-        (c->damping == ENS_DAMP_IDENTITY && ((rc = upload(c, &c->d_c2a, c2a.data(), c2a.size())) ||
-                                            (rc = upload(c, &c->d_c3a, c3a.data(), c3a.size())))) ||
-        (rc = build_device_operator(c, m, pat, Khat, alpha)) || (rc = finish_create(c, out))) {
-        std::string msg = c->err;
+    // element -> block contributions (assembled) or fans (matrix-free), global
+    std::vector<int32_t> cptr, contrib;
+    ens::Fans fans;
+    if (c->kernel == ENS_KERNEL_ASSEMBLED) {
+        cptr.assign(size_t(c->nnzb) + 1, 0);
+        contrib.resize(size_t(9 * F));
+        std::vector<int32_t> blk(size_t(9 * F));
+        for (int64_t e = 0; e < F; ++e)
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b) {
+                    const int32_t i = pat.iperm[size_t(mesh->tris[3 * e + a])], j = pat.iperm[size_t(mesh->tris[3 * e + b])];
+                    auto first = pat.col.begin() + pat.row_ptr[size_t(i)];
+                    auto last = pat.col.begin() + pat.row_ptr[size_t(i) + 1];
+                    const int32_t bi = int32_t(std::lower_bound(first, last, j) - pat.col.begin());
+                    blk[size_t(9 * e + 3 * a + b)] = bi;
+                    cptr[size_t(bi) + 1]++;
+                }
+        for (size_t k = 1; k < cptr.size(); ++k) cptr[k] += cptr[k - 1];
+        std::vector<int32_t> fillp(cptr.begin(), cptr.end() - 1);
+        for (int64_t e = 0; e < F; ++e)                   // ascending e => ascending within a block
+            for (int ab = 0; ab < 9; ++ab) contrib[size_t(fillp[size_t(blk[size_t(9 * e + ab)])]++)] = int32_t(9 * e + ab);
+    } else {
+        fans = ens::build_fans(m, pat.iperm, Khat);
+    }
+
+    // partitions: one part unless node-partitioned; all parts here unless NCCL is used
+    const int32_t P = c->dist == ENS_DIST_NODE ? c->world : 1;
+    std::vector<ens::PartPlan> plans = P > 1 ? ens::halo_plan(pat.row_ptr, pat.col, P)
+                                             : std::vector<ens::PartPlan>(1);
+    if (P == 1) {
+        plans[0].lo = 0;
+        plans[0].hi = V;
+    }
+    Global G{&m, &pat, &Khat, &alpha, &mass, mesh->fixed, &fans, &cptr, &contrib};
+    if (c->nccl_comm && P > 1) {
+        c->parts.resize(1);
+        c->parts[0].plan = plans[size_t(c->rank)];
+    } else {
+        c->parts.resize(plans.size());
+        for (size_t k = 0; k < plans.size(); ++k) c->parts[k].plan = plans[k];
+    }
+    for (Part& p : c->parts) RC_TRY(build_part(c, p, G));
+    return finish_create(c);
+}
+
+int arg_check(const ens_mesh* mesh, const ens_materials* mat) {
+    if (!mesh || !mat) return fail(nullptr, ENS_E_ARG, "mesh or materials is NULL");
+    if (mesh->n_nodes < 1 || mesh->n_tris < 1 || !mesh->xyz || !mesh->tris)
+        return fail(nullptr, ENS_E_ARG, "mesh needs n_nodes >= 1, n_tris >= 1, xyz and tris");
+    if (mesh->n_nodes >= (int64_t(1) << 31) || 9 * mesh->n_tris >= (int64_t(1) << 31))
+        return fail(nullptr, ENS_E_ARG, "mesh too large for 32-bit node / element ids");
+    if (mat->n_s < 1 || !mat->E || !mat->h) return fail(nullptr, ENS_E_ARG, "materials need n_s >= 1, E and h");
+    if (mat->n_s >= (1 << 24)) return fail(nullptr, ENS_E_ARG, "n_s must be < 2^24");
+    if (!(mat->rho > 0.0) || !std::isfinite(mat->rho)) return fail(nullptr, ENS_E_ARG, "rho must be > 0");
+    if (!(mat->nu >= 0.0 && mat->nu <= 0.5)) return fail(nullptr, ENS_E_ARG, "nu must lie in [0, 0.5]");
+    if (!(mat->k_shear > 0.0) || !std::isfinite(mat->k_shear)) return fail(nullptr, ENS_E_ARG, "k_shear must be > 0");
+    const int64_t V = mesh->n_nodes, NV = int64_t(mat->n_s) * V;
+    for (int64_t k = 0; k < NV; ++k) {
+        if (!(mat->E[k] > 0.0) || !std::isfinite(mat->E[k]))
+            return fail(nullptr, ENS_E_ARG, "E[" + std::to_string(k / V) + "][" + std::to_string(k % V) + "] must be finite and > 0");
+        if (!(mat->h[k] > 0.0) || !std::isfinite(mat->h[k]))
+            return fail(nullptr, ENS_E_ARG, "h[" + std::to_string(k / V) + "][" + std::to_string(k % V) + "] must be finite and > 0");
+    }
+    ens::MeshView m{V, mesh->n_tris, mesh->xyz, mesh->tris};
+    int64_t bad = -1;
+    const int vcode = ens::validate_mesh(m, &bad);
+    if (vcode) {
+        static const char* what[] = {"", "node index out of range in element ", "repeated node in element ",
+                                     "degenerate (zero-area) element ", "edge shared by more than two triangles at node "};
+        return fail(nullptr, ENS_E_MESH, std::string(what[vcode]) + std::to_string(bad));
+    }
+    return ENS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ens_create(const ens_mesh* mesh, const ens_materials* mat, const ens_options* opt, ens_ctx** out) {
+    if (!out) return fail(nullptr, ENS_E_ARG, "out is NULL");
+    *out = nullptr;
+    RC_TRY(arg_check(mesh, mat));
+    RC_TRY(check_opts(opt));
+    ens_ctx* c = new ens_ctx();
+    const int rc = create_impl(c, mesh, mat, opt);
+    if (rc) {
+        const std::string msg = c->err;
         free_all(c);
         delete c;
         g_err = msg;
         return rc;
     }
+    *out = c;
     return ENS_OK;
 }
 
@@ -442,52 +658,73 @@ int ens_create_csr(int64_t n_nodes, const int64_t* row_ptr, const int32_t* col, 
     *out = nullptr;
     if (n_nodes < 1 || !row_ptr || !col || n_s < 1 || !Kval || !c1 || !c2 || !c3)
         return fail(nullptr, ENS_E_ARG, "ens_create_csr: bad arguments");
-    int rc = check_opts(opt);
-    if (rc) return rc;
-    if (opt && opt->kernel != ENS_KERNEL_ASSEMBLED) return fail(nullptr, ENS_E_ARG, "ens_create_csr needs kernel = ASSEMBLED");
+    RC_TRY(check_opts(opt));
+    if (opt && (opt->kernel != ENS_KERNEL_ASSEMBLED || opt->dist == ENS_DIST_NODE))
+        return fail(nullptr, ENS_E_ARG, "ens_create_csr needs kernel = ASSEMBLED, dist != NODE");
     const int64_t V = n_nodes, nnzb = row_ptr[V];
     for (int64_t i = 0; i < V; ++i)
         if (row_ptr[i + 1] < row_ptr[i]) return fail(nullptr, ENS_E_ARG, "row_ptr not monotone");
     for (int64_t b = 0; b < nnzb; ++b)
         if (col[b] < 0 || col[b] >= V) return fail(nullptr, ENS_E_ARG, "column index out of range");
     ens_ctx* c = new ens_ctx();
-    if ((rc = init_ctx(c, opt))) { delete c; return rc; }
-    c->kernel = ENS_KERNEL_ASSEMBLED;
-    c->damping = ENS_DAMP_IDENTITY;          // arbitrary per-DOF c2, c3 arrays
-    c->V = V;
-    c->F = 0;
-    c->nnzb = nnzb;
-    c->n_s = n_s;
-    c->dt = c->dt_cfl = dt;
-    c->perm.resize(size_t(V));
-    for (int64_t i = 0; i < V; ++i) c->perm[size_t(i)] = int32_t(i);
-    c->iperm = c->perm;
-    // caller layout -> device layout
-    std::vector<double> kv(size_t(nnzb * 9 * n_s)), a1(size_t(V * n_s)), a2(a1.size()), a3(a1.size());
-    for (int64_t s = 0; s < n_s; ++s) {
-        for (int64_t b = 0; b < nnzb; ++b)
-            for (int k = 0; k < 9; ++k) kv[size_t((b * 9 + k) * n_s + s)] = Kval[(s * nnzb + b) * 9 + k];
-        for (int64_t i = 0; i < V; ++i) {
-            a1[size_t(i * n_s + s)] = c1[s * V + i];
-            a2[size_t(i * n_s + s)] = c2[s * V + i];
-            a3[size_t(i * n_s + s)] = c3[s * V + i];
+    auto body = [&]() -> int {
+        RC_TRY(init_ctx(c, opt));
+        c->kernel = ENS_KERNEL_ASSEMBLED;
+        c->damping = ENS_DAMP_IDENTITY;      // arbitrary per-DOF c2, c3 arrays
+        c->V = V;
+        c->F = 0;
+        c->nnzb = nnzb;
+        c->n_s = n_s;
+        c->dt = c->dt_cfl = dt;
+        c->perm.resize(size_t(V));
+        for (int64_t i = 0; i < V; ++i) c->perm[size_t(i)] = int32_t(i);
+        c->iperm = c->perm;
+        c->parts.resize(1);
+        Part& P = c->parts[0];
+        P.plan.lo = 0;
+        P.plan.hi = V;
+        P.n_own = V;
+        P.map_own = c->perm;
+        std::vector<double> kv(size_t(nnzb * 9 * n_s)), a1(size_t(V * n_s)), a2(a1.size()), a3(a1.size());
+        for (int64_t s = 0; s < n_s; ++s) {
+            for (int64_t b = 0; b < nnzb; ++b)
+                for (int k = 0; k < 9; ++k) kv[size_t((b * 9 + k) * n_s + s)] = Kval[(s * nnzb + b) * 9 + k];
+            for (int64_t i = 0; i < V; ++i) {
+                a1[size_t(i * n_s + s)] = c1[s * V + i];
+                a2[size_t(i * n_s + s)] = c2[s * V + i];
+                a3[size_t(i * n_s + s)] = c3[s * V + i];
+            }
         }
-    }
-    std::vector<int32_t> rp32(row_ptr, row_ptr + V + 1);
-    std::vector<uint8_t> fx(size_t(V), 0);
-    if (fixed)
-        for (int64_t i = 0; i < V; ++i) fx[size_t(i)] = fixed[i] & 7;
-    if ((rc = upload(c, &c->d_row_ptr, rp32.data(), rp32.size())) || (rc = upload(c, &c->d_col, col, size_t(nnzb))) ||
-        (rc = upload(c, &c->d_perm, c->perm.data(), c->perm.size())) || (rc = upload(c, &c->d_fixed, fx.data(), fx.size())) ||
-        (rc = upload(c, &c->d_Kval, kv.data(), kv.size())) || (rc = upload(c, &c->d_c1, a1.data(), a1.size())) ||
-        (rc = upload(c, &c->d_c2a, a2.data(), a2.size())) || (rc = upload(c, &c->d_c3a, a3.data(), a3.size())) ||
-        (rc = finish_create(c, out))) {
-        std::string msg = c->err;
+        std::vector<int32_t> rp32(row_ptr, row_ptr + V + 1);
+        std::vector<uint8_t> fx(size_t(V), 0);
+        if (fixed)
+            for (int64_t i = 0; i < V; ++i) fx[size_t(i)] = fixed[i] & 7;
+        RC_TRY(upload(c, &P.d_row_ptr, rp32.data(), rp32.size()));
+        RC_TRY(upload(c, &P.d_col, col, size_t(nnzb)));
+        RC_TRY(upload(c, &P.d_map_own, c->perm.data(), c->perm.size()));
+        RC_TRY(upload(c, &P.d_map_all, c->perm.data(), c->perm.size()));
+        P.d_map_abi = P.d_map_own;
+        RC_TRY(upload(c, &P.d_fixed, fx.data(), fx.size()));
+        RC_TRY(upload(c, &P.d_Kval, kv.data(), kv.size()));
+        RC_TRY(upload(c, &P.d_c1, a1.data(), a1.size()));
+        RC_TRY(upload(c, &P.d_c2a, a2.data(), a2.size()));
+        RC_TRY(upload(c, &P.d_c3a, a3.data(), a3.size()));
+        const size_t ns = size_t(V) * 3 * size_t(n_s);
+        RC_TRY(dalloc(c, &P.d_u0, ns));
+        RC_TRY(dalloc(c, &P.d_u1, ns));
+        CUDA_TRY(c, cudaMemsetAsync(P.d_u0, 0, ns * sizeof(double), c->stream));
+        CUDA_TRY(c, cudaMemsetAsync(P.d_u1, 0, ns * sizeof(double), c->stream));
+        return finish_create(c);
+    };
+    const int rc = body();
+    if (rc) {
+        const std::string msg = c->err;
         free_all(c);
         delete c;
         g_err = msg;
         return rc;
     }
+    *out = c;
     return ENS_OK;
 }
 
@@ -500,24 +737,24 @@ int ens_set_traction(ens_ctx* c, int32_t n_fields, const double* F, int32_t n_ta
     for (int32_t k = 0; k + 1 < n_tab; ++k)
         if (!(tab_t[k] < tab_t[k + 1])) return fail(c, ENS_E_ARG, "tab_t must be strictly increasing");
     if (!std::isfinite(period) || !std::isfinite(ramp_T)) return fail(c, ENS_E_ARG, "period / ramp_T not finite");
-    const int64_t V = c->V;
-    std::vector<double> Fd(size_t(n_fields * V * 3));
-    for (int32_t k = 0; k < n_fields; ++k)
-        for (int64_t i = 0; i < V; ++i)
-            for (int d = 0; d < 3; ++d) Fd[size_t((k * V + i) * 3 + d)] = F[(k * V + c->perm[size_t(i)]) * 3 + d];
-    // (re)allocate: sizes may change; keep previous buffers alive until the stream drains
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));       // old buffers may still be in use
     drop_graph(c);
-    dfree(c, c->d_Fk);
-    dfree(c, c->d_tab_t);
-    dfree(c, c->d_tab_g);
     c->n_fields = 0;
     c->n_tab = 0;
-    int rc;
-    if ((rc = upload(c, &c->d_Fk, Fd.data(), Fd.size()))) return rc;
+    dfree(c, c->d_tab_t);
+    dfree(c, c->d_tab_g);
+    for (Part& p : c->parts) {
+        dfree(c, p.d_Fk);
+        std::vector<double> Fd(size_t(n_fields * p.n_own * 3));
+        for (int32_t k = 0; k < n_fields; ++k)
+            for (int64_t i = 0; i < p.n_own; ++i)
+                for (int d = 0; d < 3; ++d)
+                    Fd[size_t((k * p.n_own + i) * 3 + d)] = F[(k * c->V + p.map_own[size_t(i)]) * 3 + d];
+        RC_TRY(upload(c, &p.d_Fk, Fd.data(), Fd.size()));
+    }
     if (n_tab > 0) {
-        if ((rc = upload(c, &c->d_tab_t, tab_t, size_t(n_tab))) || (rc = upload(c, &c->d_tab_g, tab_g, size_t(n_tab) * n_fields)))
-            return rc;
+        RC_TRY(upload(c, &c->d_tab_t, tab_t, size_t(n_tab)));
+        RC_TRY(upload(c, &c->d_tab_g, tab_g, size_t(n_tab) * size_t(n_fields)));
     }
     c->n_fields = n_fields;
     c->n_tab = n_tab;
@@ -531,26 +768,23 @@ int ens_step(ens_ctx* c, int64_t n) {
     if (n < 0) return fail(c, ENS_E_ARG, "n must be >= 0");
     if (c->latched) return fail(c, ENS_E_STATE, "context diverged: call ens_set_state before stepping again");
     int64_t left = n;
-    if (c->graph_steps > 0 && n >= c->graph_steps) {
-        if (c->graph_dirty) {
-            int rc = build_graph(c);
-            if (rc) return rc;
+    if (c->graph_steps > 0 && n >= c->graph_steps && !c->has_halo()) {
+        if (c->graph_dirty) RC_TRY(build_graph(c));
+        for (; left >= c->graph_steps; left -= c->graph_steps) {
+            CUDA_TRY(c, cudaGraphLaunch(c->graph, c->stream));
+            c->step += c->graph_steps;
         }
-        for (; left >= c->graph_steps; left -= c->graph_steps) CUDA_TRY(c, cudaGraphLaunch(c->graph, c->stream));
     }
-    ens::StepArgs a = step_args(c);
-    for (int64_t k = 0; k < left; ++k) {
-        a.step_off = k;
-        CUDA_TRY(c, launch(c, a));
-    }
+    for (int64_t k = 0; k < left; ++k) RC_TRY(enqueue_step(c, k, c->stream));
     if (left) CUDA_TRY(c, ens::launch_advance(c->d_step, left, c->stream));
-    c->step += n;
+    c->step += left;
     return ENS_OK;
 }
 
 int ens_sync(ens_ctx* c) {
     if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->comm_stream) CUDA_TRY(c, cudaStreamSynchronize(c->comm_stream));
     unsigned long long flag = 0;
     CUDA_TRY(c, cudaMemcpy(&flag, c->d_flag, sizeof(flag), cudaMemcpyDeviceToHost));
     if (flag != ~0ull) {
@@ -561,17 +795,21 @@ int ens_sync(ens_ctx* c) {
     return ENS_OK;
 }
 
+static int64_t abi_rows(const ens_ctx* c) { return c->nccl_comm ? c->parts[0].n_own : c->V; }
+
 int ens_get_state(ens_ctx* c, double* u_n, double* u_nm1, double* t, int64_t* step) {
     if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
-    int rc = ens_sync(c);
-    const size_t n = size_t(c->V) * 3 * size_t(c->n_s);
-    double* cur = (c->step & 1) ? c->d_u1 : c->d_u0;
-    double* old = (c->step & 1) ? c->d_u0 : c->d_u1;
+    const int rc = ens_sync(c);
+    if (rc && rc != ENS_E_DIVERGED) return rc;
+    const int64_t Vabi = abi_rows(c);
+    const size_t n = size_t(Vabi) * 3 * size_t(c->n_s);
     double* outs[2] = {u_n, u_nm1};
-    double* srcs[2] = {cur, old};
     for (int k = 0; k < 2; ++k) {
         if (!outs[k]) continue;
-        CUDA_TRY(c, ens::launch_dev_to_abi(c->V, c->n_s, c->d_perm, srcs[k], c->d_stage, c->stream));
+        for (Part& p : c->parts) {
+            double* src = ((c->step + k) & 1) ? p.d_u1 : p.d_u0;     // u_n = buf[step & 1]
+            CUDA_TRY(c, ens::launch_dev_to_abi(p.n_own, c->n_s, p.d_map_abi, Vabi, src, c->d_stage, c->stream));
+        }
         CUDA_TRY(c, cudaMemcpyAsync(outs[k], c->d_stage, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     }
@@ -580,23 +818,33 @@ int ens_get_state(ens_ctx* c, double* u_n, double* u_nm1, double* t, int64_t* st
     return rc;
 }
 
+int ens_get_owned(const ens_ctx* c, int32_t* node_ids, int64_t* n) {
+    if (!c || !n) return fail(nullptr, ENS_E_ARG, "NULL argument");
+    *n = abi_rows(c);
+    if (node_ids) {
+        if (c->nccl_comm) std::copy(c->parts[0].map_own.begin(), c->parts[0].map_own.end(), node_ids);
+        else
+            for (int64_t i = 0; i < c->V; ++i) node_ids[i] = int32_t(i);
+    }
+    return ENS_OK;
+}
+
 int ens_set_state(ens_ctx* c, const double* u_n, const double* u_nm1, double t, int64_t step) {
     if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
     if (step < 0) return fail(c, ENS_E_ARG, "step must be >= 0");
     (void)t;   // t = step * dt by construction
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->comm_stream) CUDA_TRY(c, cudaStreamSynchronize(c->comm_stream));
     const size_t n = size_t(c->V) * 3 * size_t(c->n_s);
-    double* cur = (step & 1) ? c->d_u1 : c->d_u0;
-    double* old = (step & 1) ? c->d_u0 : c->d_u1;
     const double* ins[2] = {u_n, u_nm1};
-    double* dsts[2] = {cur, old};
     for (int k = 0; k < 2; ++k) {
-        if (!ins[k]) {
-            CUDA_TRY(c, cudaMemsetAsync(dsts[k], 0, n * sizeof(double), c->stream));
-            continue;
+        if (ins[k]) CUDA_TRY(c, cudaMemcpyAsync(c->d_stage, ins[k], n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        for (Part& p : c->parts) {
+            double* dst = ((step + k) & 1) ? p.d_u1 : p.d_u0;
+            const int64_t rows = p.n_own + p.n_gh;
+            if (!ins[k]) CUDA_TRY(c, cudaMemsetAsync(dst, 0, size_t(rows) * 3 * size_t(c->n_s) * sizeof(double), c->stream));
+            else CUDA_TRY(c, ens::launch_abi_to_dev(rows, c->n_s, p.d_map_all, c->V, c->d_stage, dst, c->stream));
         }
-        CUDA_TRY(c, cudaMemcpyAsync(c->d_stage, ins[k], n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        CUDA_TRY(c, ens::launch_abi_to_dev(c->V, c->n_s, c->d_perm, c->d_stage, dsts[k], c->stream));
         CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     }
     static thread_local int64_t h_step;
@@ -611,17 +859,27 @@ int ens_set_state(ens_ctx* c, const double* u_n, const double* u_nm1, double t, 
 
 int ens_apply_stiffness(ens_ctx* c, const double* u, double* y) {
     if (!c || !u || !y) return fail(c, ENS_E_ARG, "ens_apply_stiffness: NULL argument");
-    const size_t n = size_t(c->V) * 3 * size_t(c->n_s);
-    int rc;
-    if (!c->d_scratch_u && ((rc = dalloc(c, &c->d_scratch_u, n)) || (rc = dalloc(c, &c->d_scratch_y, n)))) return rc;
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_stage, u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(c, ens::launch_abi_to_dev(c->V, c->n_s, c->d_perm, c->d_stage, c->d_scratch_u, c->stream));
-    ens::StepArgs a = step_args(c);
-    a.ubuf0 = a.ubuf1 = c->d_scratch_u;
-    a.y_out = c->d_scratch_y;
-    CUDA_TRY(c, launch(c, a));
-    CUDA_TRY(c, ens::launch_dev_to_abi(c->V, c->n_s, c->d_perm, c->d_scratch_y, c->d_stage, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(y, c->d_stage, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    const size_t nfull = size_t(c->V) * 3 * size_t(c->n_s);
+    CUDA_TRY(c, cudaMemcpyAsync(c->d_stage, u, nfull * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    for (Part& p : c->parts) {
+        const int64_t rows = p.n_own + p.n_gh;
+        if (!p.d_scratch_u) {
+            RC_TRY(dalloc(c, &p.d_scratch_u, size_t(rows) * 3 * size_t(c->n_s)));
+            RC_TRY(dalloc(c, &p.d_scratch_y, size_t(p.n_own) * 3 * size_t(c->n_s)));
+        }
+        CUDA_TRY(c, ens::launch_abi_to_dev(rows, c->n_s, p.d_map_all, c->V, c->d_stage, p.d_scratch_u, c->stream));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    const int64_t Vabi = abi_rows(c);
+    for (Part& p : c->parts) {
+        ens::StepArgs a = part_args(c, p);
+        a.ubuf0 = a.ubuf1 = p.d_scratch_u;
+        a.y_out = p.d_scratch_y;
+        CUDA_TRY(c, launch_rows(c, a, 0, p.n_own, c->stream));
+        CUDA_TRY(c, ens::launch_dev_to_abi(p.n_own, c->n_s, p.d_map_abi, Vabi, p.d_scratch_y, c->d_stage, c->stream));
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(y, c->d_stage, size_t(Vabi) * 3 * size_t(c->n_s) * sizeof(double),
+                                cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return ENS_OK;
 }
@@ -641,24 +899,36 @@ int ens_query(const ens_ctx* c, ens_info* info) {
     info->step = c->step;
     info->device_bytes = c->device_bytes;
     info->rcm_bandwidth = c->bandwidth;
-    info->launches_per_step = 1;
-    info->graph_steps = c->graph_steps;
-    // algorithmic bytes: values + state read/read/write + c1 (+ c2, c3)
-    const int64_t ns = c->n_s, per_node_state = 3 * 8 * 3 + 8 + (c->d_c2a ? 16 : 0);
+    info->graph_steps = c->has_halo() ? 0 : c->graph_steps;
+    // algorithmic HBM bytes of the rows this context advances: values +
+    // u_n, u_{n-1} read, u_{n+1} written, c1 (+ c2, c3) per node per realisation
+    const int64_t ns = c->n_s, per_node = 3 * 8 * 3 + 8 + (c->damping == ENS_DAMP_IDENTITY ? 16 : 0);
+    int64_t own = 0, blocks = 0, inc = 0, halo = 0, launches = 0;
+    for (const Part& p : c->parts) {
+        own += p.n_own;
+        blocks += (c->kernel == ENS_KERNEL_ASSEMBLED) ? 0 : 0;
+        halo += int64_t(p.plan.send_rows.size());
+        for (const auto& pe : p.plan.peers) halo += pe.recv_n;
+        launches += c->has_halo() ? (1 + (p.plan.b_lo > 0) + (p.plan.b_hi > 0) + !p.plan.send_rows.empty()) : 1;
+    }
+    (void)blocks;
+    (void)inc;
+    info->n_owned = own;
+    info->halo_bytes_per_step = halo * 3 * 8 * ns;
+    info->launches_per_step = int32_t(launches);
+    const double frac = c->V ? double(own) / double(c->V) : 1.0;
     if (c->kernel == ENS_KERNEL_ASSEMBLED) {
-        info->bytes_per_step = ns * (72 * c->nnzb + per_node_state * c->V);
-        info->flops_per_step = ns * (18 * c->nnzb + 3 * 5 * c->V);
+        info->bytes_per_step = int64_t(frac * double(ns * (72 * c->nnzb + per_node * c->V)));
+        info->flops_per_step = int64_t(frac * double(ns * (18 * c->nnzb + 3 * 5 * c->V)));
     } else {
-        info->bytes_per_step = ns * (8 * c->F + per_node_state * c->V) + 648 * c->F;
-        info->flops_per_step = ns * (3 * c->F * 60 + 3 * 5 * c->V);
+        info->bytes_per_step = int64_t(frac * double(ns * (8 * c->F + per_node * c->V) + 648 * c->F));
+        info->flops_per_step = int64_t(frac * double(ns * (3 * c->F * 60 + 3 * 5 * c->V)));
     }
     return ENS_OK;
 }
 
 void ens_destroy(ens_ctx* c) {
     if (!c) return;
-    if (c->stream) cudaStreamSynchronize(c->stream);
-    drop_graph(c);
     free_all(c);
     delete c;
 }
@@ -671,7 +941,7 @@ int ens_host_validate(int64_t n_nodes, int64_t n_tris, const double* xyz, const 
                       int64_t* bad) {
     ens::MeshView m{n_nodes, n_tris, xyz, tris};
     int64_t b = -1;
-    int v = ens::validate_mesh(m, &b);
+    const int v = ens::validate_mesh(m, &b);
     if (code) *code = v;
     if (bad) *bad = b;
     return v ? ENS_E_MESH : ENS_OK;
@@ -680,7 +950,7 @@ int ens_host_validate(int64_t n_nodes, int64_t n_tris, const double* xyz, const 
 int ens_host_pattern(int64_t n_nodes, int64_t n_tris, const int32_t* tris, int32_t* perm, int64_t* row_ptr,
                      int32_t* col, int64_t col_cap, int64_t* nnzb) {
     ens::MeshView m{n_nodes, n_tris, nullptr, tris};
-    ens::Pattern p = ens::build_pattern(m);
+    const ens::Pattern p = ens::build_pattern(m);
     *nnzb = int64_t(p.col.size());
     if (*nnzb > col_cap) return fail(nullptr, ENS_E_ARG, "col_cap too small");
     std::copy(p.perm.begin(), p.perm.end(), perm);
@@ -691,20 +961,47 @@ int ens_host_pattern(int64_t n_nodes, int64_t n_tris, const int32_t* tris, int32
 
 int ens_host_partition(int64_t n_nodes, const int64_t* row_ptr, int32_t n_parts, int64_t* bounds) {
     if (n_parts < 1) return fail(nullptr, ENS_E_ARG, "n_parts must be >= 1");
-    std::vector<int64_t> rp(row_ptr, row_ptr + n_nodes + 1);
-    auto b = ens::partition_bounds(rp, n_parts);
+    const std::vector<int64_t> rp(row_ptr, row_ptr + n_nodes + 1);
+    const auto b = ens::partition_bounds(rp, n_parts);
     std::copy(b.begin(), b.end(), bounds);
     return ENS_OK;
 }
 
 int ens_host_ghosts(int64_t n_nodes, const int64_t* row_ptr, const int32_t* col, int64_t lo, int64_t hi,
                     int32_t* ghosts, int64_t cap, int64_t* n) {
-    std::vector<int64_t> rp(row_ptr, row_ptr + n_nodes + 1);
-    std::vector<int32_t> cl(col, col + row_ptr[n_nodes]);
-    auto g = ens::ghost_rows(rp, cl, lo, hi);
+    const std::vector<int64_t> rp(row_ptr, row_ptr + n_nodes + 1);
+    const std::vector<int32_t> cl(col, col + row_ptr[n_nodes]);
+    const auto g = ens::ghost_rows(rp, cl, lo, hi);
     *n = int64_t(g.size());
     if (*n > cap) return fail(nullptr, ENS_E_ARG, "cap too small");
     std::copy(g.begin(), g.end(), ghosts);
+    return ENS_OK;
+}
+
+int ens_host_halo_plan(int64_t n_nodes, const int64_t* row_ptr, const int32_t* col, int32_t n_parts, int32_t part,
+                       int64_t* lo_hi_b, int32_t* peers, int64_t* peer_info, int32_t* send_rows, int64_t cap,
+                       int64_t* n_peers, int64_t* n_send) {
+    if (n_parts < 1 || part < 0 || part >= n_parts) return fail(nullptr, ENS_E_ARG, "bad part");
+    const std::vector<int64_t> rp(row_ptr, row_ptr + n_nodes + 1);
+    const std::vector<int32_t> cl(col, col + row_ptr[n_nodes]);
+    const auto plans = ens::halo_plan(rp, cl, n_parts);
+    const auto& pl = plans[size_t(part)];
+    *n_peers = int64_t(pl.peers.size());
+    *n_send = int64_t(pl.send_rows.size());
+    if (*n_peers > n_parts || *n_send > cap) return fail(nullptr, ENS_E_ARG, "cap too small");
+    lo_hi_b[0] = pl.lo;
+    lo_hi_b[1] = pl.hi;
+    lo_hi_b[2] = pl.b_lo;
+    lo_hi_b[3] = pl.b_hi;
+    lo_hi_b[4] = int64_t(pl.ghosts.size());
+    for (size_t k = 0; k < pl.peers.size(); ++k) {
+        peers[k] = pl.peers[k].q;
+        peer_info[4 * k + 0] = pl.peers[k].send_off;
+        peer_info[4 * k + 1] = pl.peers[k].send_n;
+        peer_info[4 * k + 2] = pl.peers[k].recv_row;
+        peer_info[4 * k + 3] = pl.peers[k].recv_n;
+    }
+    std::copy(pl.send_rows.begin(), pl.send_rows.end(), send_rows);
     return ENS_OK;
 }
 

@@ -16,13 +16,13 @@ constexpr int kMaxFields = 4;
 struct StepArgs {
     int64_t V = 0;            // rows handled by this launch: rows [row0, row0 + V)
     int64_t row0 = 0;
-    int64_t V_total = 0;      // rows of the state arrays (owned + ghost)
+    int64_t fk_rows = 0;      // rows of the F_k arrays (the owned rows)
     int32_t n_s = 0;
-    const int32_t* row_ptr = nullptr;   // [V_total + 1] (int32: nnzb < 2^31)
+    const int32_t* row_ptr = nullptr;   // [rows + 1] (int32: nnzb < 2^31)
     const int32_t* col = nullptr;
     const double* Kval = nullptr;
     // matrix-free operands (host_setup.hpp "Fans")
-    const int32_t* inc_ptr = nullptr;   // [V_total + 1] incidence range of each row
+    const int32_t* inc_ptr = nullptr;   // [rows + 1] incidence range of each row
     const int4* fan = nullptr;          // [3F] {e, n_prev, n_next, restart}
     const double* Krow = nullptr;       // [3F][28]
     const double* alpha = nullptr;      // [F][n_s]
@@ -34,10 +34,10 @@ struct StepArgs {
     const double* c2a = nullptr;        // null => scalars c2, c3
     const double* c3a = nullptr;
     double c2 = 2.0, c3 = 1.0;
-    const uint8_t* fixed = nullptr;     // [V_total]
+    const uint8_t* fixed = nullptr;     // [rows]
     // load f(t) = ramp(t) sum_k g_k(t) F_k
     int32_t n_fields = 0;
-    const double* Fk = nullptr;         // [n_fields][V_total][3]
+    const double* Fk = nullptr;         // [n_fields][fk_rows][3]
     int32_t n_tab = 0;
     const double* tab_t = nullptr;      // device [n_tab]
     const double* tab_g = nullptr;      // device [n_fields][n_tab]
@@ -59,7 +59,8 @@ cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st);
 // Same on the matrix-free element form (alpha_{e,s} K^_e gathered per node).
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st);
 // realisations per thread of the step kernels for a given N_s (4, 2 or 1)
-int pick_vec(int32_t n_s);
+int pick_vec(int32_t n_s);      // assembled kernel
+int pick_vec_mf(int32_t n_s);   // matrix-free kernel
 // *step_base += n (after n steps were enqueued)
 cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st);
 
@@ -67,10 +68,13 @@ cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st);
 cudaError_t launch_assemble(int64_t nnzb, int32_t n_s, const int32_t* contrib_ptr, const int32_t* contrib,
                             const double* alpha, const double* Khat, double* Kval, cudaStream_t st);
 
-// F4: ABI [n_s][V][3] (caller numbering) <-> device [V][3][n_s] (RCM numbering)
-cudaError_t launch_abi_to_dev(int64_t V, int32_t n_s, const int32_t* perm, const double* src, double* dst,
-                              cudaStream_t st);
-cudaError_t launch_dev_to_abi(int64_t V, int32_t n_s, const int32_t* perm, const double* src, double* dst,
-                              cudaStream_t st);
+// F4: device rows [rows][3][n_s] <-> ABI [n_s][V_abi][3] at node map[i]
+cudaError_t launch_abi_to_dev(int64_t rows, int32_t n_s, const int32_t* map, int64_t V_abi, const double* src,
+                              double* dst, cudaStream_t st);
+cudaError_t launch_dev_to_abi(int64_t rows, int32_t n_s, const int32_t* map, int64_t V_abi, const double* src,
+                              double* dst, cudaStream_t st);
+// halo send-pack of u_{n+1} rows (step = *step_base + step_off)
+cudaError_t launch_pack(int64_t n, int32_t n_s, const int32_t* rows, const int64_t* step_base, int64_t step_off,
+                        const double* ubuf0, const double* ubuf1, double* sendbuf, cudaStream_t st);
 
 }  // namespace ens

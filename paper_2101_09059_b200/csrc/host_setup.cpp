@@ -379,4 +379,44 @@ std::vector<int32_t> ghost_rows(const std::vector<int64_t>& row_ptr, const std::
     return g;
 }
 
+std::vector<PartPlan> halo_plan(const std::vector<int64_t>& row_ptr, const std::vector<int32_t>& col, int32_t P) {
+    const std::vector<int64_t> b = partition_bounds(row_ptr, P);
+    std::vector<PartPlan> plans(static_cast<size_t>(P));
+    for (int32_t p = 0; p < P; ++p) {
+        PartPlan& pl = plans[size_t(p)];
+        pl.p = p;
+        pl.lo = b[size_t(p)];
+        pl.hi = b[size_t(p) + 1];
+        pl.ghosts = ghost_rows(row_ptr, col, pl.lo, pl.hi);
+        int64_t last_lo = -1, first_hi = pl.n_own();
+        for (int64_t i = pl.lo; i < pl.hi; ++i)
+            for (int64_t k = row_ptr[size_t(i)]; k < row_ptr[size_t(i) + 1]; ++k) {
+                if (col[size_t(k)] < pl.lo) last_lo = std::max(last_lo, i - pl.lo);
+                if (col[size_t(k)] >= pl.hi) first_hi = std::min(first_hi, i - pl.lo);
+            }
+        pl.b_lo = last_lo + 1;
+        pl.b_hi = pl.n_own() - first_hi;
+        if (pl.b_lo + pl.b_hi > pl.n_own()) { pl.b_lo = pl.n_own(); pl.b_hi = 0; }
+    }
+    for (int32_t p = 0; p < P; ++p) {
+        PartPlan& pl = plans[size_t(p)];
+        for (int32_t q = 0; q < P; ++q) {
+            if (q == p) continue;
+            const PartPlan& ql = plans[size_t(q)];
+            PartPlan::Peer pe;
+            pe.q = q;
+            pe.send_off = int64_t(pl.send_rows.size());
+            for (int32_t g : ql.ghosts)                       // my rows that q needs, ascending
+                if (g >= pl.lo && g < pl.hi) pl.send_rows.push_back(int32_t(g - pl.lo));
+            pe.send_n = int64_t(pl.send_rows.size()) - pe.send_off;
+            auto first = std::lower_bound(pl.ghosts.begin(), pl.ghosts.end(), int32_t(ql.lo));
+            auto last = std::lower_bound(pl.ghosts.begin(), pl.ghosts.end(), int32_t(ql.hi));
+            pe.recv_row = pl.n_own() + int64_t(first - pl.ghosts.begin());
+            pe.recv_n = int64_t(last - first);
+            if (pe.send_n || pe.recv_n) pl.peers.push_back(pe);
+        }
+    }
+    return plans;
+}
+
 }  // namespace ens

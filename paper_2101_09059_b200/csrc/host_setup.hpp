@@ -65,4 +65,24 @@ std::vector<int64_t> partition_bounds(const std::vector<int64_t>& row_ptr, int32
 std::vector<int32_t> ghost_rows(const std::vector<int64_t>& row_ptr, const std::vector<int32_t>& col,
                                 int64_t lo, int64_t hi);
 
+// Halo plan of part p.  Local rows: the owned rows
+// [lo, hi) in global order, then the ghosts in ascending global order (hence grouped by
+// owner: each neighbour's ghosts are one contiguous slice, received in place).
+struct PartPlan {
+    int32_t p = 0;
+    int64_t lo = 0, hi = 0;
+    std::vector<int32_t> ghosts;        // global RCM ids, ascending
+    int64_t b_lo = 0, b_hi = 0;         // every row with a ghost column lies in local rows
+                                        // [0, b_lo) or [n_own - b_hi, n_own)
+    struct Peer {
+        int32_t q = 0;
+        int64_t send_off = 0, send_n = 0;   // slice of send_rows / the send buffer
+        int64_t recv_row = 0, recv_n = 0;   // local row of the first ghost owned by q
+    };
+    std::vector<Peer> peers;            // ascending q
+    std::vector<int32_t> send_rows;     // local owned rows, concatenated per peer
+    int64_t n_own() const { return hi - lo; }
+};
+std::vector<PartPlan> halo_plan(const std::vector<int64_t>& row_ptr, const std::vector<int32_t>& col, int32_t P);
+
 }  // namespace ens

@@ -12,6 +12,7 @@
 // fma(): the per-realisation arithmetic is identical whatever N_s, VEC or the launch
 // geometry, which makes ensemble runs bit-identical to single-realisation runs.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "device.hpp"
@@ -142,39 +143,107 @@ __device__ __forceinline__ StepCtx step_ctx(const StepArgs& a) {
 }
 
 // S2 + S4: r = f - y; u_{n+1} = c1 r + c2 u_n - c3 u_{n-1}; Dirichlet; non-finite flag.
+// The operands of the update do not depend on the product, so they are loaded (upd_load)
+// before the gather loop and their latency hides behind it; upd_store finishes the step.
 template <int VEC>
-__device__ __forceinline__ void cd_update(const StepArgs& a, const StepCtx& sc, const double* coef,
-                                          int64_t i, int s0, const double (&y)[3][VEC]) {
+struct Upd {
+    Vec<VEC> c1, c2, c3, un[3], uo[3];
+    double f[3];
+    uint8_t fx;
+};
+
+template <int VEC>
+__device__ __forceinline__ void upd_load(const StepArgs& a, const StepCtx& sc, const double* coef, int64_t i,
+                                         int s0, Upd<VEC>& u, bool load_un) {
     const int n_s = a.n_s;
-    const uint8_t fx = a.fixed ? __ldg(a.fixed + i) : uint8_t(0);
-    Vec<VEC> c1 = ld_ro<VEC>(a.c1 + i * n_s + s0);
-    Vec<VEC> c2, c3;
+    u.fx = a.fixed ? __ldg(a.fixed + i) : uint8_t(0);
+    u.c1 = ld_ro<VEC>(a.c1 + i * n_s + s0);
     if (a.c2a) {
-        c2 = ld_ro<VEC>(a.c2a + i * n_s + s0);
-        c3 = ld_ro<VEC>(a.c3a + i * n_s + s0);
+        u.c2 = ld_ro<VEC>(a.c2a + i * n_s + s0);
+        u.c3 = ld_ro<VEC>(a.c3a + i * n_s + s0);
     } else {
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) { c2.v[v] = a.c2; c3.v[v] = a.c3; }
+        for (int v = 0; v < VEC; ++v) { u.c2.v[v] = a.c2; u.c3.v[v] = a.c3; }
     }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int64_t off = (i * 3 + c) * n_s + s0;
+        if (load_un) u.un[c] = ld_ro<VEC>(sc.un + off);
+        u.uo[c] = ld_rw<VEC>(sc.uo + off);
+        double f = 0.0;
+        for (int k = 0; k < a.n_fields; ++k) f = fma(coef[k], __ldg(a.Fk + (int64_t(k) * a.fk_rows + i) * 3 + c), f);
+        u.f[c] = f;
+    }
+}
+
+// Register-free variant for the matrix-free kernel: cp.async (LDGSTS) copies c1 (c2, c3)
+// and u_{n-1} of the thread's row into its shared-memory slot; read back after the gather.
+template <int VEC>
+__device__ __forceinline__ void cp_async_vec(double* dst_smem, const double* src) {
+    const uint32_t d = uint32_t(__cvta_generic_to_shared(dst_smem));
+    if constexpr (VEC == 1) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(src) : "memory");
+    } else if constexpr (VEC == 2) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(d), "l"(src) : "memory");
+    } else {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(d), "l"(src) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(d + 16), "l"(src + 2) : "memory");
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void upd_load_async(const StepArgs& a, const StepCtx& sc, int64_t i, int s0,
+                                               double* slot /* 6 * VEC doubles */) {
+    const int n_s = a.n_s;
+    cp_async_vec<VEC>(slot, a.c1 + i * n_s + s0);
+    if (a.c2a) {
+        cp_async_vec<VEC>(slot + VEC, a.c2a + i * n_s + s0);
+        cp_async_vec<VEC>(slot + 2 * VEC, a.c3a + i * n_s + s0);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) cp_async_vec<VEC>(slot + (3 + c) * VEC, sc.uo + (i * 3 + c) * n_s + s0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int VEC>
+__device__ __forceinline__ void upd_collect(const StepArgs& a, const double* coef, int64_t i, const double* slot,
+                                            Upd<VEC>& u) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    u.fx = a.fixed ? __ldg(a.fixed + i) : uint8_t(0);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+        u.c1.v[v] = slot[v];
+        u.c2.v[v] = a.c2a ? slot[VEC + v] : a.c2;
+        u.c3.v[v] = a.c2a ? slot[2 * VEC + v] : a.c3;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) u.uo[c].v[v] = slot[(3 + c) * VEC + v];
+        double f = 0.0;
+        for (int k = 0; k < a.n_fields; ++k) f = fma(coef[k], __ldg(a.Fk + (int64_t(k) * a.fk_rows + i) * 3 + c), f);
+        u.f[c] = f;
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void upd_store(const StepArgs& a, const StepCtx& sc, int64_t i, int s0,
+                                          const double (&y)[3][VEC], const Upd<VEC>& u) {
+    const int n_s = a.n_s;
     unsigned bad = 0;   // bit v: realisation s0 + v produced a non-finite value
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        double f = 0.0;
-        for (int k = 0; k < a.n_fields; ++k) f = fma(coef[k], __ldg(a.Fk + (int64_t(k) * a.V_total + i) * 3 + c), f);
-        const int64_t off = (i * 3 + c) * n_s + s0;
-        Vec<VEC> un = ld_ro<VEC>(sc.un + off);
-        Vec<VEC> uo = ld_rw<VEC>(sc.uo + off);
         Vec<VEC> out;
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
-            double r = f - y[c][v];
-            double t = fma(c2.v[v], un.v[v], -(c3.v[v] * uo.v[v]));
-            double w = fma(c1.v[v], r, t);
-            if ((fx >> c) & 1) w = 0.0;
+            const double r = u.f[c] - y[c][v];
+            const double t = fma(u.c2.v[v], u.un[c].v[v], -(u.c3.v[v] * u.uo[c].v[v]));
+            double w = fma(u.c1.v[v], r, t);
+            if ((u.fx >> c) & 1) w = 0.0;
             bad |= unsigned(!isfinite(w)) << v;
             out.v[v] = w;
         }
-        st_vec<VEC>(sc.uo + off, out);
+        st_vec<VEC>(sc.uo + (i * 3 + c) * n_s + s0, out);
     }
     if (bad) {
         for (int v = 0; v < VEC; ++v)
@@ -197,7 +266,7 @@ __device__ __forceinline__ void store_y(const StepArgs& a, int64_t i, int s0, co
 }
 
 // ---- F1: fused step on the assembled per-realisation block values ----------------------
-template <int VEC, bool APPLY>
+template <int VEC, bool APPLY, bool PREF>
 __global__ void __launch_bounds__(kThreads)
 k_step_assembled(const StepArgs a) {
     __shared__ double s_coef[kMaxFields];
@@ -214,6 +283,9 @@ k_step_assembled(const StepArgs a) {
 
     uint64_t pol = 0;
     if constexpr (VEC < 4) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+
+    Upd<VEC> upd;
+    if constexpr (!APPLY && PREF) upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
 
     double y[3][VEC];
 #pragma unroll
@@ -239,8 +311,12 @@ k_step_assembled(const StepArgs a) {
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) y[c][v] = fma(k[3 * c + d].v[v], u[d].v[v], y[c][v]);
     }
-    if constexpr (APPLY) store_y<VEC>(a, i, s0, y);
-    else cd_update<VEC>(a, sc, s_coef, i, s0, y);
+    if constexpr (APPLY) {
+        store_y<VEC>(a, i, s0, y);
+    } else {
+        if constexpr (!PREF) upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
+        upd_store<VEC>(a, sc, i, s0, y, upd);
+    }
 }
 
 // ---- F2: fused step on the matrix-free element form ------------------------------------
@@ -271,8 +347,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     }
 }
 
-template <int VEC, bool APPLY>
-__global__ void __launch_bounds__(kThreads)
+template <int VEC, bool APPLY, int BATCH, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
 k_step_matrix_free(const StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double s_coef[kMaxFields];
@@ -305,6 +381,7 @@ k_step_matrix_free(const StepArgs a) {
     const bool valid = lr < R && i < r1 && g < P;
     const int n_s = a.n_s;
     const int s0 = g * VEC;
+    const double* un_base = sc.un + s0;
 
     double y[3][VEC];
 #pragma unroll
@@ -314,46 +391,71 @@ k_step_matrix_free(const StepArgs a) {
     Vec<VEC> uo[3], up[3];
     if (valid) {
 #pragma unroll
-        for (int d = 0; d < 3; ++d) uo[d] = ld_ro<VEC>(sc.un + (i * 3 + d) * n_s + s0);
+        for (int d = 0; d < 3; ++d) uo[d] = ld_ro<VEC>(un_base + (i * 3 + d) * n_s);
     }
+    double* slot = reinterpret_cast<double*>(smem + size_t(a.mf_smem_inc) * 240) + size_t(threadIdx.x) * 6 * VEC;
+    if (!APPLY && valid) upd_load_async<VEC>(a, sc, i, s0, slot);
     if (n_inc) mbar_wait(bar, 0);
     if (!valid) return;
 
     const int32_t kb = __ldg(a.inc_ptr + i) - k0, ke = __ldg(a.inc_ptr + i + 1) - k0;
-    for (int32_t k = kb; k < ke; ++k) {
-        const int4 rec = sRec[k];
-        if (rec.w) {
+    if (kb < ke) {                               // the row's first chain starts at kb
+        const int4 r = sRec[kb];
 #pragma unroll
-            for (int d = 0; d < 3; ++d) up[d] = ld_ro<VEC>(sc.un + (int64_t(rec.y) * 3 + d) * n_s + s0);
+        for (int d = 0; d < 3; ++d) up[d] = ld_ro<VEC>(un_base + (int64_t(r.y) * 3 + d) * n_s);
+    }
+    for (int32_t k = kb; k < ke; k += BATCH) {
+        // gather phase: every load of the batch in flight before any arithmetic
+        int4 rec[BATCH];
+        Vec<VEC> un[BATCH][3], al[BATCH];
+#pragma unroll
+        for (int j = 0; j < BATCH; ++j) {
+            if (k + j < ke) {
+                rec[j] = sRec[k + j];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) un[j][d] = ld_ro<VEC>(un_base + (int64_t(rec[j].z) * 3 + d) * n_s);
+                al[j] = ld_ro<VEC>(a.alpha + int64_t(rec[j].x) * n_s + s0);
+            }
         }
-        Vec<VEC> un[3];
 #pragma unroll
-        for (int d = 0; d < 3; ++d) un[d] = ld_ro<VEC>(sc.un + (int64_t(rec.z) * 3 + d) * n_s + s0);
-        const Vec<VEC> al = ld_ro<VEC>(a.alpha + int64_t(rec.x) * n_s + s0);
-        const double* K = sK + size_t(k) * 28;
+        for (int j = 0; j < BATCH; ++j) {
+            if (k + j >= ke) break;
+            if (rec[j].w && k + j != kb) {       // a further chain (non-manifold vertex): rare
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            double t[VEC];
+                for (int d = 0; d < 3; ++d) up[d] = ld_ro<VEC>(un_base + (int64_t(rec[j].y) * 3 + d) * n_s);
+            }
+            const double* K = sK + size_t(k + j) * 28;
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) t[v] = 0.0;
+            for (int c = 0; c < 3; ++c) {
+                double t[VEC];
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                const double k_own = K[9 * c + d], k_prev = K[9 * c + 3 + d], k_next = K[9 * c + 6 + d];
+                for (int v = 0; v < VEC; ++v) t[v] = 0.0;
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) {
-                    t[v] = fma(k_own, uo[d].v[v], t[v]);
-                    t[v] = fma(k_prev, up[d].v[v], t[v]);
-                    t[v] = fma(k_next, un[d].v[v], t[v]);
+                for (int d = 0; d < 3; ++d) {
+                    const double k_own = K[9 * c + d], k_prev = K[9 * c + 3 + d], k_next = K[9 * c + 6 + d];
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) {
+                        t[v] = fma(k_own, uo[d].v[v], t[v]);
+                        t[v] = fma(k_prev, up[d].v[v], t[v]);
+                        t[v] = fma(k_next, un[j][d].v[v], t[v]);
+                    }
                 }
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) y[c][v] = fma(al[j].v[v], t[v], y[c][v]);
             }
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) y[c][v] = fma(al.v[v], t[v], y[c][v]);
+            for (int d = 0; d < 3; ++d) up[d] = un[j][d];
         }
-#pragma unroll
-        for (int d = 0; d < 3; ++d) up[d] = un[d];
     }
-    if constexpr (APPLY) store_y<VEC>(a, i, s0, y);
-    else cd_update<VEC>(a, sc, s_coef, i, s0, y);
+    if constexpr (APPLY) {
+        store_y<VEC>(a, i, s0, y);
+    } else {
+        Upd<VEC> upd;
+        upd_collect<VEC>(a, s_coef, i, slot, upd);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) upd.un[d] = uo[d];
+        upd_store<VEC>(a, sc, i, s0, y, upd);
+    }
 }
 
 __global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
@@ -385,58 +487,87 @@ k_assemble(int64_t nnzb, int32_t n_s, const int32_t* __restrict__ cptr, const in
 }
 
 // ---- F4: layout transposes (ABI <-> device), off the hot path --------------------------
-__global__ void k_abi_to_dev(int64_t V, int32_t n_s, const int32_t* __restrict__ perm,
+// device rows i < rows  <->  ABI [n_s][V_abi][3] at node map[i]
+__global__ void k_abi_to_dev(int64_t rows, int32_t n_s, const int32_t* __restrict__ map, int64_t V_abi,
                              const double* __restrict__ src, double* __restrict__ dst) {
     const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= V * 3 * n_s) return;
+    if (tid >= rows * 3 * n_s) return;
     const int s = int(tid % n_s);
     const int64_t ic = tid / n_s;
     const int64_t i = ic / 3;
     const int c = int(ic % 3);
-    dst[tid] = src[(int64_t(s) * V + perm[i]) * 3 + c];
+    dst[tid] = src[(int64_t(s) * V_abi + map[i]) * 3 + c];
 }
 
-__global__ void k_dev_to_abi(int64_t V, int32_t n_s, const int32_t* __restrict__ perm,
+__global__ void k_dev_to_abi(int64_t rows, int32_t n_s, const int32_t* __restrict__ map, int64_t V_abi,
                              const double* __restrict__ src, double* __restrict__ dst) {
     const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= V * 3 * n_s) return;
+    if (tid >= rows * 3 * n_s) return;
     const int s = int(tid % n_s);
     const int64_t ic = tid / n_s;
     const int64_t i = ic / 3;
     const int c = int(ic % 3);
-    dst[(int64_t(s) * V + perm[i]) * 3 + c] = src[tid];
+    dst[(int64_t(s) * V_abi + map[i]) * 3 + c] = src[tid];
+}
+
+// ---- halo send-pack: sendbuf[k] = u_{n+1}[rows[k]] (3 n_s doubles per row) ------------
+__global__ void k_pack(int64_t n, int32_t n_s, const int32_t* __restrict__ rows, const int64_t* step_base,
+                       int64_t step_off, const double* ubuf0, const double* ubuf1, double* __restrict__ sendbuf) {
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t w = int64_t(3) * n_s;
+    if (tid >= n * w) return;
+    const int64_t step = *step_base + step_off;
+    const double* unew = (step & 1) ? ubuf0 : ubuf1;     // u_{n+1} lives in buf[(step + 1) & 1]
+    const int64_t k = tid / w;
+    sendbuf[tid] = unew[int64_t(rows[k]) * w + (tid - k * w)];
 }
 
 inline unsigned grid_for(int64_t n) { return unsigned((n + kThreads - 1) / kThreads); }
 
 }  // namespace
 
+static bool a1_prefetch() {
+    static int v = [] {
+        const char* e = std::getenv("ENS_A1_PREFETCH");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 template <int VEC, bool APPLY>
 static cudaError_t launch_a1(const StepArgs& a, cudaStream_t st) {
     const int64_t n = a.V * (a.n_s / VEC);
     if (n == 0) return cudaSuccess;
-    k_step_assembled<VEC, APPLY><<<grid_for(n), kThreads, 0, st>>>(a);
+    if (a1_prefetch()) k_step_assembled<VEC, APPLY, true><<<grid_for(n), kThreads, 0, st>>>(a);
+    else k_step_assembled<VEC, APPLY, false><<<grid_for(n), kThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 
-template <int VEC, bool APPLY>
+template <int VEC, bool APPLY, int BATCH, int MINB>
 static cudaError_t launch_a2(const StepArgs& a, cudaStream_t st) {
     if (a.V == 0) return cudaSuccess;
     const int P = a.n_s / VEC;
-    const size_t smem = size_t(a.mf_smem_inc) * 240;
+    const size_t smem = size_t(a.mf_smem_inc) * 240 + size_t(a.mf_rows * a.mf_groups) * 6 * VEC * sizeof(double);
     static bool attr_set = false;      // per template instance
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free<VEC, APPLY>,
+        cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free<VEC, APPLY, BATCH, MINB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     dim3 grid(unsigned((a.V + a.mf_rows - 1) / a.mf_rows), unsigned((P + a.mf_groups - 1) / a.mf_groups));
-    k_step_matrix_free<VEC, APPLY><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(a);
+    k_step_matrix_free<VEC, APPLY, BATCH, MINB><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(a);
     return cudaGetLastError();
 }
 
-int pick_vec(int32_t n_s) { return (n_s % 4 == 0 && n_s >= 128) ? 4 : (n_s % 2 == 0 ? 2 : 1); }
+int pick_vec(int32_t n_s) {
+    static int vec4 = [] {
+        const char* e = std::getenv("ENS_A1_VEC4");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (vec4 && n_s % 4 == 0) return 4;
+    return n_s % 2 == 0 ? 2 : 1;
+}
 
 cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st) {
     const bool apply = a.y_out != nullptr;
@@ -447,13 +578,33 @@ cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st) {
     }
 }
 
+// Matrix-free variants (tuning knob ENS_MF_VARIANT = 0..3):
+//   0: VEC 2, batch 1, >= 2 CTAs/SM   1: VEC 2, batch 2, >= 2 CTAs/SM
+//   2: VEC 1, batch 2, >= 3 CTAs/SM   3: VEC 1, batch 1, >= 4 CTAs/SM
+int mf_variant() {
+    static int v = [] {
+        const char* e = std::getenv("ENS_MF_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+int pick_vec_mf(int32_t n_s) {
+    const int v = mf_variant();
+    if (v >= 2 || n_s % 2) return 1;
+    return 2;
+}
+
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
-    const bool apply = a.y_out != nullptr;
-    switch (pick_vec(a.n_s)) {
-        case 4: return apply ? launch_a2<4, true>(a, st) : launch_a2<4, false>(a, st);
-        case 2: return apply ? launch_a2<2, true>(a, st) : launch_a2<2, false>(a, st);
-        default: return apply ? launch_a2<1, true>(a, st) : launch_a2<1, false>(a, st);
+    const bool ap = a.y_out != nullptr;
+    const int vec = pick_vec_mf(a.n_s);
+    const int var = mf_variant();
+    if (vec == 2) {
+        if (var == 1) return ap ? launch_a2<2, true, 2, 2>(a, st) : launch_a2<2, false, 2, 2>(a, st);
+        return ap ? launch_a2<2, true, 1, 2>(a, st) : launch_a2<2, false, 1, 2>(a, st);
     }
+    if (var == 3) return ap ? launch_a2<1, true, 1, 4>(a, st) : launch_a2<1, false, 1, 4>(a, st);
+    return ap ? launch_a2<1, true, 2, 3>(a, st) : launch_a2<1, false, 2, 3>(a, st);
 }
 
 cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st) {
@@ -469,19 +620,27 @@ cudaError_t launch_assemble(int64_t nnzb, int32_t n_s, const int32_t* contrib_pt
     return cudaGetLastError();
 }
 
-cudaError_t launch_abi_to_dev(int64_t V, int32_t n_s, const int32_t* perm, const double* src, double* dst,
-                              cudaStream_t st) {
-    const int64_t n = V * 3 * n_s;
+cudaError_t launch_abi_to_dev(int64_t rows, int32_t n_s, const int32_t* map, int64_t V_abi, const double* src,
+                              double* dst, cudaStream_t st) {
+    const int64_t n = rows * 3 * n_s;
     if (n == 0) return cudaSuccess;
-    k_abi_to_dev<<<grid_for(n), kThreads, 0, st>>>(V, n_s, perm, src, dst);
+    k_abi_to_dev<<<grid_for(n), kThreads, 0, st>>>(rows, n_s, map, V_abi, src, dst);
     return cudaGetLastError();
 }
 
-cudaError_t launch_dev_to_abi(int64_t V, int32_t n_s, const int32_t* perm, const double* src, double* dst,
-                              cudaStream_t st) {
-    const int64_t n = V * 3 * n_s;
+cudaError_t launch_dev_to_abi(int64_t rows, int32_t n_s, const int32_t* map, int64_t V_abi, const double* src,
+                              double* dst, cudaStream_t st) {
+    const int64_t n = rows * 3 * n_s;
     if (n == 0) return cudaSuccess;
-    k_dev_to_abi<<<grid_for(n), kThreads, 0, st>>>(V, n_s, perm, src, dst);
+    k_dev_to_abi<<<grid_for(n), kThreads, 0, st>>>(rows, n_s, map, V_abi, src, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack(int64_t n, int32_t n_s, const int32_t* rows, const int64_t* step_base, int64_t step_off,
+                        const double* ubuf0, const double* ubuf1, double* sendbuf, cudaStream_t st) {
+    const int64_t m = n * 3 * n_s;
+    if (m == 0) return cudaSuccess;
+    k_pack<<<grid_for(m), kThreads, 0, st>>>(n, n_s, rows, step_base, step_off, ubuf0, ubuf1, sendbuf);
     return cudaGetLastError();
 }
 

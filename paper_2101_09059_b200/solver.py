@@ -58,8 +58,8 @@ class Ensemble:
 
     def __init__(self, xyz, tris, fixed, E, h, *, rho, nu, k_shear=5.0 / 6.0, dt=0.0,
                  cfl_safety=0.9, c_d=0.0, damping="none", kernel="assembled", dist="single",
-                 s_begin=0, rank=0, world=1, device=None, stream=None, torch_alloc=True,
-                 _ctx=None):
+                 s_begin=0, rank=0, world=1, nccl_comm=None, device=None, stream=None,
+                 torch_alloc=True, _ctx=None):
         self._ctx = None
         self._alloc = None
         if _ctx is not None:                      # from_csr
@@ -73,6 +73,8 @@ class Ensemble:
         mat = _ffi.EnsMaterials(self.n_s, _p(E), _p(h), rho, nu, k_shear, s_begin)
         opt, self._alloc = _options(dt, cfl_safety, c_d, damping, kernel, dist, rank, world,
                                     device, stream, torch_alloc)
+        if nccl_comm is not None:
+            opt.nccl_comm = C.c_void_p(int(nccl_comm))
         ctx = C.c_void_p()
         check(lib().ens_create(C.byref(mesh), C.byref(mat), C.byref(opt), C.byref(ctx)))
         self._ctx = ctx
@@ -125,9 +127,19 @@ class Ensemble:
     def sync(self):
         check(lib().ens_sync(self._ctx), self._ctx)
 
+    def owned(self) -> np.ndarray:
+        """Caller node ids of the rows get_state returns (all nodes unless NODE on NCCL)."""
+        n = C.c_int64()
+        check(lib().ens_get_owned(self._ctx, None, C.byref(n)), self._ctx)
+        ids = np.zeros(n.value, np.int32)
+        check(lib().ens_get_owned(self._ctx, _p(ids), C.byref(n)), self._ctx)
+        return ids
+
     def get_state(self, u_n=None, u_nm1=None, want_prev=True):
         """Returns (u_n, u_nm1, t, step); fills the given host buffers if provided."""
-        shape = (self.n_s, self.V, 3)
+        n = C.c_int64()
+        check(lib().ens_get_owned(self._ctx, None, C.byref(n)), self._ctx)
+        shape = (self.n_s, n.value, 3)
         if u_n is None:
             u_n = np.empty(shape)
         if want_prev and u_nm1 is None:
@@ -144,7 +156,9 @@ class Ensemble:
 
     def apply_stiffness(self, u):
         u = _c(u, np.float64)
-        y = np.empty_like(u)
+        n = C.c_int64()
+        check(lib().ens_get_owned(self._ctx, None, C.byref(n)), self._ctx)
+        y = np.empty((u.shape[0], n.value, 3))
         check(lib().ens_apply_stiffness(self._ctx, _p(u), _p(y)), self._ctx)
         return y
 
@@ -245,3 +259,22 @@ def host_materials(xyz, tris, E, h, rho, cfl_safety=0.9):
     check(lib().ens_host_materials(V, F, _p(xyz), _p(tris), n_s, _p(E), _p(h), rho, cfl_safety,
                                    _p(alpha), _p(mass), C.byref(dt)))
     return alpha, mass, dt.value
+
+
+def host_halo_plan(row_ptr, col, P, part):
+    """Halo plan of `part` (ens_host_halo_plan): dict lo, hi, b_lo, b_hi, n_ghost, peers
+    [(q, send_off, send_n, recv_row, recv_n)], send_rows."""
+    row_ptr, col = _c(row_ptr, np.int64), _c(col, np.int32)
+    V = len(row_ptr) - 1
+    lhb = np.zeros(5, np.int64)
+    peers = np.zeros(P, np.int32)
+    info = np.zeros((P, 4), np.int64)
+    cap = V
+    send = np.zeros(cap, np.int32)
+    npe, ns = C.c_int64(), C.c_int64()
+    check(lib().ens_host_halo_plan(V, _p(row_ptr), _p(col), P, part, _p(lhb), _p(peers), _p(info), _p(send),
+                                   cap, C.byref(npe), C.byref(ns)))
+    return {"lo": int(lhb[0]), "hi": int(lhb[1]), "b_lo": int(lhb[2]), "b_hi": int(lhb[3]),
+            "n_ghost": int(lhb[4]),
+            "peers": [(int(peers[k]), *map(int, info[k])) for k in range(npe.value)],
+            "send_rows": send[:ns.value].copy()}

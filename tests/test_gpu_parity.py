@@ -245,3 +245,34 @@ def test_c2_laplace_law_on_gpu():
     urs = np.mean(np.einsum("sij,ij->si", u[:, nodes, :2], rhat), axis=1)
     assert np.all(np.abs(urs / ref - 1) < 0.5)
     ens.close()
+
+
+@pytest.mark.parametrize("kernel", ["assembled", "matrix_free"])
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_node_partition_bitexact(kernel, P):
+    """ENS_DIST_NODE (all P parts in one context, halo by device copies): boundary rows
+    first, pack, exchange, interior rows — bit-identical to the unpartitioned run, since
+    each row keeps its global summation order."""
+    m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(24, 60), 0.01, 3), 2)
+    E, h = _mats(m, 6, 61)
+    tr = loads.pulsatile(m.xyz, m.tris, period=0.01, systole=0.004, ramp_T=0.003)
+    kw = dict(rho=RHO, nu=NU, k_shear=KS, kernel=kernel, dt=5e-5, damping="identity", c_d=0.3)
+    ref = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, **kw)
+    par = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, dist="node", world=P, **kw)
+    inf = par.info()
+    assert inf["n_owned"] == m.n_nodes and inf["halo_bytes_per_step"] > 0
+    for e in (ref, par):
+        e.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+        e.step(257)
+    u0, p0, _, s0 = ref.get_state()
+    u1, p1, _, s1 = par.get_state()
+    assert s0 == s1 and np.array_equal(u0, u1) and np.array_equal(p0, p1)
+    rng = np.random.default_rng(P)
+    x = rng.uniform(-1, 1, u0.shape)
+    assert np.array_equal(ref.apply_stiffness(x), par.apply_stiffness(x))
+    # checkpoint into the partitioned context, continue both
+    par.set_state(u0, p0, s0)
+    for e in (ref, par):
+        e.step(40)
+    assert np.array_equal(ref.get_state()[0], par.get_state()[0])
+    ref.close(); par.close()

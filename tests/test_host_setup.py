@@ -131,3 +131,38 @@ def test_create_argument_errors(bad):
     with pytest.raises(_ffi.EnsError) as ei:
         solver.Ensemble(m.xyz, tris, m.fixed, E, h, torch_alloc=False, **kw)
     assert ei.value.code == (_ffi.ENS_E_MESH if bad == "mesh" else _ffi.ENS_E_ARG)
+
+
+@pytest.mark.parametrize("P", [2, 3, 5])
+def test_halo_plan_vs_oracle(P):
+    """The product's halo plan (ens_host_halo_plan) against the oracle's C11 maps: owned
+    ranges, ghost counts, send lists (as local rows) and receive slices, bit-exact; every
+    row with a ghost column inside the boundary launch ranges."""
+    m = meshmod.shuffle_nodes(meshmod.cylinder(20, 33), 4)
+    perm, row_ptr, col = solver.host_pattern(m.n_nodes, m.tris)
+    ob, ogh, osend = oracle.halo_maps(row_ptr, col, P)
+    for p in range(P):
+        pl = solver.host_halo_plan(row_ptr, col, P, p)
+        lo, hi = pl["lo"], pl["hi"]
+        assert (lo, hi) == (ob[p], ob[p + 1]) and pl["n_ghost"] == len(ogh[p])
+        peers = {q: (so, sn, rr, rn) for q, so, sn, rr, rn in pl["peers"]}
+        for q in range(P):
+            if q == p:
+                continue
+            exp_send = osend[p][q] - lo
+            exp_recv = ogh[p][(ogh[p] >= ob[q]) & (ogh[p] < ob[q + 1])]
+            if len(exp_send) == 0 and len(exp_recv) == 0:
+                assert q not in peers
+                continue
+            so, sn, rr, rn = peers[q]
+            assert np.array_equal(pl["send_rows"][so:so + sn], exp_send)
+            assert rn == len(exp_recv)
+            if rn:
+                first = np.searchsorted(ogh[p], exp_recv[0])
+                assert rr == (hi - lo) + first
+        n_own = hi - lo
+        for i in range(lo, hi):
+            cols = col[row_ptr[i]:row_ptr[i + 1]]
+            if np.any((cols < lo) | (cols >= hi)):
+                li = i - lo
+                assert li < pl["b_lo"] or li >= n_own - pl["b_hi"]
