@@ -180,8 +180,9 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
     ap.add_argument("--n-s", type=int, default=None, help="realisations per GPU (default: the config's)")
-    ap.add_argument("--kernel", default="assembled", choices=["assembled", "matrix_free"])
+    ap.add_argument("--kernel", default="assembled", choices=["assembled", "assembled_sym", "matrix_free"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-node", action="store_true", help="skip the node-partitioned run at N > 1")
     ap.add_argument("--e2e-windows", type=int, default=10)
     ap.add_argument("--obs-every", type=int, default=100)
     args = ap.parse_args(argv)
@@ -270,6 +271,36 @@ def main(argv=None):
     h2d = Fp.numel() * 8 + tr.tab_t.size * 8 + tr.tab_g.size * 8
     d2h = out.numel() * 8
 
+    # node partition (strong scaling of the full config): the same N_s realisations on
+    # every rank, RCM rows split across ranks, NCCL halo of the interface rows per step
+    node = None
+    if world > 1 and not args.no_node:
+        comm = solver.nccl_comm_of()
+        npar = solver.Ensemble(m.xyz, m.tris, m.fixed, base.E, base.h, rho=cfg.rho, nu=cfg.nu,
+                               k_shear=cfg.k_shear, damping=cfg.damping, c_d=cfg.c_d,
+                               kernel=args.kernel, dist="node", rank=rank, world=world,
+                               nccl_comm=comm, device=local)
+        npar.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+        npar.step(max(3, args.warmup))
+        npar.sync()
+        barrier()
+        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0.record(stream)
+        npar.step(args.steps)
+        n1.record(stream)
+        n1.synchronize()
+        barrier()
+        npar.sync()
+        t = torch.tensor([n0.elapsed_time(n1) / 1e3], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ninf = npar.info()
+        node = {"value": n_s * 3 * m.n_nodes * args.steps / float(t.item()), "unit": "DOF-updates/s",
+                "ms_per_step": 1e3 * float(t.item()) / args.steps, "scaling": "strong",
+                "n_s_total": n_s, "rows_rank0": ninf["n_owned"],
+                "halo_bytes_per_step_rank0": ninf["halo_bytes_per_step"],
+                "launches_per_step": ninf["launches_per_step"]}
+        npar.close()
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = _cpu_baseline(base)
@@ -286,9 +317,11 @@ def main(argv=None):
                        "l2": f"inputs larger than L2: {info['bytes_per_step'] / 1e9:.3f} GB streamed per step vs 126 MB L2 (no flush)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_step_assembled" if args.kernel == "assembled" else "k_step_matrix_free",
+                         "kernel": {"assembled": "k_step_assembled", "assembled_sym": "k_step_assembled_sym",
+                                    "matrix_free": "k_step_matrix_free"}[args.kernel],
                          "algorithmic_bytes_per_launch": info["bytes_per_step"]},
             "cpu_baseline": cpu,
+            "node_partition": node,
             "e2e": {"value": e2e_value, "unit": "DOF-updates/s", "h2d_bytes_per_step": h2d / win,
                     "d2h_bytes_per_step": d2h / win,
                     "window": f"{win} steps + ens_set_traction (H2D {h2d} B) + ens_get_state u_n (D2H {d2h} B)"},

@@ -82,7 +82,7 @@ typedef struct {
 } ens_materials;
 
 enum { ENS_DAMP_NONE = 0, ENS_DAMP_MASS = 1, ENS_DAMP_IDENTITY = 2 };
-enum { ENS_KERNEL_ASSEMBLED = 0, ENS_KERNEL_MATRIX_FREE = 1 };
+enum { ENS_KERNEL_ASSEMBLED = 0, ENS_KERNEL_MATRIX_FREE = 1, ENS_KERNEL_ASSEMBLED_SYM = 2 };
 enum { ENS_DIST_SINGLE = 0, ENS_DIST_NODE = 1, ENS_DIST_ENSEMBLE = 2 };
 
 typedef struct {
@@ -90,7 +90,10 @@ typedef struct {
     double cfl_safety;      /* 0 => 0.9 */
     double c_d;             /* damping coefficient */
     int32_t damping;        /* ENS_DAMP_*: NONE C~ = 0; MASS C~ = c_d M~ (1/s); IDENTITY C~ = c_d I (g/s) */
-    int32_t kernel;         /* ENS_KERNEL_*: ASSEMBLED (per-realisation block-CSR values) or MATRIX_FREE */
+    int32_t kernel;         /* ENS_KERNEL_*: ASSEMBLED (per-realisation block-CSR values, 9 N_s per block,
+                               PAPER.md:349); ASSEMBLED_SYM (the same with only the blocks (i, j >= i)
+                               stored: K_s is symmetric, results bit-identical, ~half the bytes);
+                               MATRIX_FREE (alpha_{e,s} K^_e per element) */
     int32_t dist;           /* ENS_DIST_*.  ENSEMBLE: this context holds realisations [s_begin, s_begin + n_s)
                                of a sharded ensemble (no communication).  NODE: the RCM rows are split
                                into `world` parts balanced by blocks, each advanced with a halo

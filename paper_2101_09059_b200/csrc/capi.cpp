@@ -42,6 +42,9 @@ struct Part {
     int4* d_fan = nullptr;
     double *d_Krow = nullptr, *d_alpha = nullptr;
     int32_t mf_rows = 1, mf_groups = 1, mf_smem_inc = 0;
+    int32_t *d_sym_lptr = nullptr, *d_sym_lidx = nullptr, *d_sym_lcol = nullptr, *d_sym_scol = nullptr;
+    int2* d_sym_urange = nullptr;
+    int64_t n_stored = 0;                                  // value blocks held (assembled kernels)
     double *d_scratch_u = nullptr, *d_scratch_y = nullptr;
     std::vector<int32_t> map_own;                          // host copy (ens_get_owned)
 };
@@ -180,7 +183,7 @@ int check_opts(const ens_options* opt) {
     if (!opt) return ENS_OK;
     if (!(std::isfinite(opt->dt))) return fail(nullptr, ENS_E_ARG, "opt->dt is not finite");
     if (opt->damping < 0 || opt->damping > 2) return fail(nullptr, ENS_E_ARG, "opt->damping must be 0, 1 or 2");
-    if (opt->kernel < 0 || opt->kernel > 1) return fail(nullptr, ENS_E_ARG, "opt->kernel must be 0 or 1");
+    if (opt->kernel < 0 || opt->kernel > 2) return fail(nullptr, ENS_E_ARG, "opt->kernel must be 0, 1 or 2");
     if (!(opt->c_d >= 0.0) || !std::isfinite(opt->c_d)) return fail(nullptr, ENS_E_ARG, "opt->c_d must be finite and >= 0");
     if (opt->dist < 0 || opt->dist > 2) return fail(nullptr, ENS_E_ARG, "opt->dist must be 0, 1 or 2");
     if (opt->dist == ENS_DIST_NODE) {
@@ -237,6 +240,11 @@ ens::StepArgs part_args(const ens_ctx* c, const Part& p) {
     a.mf_rows = p.mf_rows;
     a.mf_groups = p.mf_groups;
     a.mf_smem_inc = p.mf_smem_inc;
+    a.sym_lptr = p.d_sym_lptr;
+    a.sym_lidx = p.d_sym_lidx;
+    a.sym_lcol = p.d_sym_lcol;
+    a.sym_urange = p.d_sym_urange;
+    a.sym_scol = p.d_sym_scol;
     a.c1 = p.d_c1;
     a.c2a = p.d_c2a;
     a.c3a = p.d_c3a;
@@ -263,8 +271,11 @@ cudaError_t launch_rows(const ens_ctx* c, ens::StepArgs a, int64_t row0, int64_t
     if (rows <= 0) return cudaSuccess;
     a.row0 = row0;
     a.V = rows;
-    return c->kernel == ENS_KERNEL_MATRIX_FREE ? ens::launch_step_matrix_free(a, st)
-                                               : ens::launch_step_assembled(a, st);
+    switch (c->kernel) {
+        case ENS_KERNEL_MATRIX_FREE: return ens::launch_step_matrix_free(a, st);
+        case ENS_KERNEL_ASSEMBLED_SYM: return ens::launch_step_assembled_sym(a, st);
+        default: return ens::launch_step_assembled(a, st);
+    }
 }
 
 // ---- one time step of every part (step index = ctx step + k) ---------------------------
@@ -443,17 +454,65 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
     std::vector<double> al(size_t(Fl * n_s));
     for (int64_t k = 0; k < Fl; ++k)
         for (int64_t s = 0; s < n_s; ++s) al[size_t(k * n_s + s)] = (*G.alpha)[size_t(s * G.m->F + elems[size_t(k)])];
-    if (c->kernel == ENS_KERNEL_ASSEMBLED) {
-        // F0 on the owned blocks: contributions re-indexed to local elements
-        std::vector<int32_t> cp(size_t(b1 - b0) + 1), cc;
+    if (c->kernel == ENS_KERNEL_ASSEMBLED || c->kernel == ENS_KERNEL_ASSEMBLED_SYM) {
+        // the global (full-CSR) blocks whose values this part stores
+        std::vector<int64_t> blocks;
+        if (c->kernel == ENS_KERNEL_ASSEMBLED) {
+            for (int64_t b = b0; b < b1; ++b) blocks.push_back(b);
+        } else {
+            // half storage: row i keeps its blocks (i, j >= i); its blocks (i, j < i) are the
+            // transposes of blocks (j, i), stored with row j if j is owned, else copied here
+            std::vector<int32_t> lp(size_t(P.n_own) + 1, 0), li, lc, sc;
+            std::vector<int2> ur(static_cast<size_t>(P.n_own));
+            std::vector<int32_t> upper_at(size_t(b1 - b0), -1);
+            auto find_block = [&](int32_t r, int32_t j) {
+                auto first = pat.col.begin() + pat.row_ptr[size_t(r)];
+                auto last = pat.col.begin() + pat.row_ptr[size_t(r) + 1];
+                return int64_t(std::lower_bound(first, last, j) - pat.col.begin());
+            };
+            for (int64_t i = lo; i < hi; ++i) {
+                for (int64_t b = pat.row_ptr[size_t(i)]; b < pat.row_ptr[size_t(i) + 1]; ++b) {
+                    const int32_t j = pat.col[size_t(b)];
+                    if (j >= i) continue;
+                    int32_t idx;
+                    if (j >= lo) {
+                        idx = upper_at[size_t(find_block(j, int32_t(i)) - b0)];
+                    } else {
+                        idx = int32_t(blocks.size());
+                        blocks.push_back(find_block(j, int32_t(i)));
+                        sc.push_back(-1);
+                    }
+                    li.push_back(idx);
+                    lc.push_back(local(j));
+                }
+                lp[size_t(i - lo) + 1] = int32_t(li.size());
+                ur[size_t(i - lo)].x = int32_t(blocks.size());
+                for (int64_t b = pat.row_ptr[size_t(i)]; b < pat.row_ptr[size_t(i) + 1]; ++b) {
+                    const int32_t j = pat.col[size_t(b)];
+                    if (j < i) continue;
+                    upper_at[size_t(b - b0)] = int32_t(blocks.size());
+                    blocks.push_back(b);
+                    sc.push_back(local(j));
+                }
+                ur[size_t(i - lo)].y = int32_t(blocks.size());
+            }
+            RC_TRY(upload(c, &P.d_sym_lptr, lp.data(), lp.size()));
+            RC_TRY(upload(c, &P.d_sym_lidx, li.data(), li.size()));
+            RC_TRY(upload(c, &P.d_sym_lcol, lc.data(), lc.size()));
+            RC_TRY(upload(c, &P.d_sym_urange, ur.data(), ur.size()));
+            RC_TRY(upload(c, &P.d_sym_scol, sc.data(), sc.size()));
+        }
+        P.n_stored = int64_t(blocks.size());
+        // F0 on the stored blocks: contributions re-indexed to local elements
+        std::vector<int32_t> cp(blocks.size() + 1), cc;
         const auto& gcp = *G.contrib_ptr;
         const auto& gc = *G.contrib;
-        for (int64_t b = b0; b < b1; ++b) {
-            cp[size_t(b - b0)] = int32_t(cc.size());
-            for (int32_t q = gcp[size_t(b)]; q < gcp[size_t(b) + 1]; ++q)
+        for (size_t k = 0; k < blocks.size(); ++k) {
+            cp[k] = int32_t(cc.size());
+            for (int32_t q = gcp[size_t(blocks[k])]; q < gcp[size_t(blocks[k]) + 1]; ++q)
                 cc.push_back(eloc[size_t(gc[size_t(q)] / 9)] * 9 + gc[size_t(q)] % 9);
         }
-        cp[size_t(b1 - b0)] = int32_t(cc.size());
+        cp[blocks.size()] = int32_t(cc.size());
         std::vector<double> kh(size_t(Fl) * 81);
         for (int64_t k = 0; k < Fl; ++k)
             std::copy_n(G.Khat->data() + size_t(elems[size_t(k)]) * 81, 81, kh.data() + size_t(k) * 81);
@@ -463,8 +522,8 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
         RC_TRY(upload(c, &d_cc, cc.data(), cc.size()));
         RC_TRY(upload(c, &d_al, al.data(), al.size()));
         RC_TRY(upload(c, &d_kh, kh.data(), kh.size()));
-        RC_TRY(dalloc(c, &P.d_Kval, size_t(b1 - b0) * 9 * size_t(n_s)));
-        CUDA_TRY(c, ens::launch_assemble(b1 - b0, c->n_s, d_cp, d_cc, d_al, d_kh, P.d_Kval, c->stream));
+        RC_TRY(dalloc(c, &P.d_Kval, blocks.size() * 9 * size_t(n_s)));
+        CUDA_TRY(c, ens::launch_assemble(int64_t(blocks.size()), c->n_s, d_cp, d_cc, d_al, d_kh, P.d_Kval, c->stream));
         CUDA_TRY(c, cudaStreamSynchronize(c->stream));
         dfree(c, d_cp);
         dfree(c, d_cc);
@@ -558,7 +617,7 @@ int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, cons
     // element -> block contributions (assembled) or fans (matrix-free), global
     std::vector<int32_t> cptr, contrib;
     ens::Fans fans;
-    if (c->kernel == ENS_KERNEL_ASSEMBLED) {
+    if (c->kernel != ENS_KERNEL_MATRIX_FREE) {
         cptr.assign(size_t(c->nnzb) + 1, 0);
         contrib.resize(size_t(9 * F));
         std::vector<int32_t> blk(size_t(9 * F));
@@ -917,8 +976,13 @@ int ens_query(const ens_ctx* c, ens_info* info) {
     info->halo_bytes_per_step = halo * 3 * 8 * ns;
     info->launches_per_step = int32_t(launches);
     const double frac = c->V ? double(own) / double(c->V) : 1.0;
+    int64_t stored = 0;
+    for (const Part& p : c->parts) stored += p.n_stored;
     if (c->kernel == ENS_KERNEL_ASSEMBLED) {
         info->bytes_per_step = int64_t(frac * double(ns * (72 * c->nnzb + per_node * c->V)));
+        info->flops_per_step = int64_t(frac * double(ns * (18 * c->nnzb + 3 * 5 * c->V)));
+    } else if (c->kernel == ENS_KERNEL_ASSEMBLED_SYM) {
+        info->bytes_per_step = ns * (72 * stored + int64_t(frac * double(per_node * c->V)));
         info->flops_per_step = int64_t(frac * double(ns * (18 * c->nnzb + 3 * 5 * c->V)));
     } else {
         info->bytes_per_step = int64_t(frac * double(ns * (8 * c->F + per_node * c->V) + 648 * c->F));

@@ -21,6 +21,12 @@ struct StepArgs {
     const int32_t* row_ptr = nullptr;   // [rows + 1] (int32: nnzb < 2^31)
     const int32_t* col = nullptr;
     const double* Kval = nullptr;
+    // symmetric (half) block storage: Kval holds the stored blocks
+    const int32_t* sym_lptr = nullptr;  // [rows + 1] lower references of each row
+    const int32_t* sym_lidx = nullptr;  // stored block (j, i) used transposed by row i
+    const int32_t* sym_lcol = nullptr;  // its column j (< i)
+    const int2* sym_urange = nullptr;   // [rows] stored blocks (i, j >= i) of row i
+    const int32_t* sym_scol = nullptr;  // [stored] column of each stored block
     // matrix-free operands (host_setup.hpp "Fans")
     const int32_t* inc_ptr = nullptr;   // [rows + 1] incidence range of each row
     const int4* fan = nullptr;          // [3F] {e, n_prev, n_next, restart}
@@ -56,6 +62,8 @@ struct StepArgs {
 // Fused step (S2 load + S3 ensemble SpMM + S4 central-difference update) on the
 // assembled values: one launch advances rows [row0, row0+V) by one step.
 cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st);
+// Same on the symmetric half storage (blocks j >= i stored; bit-identical results).
+cudaError_t launch_step_assembled_sym(const StepArgs& a, cudaStream_t st);
 // Same on the matrix-free element form (alpha_{e,s} K^_e gathered per node).
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st);
 // realisations per thread of the step kernels for a given N_s (4, 2 or 1)

@@ -57,6 +57,22 @@ __device__ __forceinline__ Vec<4> ld_stream<4>(const double* p, uint64_t) {
     return r;
 }
 
+// Symmetric storage: each stored block is read twice (by its row and, transposed, by its
+// column's row within the RCM bandwidth), so no L1 allocation but the normal L2 policy.
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ld_once_l1(const double* p) {
+    Vec<VEC> r;
+    if constexpr (VEC == 1) {
+        asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r.v[0]) : "l"(p));
+    } else if constexpr (VEC == 2) {
+        asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
+    } else {
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+                     : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
+    }
+    return r;
+}
+
 // u_n and the coefficient arrays: read-only within a launch, re-used across rows via L1/L2.
 template <int VEC>
 __device__ __forceinline__ Vec<VEC> ld_ro(const double* p) {
@@ -319,6 +335,81 @@ k_step_assembled(const StepArgs a) {
     }
 }
 
+// ---- F1s: fused step on symmetric (half) block storage ----------------------------------
+// K_s is symmetric (Eq. 10: B^T C B), so only the blocks (i, j >= i) are stored; row i takes
+// its blocks (i, j < i) as the transposes of blocks stored with row j (within the RCM
+// bandwidth, so still in L2).  Lower references (j ascending) then the row's own upper
+// blocks (j ascending) visit the columns in exactly the order of the full CSR row, and
+// K^_e is exactly symmetric, so the result is bit-identical to F1 with ~half the bytes.
+template <int VEC, bool APPLY, bool PREF>
+__global__ void __launch_bounds__(kThreads)
+k_step_assembled_sym(const StepArgs a) {
+    __shared__ double s_coef[kMaxFields];
+    const StepCtx sc = step_ctx(a);
+    if (!APPLY && threadIdx.x == 0) load_coeffs(a, double(sc.step) * a.dt, s_coef);
+    if (!APPLY) __syncthreads();
+
+    const int P = a.n_s / VEC;
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (tid >= a.V * P) return;
+    const int64_t i = a.row0 + tid / P;
+    const int s0 = int(tid % P) * VEC;
+    const int n_s = a.n_s;
+
+    Upd<VEC> upd;
+    if constexpr (!APPLY && PREF) upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
+
+    double y[3][VEC];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) y[c][v] = 0.0;
+
+    const int32_t l_end = __ldg(a.sym_lptr + i + 1);
+#pragma unroll 2
+    for (int32_t k = __ldg(a.sym_lptr + i); k < l_end; ++k) {          // blocks (i, j < i) = (j, i)^T
+        const int64_t b = __ldg(a.sym_lidx + k);
+        const int64_t j = __ldg(a.sym_lcol + k);
+        const double* kp = a.Kval + b * 9 * n_s + s0;
+        const double* up = sc.un + j * 3 * n_s + s0;
+        Vec<VEC> u[3], kk[9];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) u[d] = ld_ro<VEC>(up + d * n_s);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) kk[e] = ld_once_l1<VEC>(kp + e * n_s);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) y[c][v] = fma(kk[3 * d + c].v[v], u[d].v[v], y[c][v]);
+    }
+    const int2 ur = a.sym_urange[i];
+#pragma unroll 2
+    for (int32_t b = ur.x; b < ur.y; ++b) {                              // stored blocks (i, j >= i)
+        const int64_t j = __ldg(a.sym_scol + b);
+        const double* kp = a.Kval + int64_t(b) * 9 * n_s + s0;
+        const double* up = sc.un + j * 3 * n_s + s0;
+        Vec<VEC> u[3], kk[9];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) u[d] = ld_ro<VEC>(up + d * n_s);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) kk[e] = ld_once_l1<VEC>(kp + e * n_s);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) y[c][v] = fma(kk[3 * c + d].v[v], u[d].v[v], y[c][v]);
+    }
+    if constexpr (APPLY) {
+        store_y<VEC>(a, i, s0, y);
+    } else {
+        if constexpr (!PREF) upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
+        upd_store<VEC>(a, sc, i, s0, y, upd);
+    }
+}
+
 // ---- F2: fused step on the matrix-free element form ------------------------------------
 // y[i][c][s] = sum over the incidences (e, a) of row i of alpha[e][s] * sum_{b, d}
 //              K^_e[3a+c][3 loc(b) + d] u[node_b][d][s]
@@ -526,13 +617,6 @@ inline unsigned grid_for(int64_t n) { return unsigned((n + kThreads - 1) / kThre
 
 }  // namespace
 
-static bool a1_prefetch() {
-    static int v = [] {
-        const char* e = std::getenv("ENS_A1_PREFETCH");
-        return e ? std::atoi(e) : 1;
-    }();
-    return v != 0;
-}
 
 template <int VEC, bool APPLY>
 static cudaError_t launch_a1(const StepArgs& a, cudaStream_t st) {
@@ -569,6 +653,32 @@ int pick_vec(int32_t n_s) {
     return n_s % 2 == 0 ? 2 : 1;
 }
 
+static bool a1_prefetch() {
+    static int v = [] {
+        const char* e = std::getenv("ENS_A1_PREFETCH");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v != 0;
+}
+
+template <int VEC, bool APPLY>
+static cudaError_t launch_a1s(const StepArgs& a, cudaStream_t st) {
+    const int64_t n = a.V * (a.n_s / VEC);
+    if (n == 0) return cudaSuccess;
+    if (a1_prefetch()) k_step_assembled_sym<VEC, APPLY, true><<<grid_for(n), kThreads, 0, st>>>(a);
+    else k_step_assembled_sym<VEC, APPLY, false><<<grid_for(n), kThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_step_assembled_sym(const StepArgs& a, cudaStream_t st) {
+    const bool apply = a.y_out != nullptr;
+    switch (pick_vec(a.n_s)) {
+        case 4: return apply ? launch_a1s<4, true>(a, st) : launch_a1s<4, false>(a, st);
+        case 2: return apply ? launch_a1s<2, true>(a, st) : launch_a1s<2, false>(a, st);
+        default: return apply ? launch_a1s<1, true>(a, st) : launch_a1s<1, false>(a, st);
+    }
+}
+
 cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st) {
     const bool apply = a.y_out != nullptr;
     switch (pick_vec(a.n_s)) {
@@ -584,7 +694,7 @@ cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st) {
 int mf_variant() {
     static int v = [] {
         const char* e = std::getenv("ENS_MF_VARIANT");
-        return e ? std::atoi(e) : 0;
+        return e ? std::atoi(e) : 1;
     }();
     return v;
 }

@@ -14,7 +14,7 @@ from . import _ffi
 from ._ffi import EnsError, check, lib
 
 DAMPING = {"none": 0, "mass": 1, "identity": 2, 0: 0, 1: 1, 2: 2}
-KERNEL = {"assembled": 0, "matrix_free": 1, 0: 0, 1: 1}
+KERNEL = {"assembled": 0, "matrix_free": 1, "assembled_sym": 2, 0: 0, 1: 1, 2: 2}
 DIST = {"single": 0, "node": 1, "ensemble": 2, 0: 0, 1: 1, 2: 2}
 
 
@@ -278,3 +278,14 @@ def host_halo_plan(row_ptr, col, P, part):
             "n_ghost": int(lhb[4]),
             "peers": [(int(peers[k]), *map(int, info[k])) for k in range(npe.value)],
             "send_rows": send[:ns.value].copy()}
+
+
+def nccl_comm_of(group=None, device=None) -> int:
+    """ncclComm_t (as an int) of torch's ProcessGroupNCCL for `group` (default group): the
+    communicator ENS_DIST_NODE exchanges its halo on.  The group must be initialised with
+    device_id (eager NCCL init) or have run a collective."""
+    import torch
+    import torch.distributed as dist
+    pg = group or dist.distributed_c10d._get_default_group()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    return int(pg._get_backend(dev)._comm_ptr())

@@ -44,7 +44,7 @@ def _check_spmm(ens, om, u):
     assert np.all(np.abs(y - yo) <= 4 * nnz_row * EPS * absKu + 1e-300)
 
 
-@pytest.mark.parametrize("kernel", ["assembled", "matrix_free"])
+@pytest.mark.parametrize("kernel", ["assembled", "assembled_sym", "matrix_free"])
 @pytest.mark.parametrize("n_s", [1, 3, 4, 6, 64, 128])
 def test_spmm_parity(kernel, n_s):
     """Several tiles and a ragged tail: 40 x 51 rings, V = 2,040, N_s odd/even/x4."""
@@ -106,7 +106,7 @@ def test_pulsatile_damped_parity(damping, c_d):
     ens.close()
 
 
-@pytest.mark.parametrize("kernel", ["assembled", "matrix_free"])
+@pytest.mark.parametrize("kernel", ["assembled", "assembled_sym", "matrix_free"])
 def test_ensemble_equivalence_bitexact(kernel):
     """N_s = 8 together (VEC = 2 lanes) == each realisation alone (VEC = 1): bit for bit."""
     m = meshmod.cylinder(24, 40)
@@ -247,7 +247,7 @@ def test_c2_laplace_law_on_gpu():
     ens.close()
 
 
-@pytest.mark.parametrize("kernel", ["assembled", "matrix_free"])
+@pytest.mark.parametrize("kernel", ["assembled", "assembled_sym", "matrix_free"])
 @pytest.mark.parametrize("P", [2, 3, 4])
 def test_node_partition_bitexact(kernel, P):
     """ENS_DIST_NODE (all P parts in one context, halo by device copies): boundary rows
@@ -276,3 +276,22 @@ def test_node_partition_bitexact(kernel, P):
         e.step(40)
     assert np.array_equal(ref.get_state()[0], par.get_state()[0])
     ref.close(); par.close()
+
+
+def test_symmetric_storage_bitexact_vs_full():
+    """ASSEMBLED_SYM stores only blocks (i, j >= i) and reads (j, i)^T for j < i, in the
+    full row's column order: bit-identical to ASSEMBLED, with fewer value bytes."""
+    m = meshmod.shuffle_nodes(meshmod.cylinder(32, 41), 5)
+    E, h = _mats(m, 64, 71)
+    tr = loads.pulsatile(m.xyz, m.tris, period=0.01, systole=0.004, ramp_T=0.003)
+    out = []
+    for kernel in ("assembled", "assembled_sym"):
+        e = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, kernel=kernel,
+                            damping="mass", c_d=100.0)
+        e.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+        e.step(300)
+        out.append((e.get_state(), e.info()))
+        e.close()
+    (a, ia), (b, ib) = out
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert ib["bytes_per_step"] < 0.7 * ia["bytes_per_step"]
