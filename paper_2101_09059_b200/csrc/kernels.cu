@@ -618,6 +618,14 @@ inline unsigned grid_for(int64_t n) { return unsigned((n + kThreads - 1) / kThre
 }  // namespace
 
 
+static bool a1_prefetch() {
+    static int v = [] {
+        const char* e = std::getenv("ENS_A1_PREFETCH");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v != 0;
+}
+
 template <int VEC, bool APPLY>
 static cudaError_t launch_a1(const StepArgs& a, cudaStream_t st) {
     const int64_t n = a.V * (a.n_s / VEC);
@@ -653,13 +661,6 @@ int pick_vec(int32_t n_s) {
     return n_s % 2 == 0 ? 2 : 1;
 }
 
-static bool a1_prefetch() {
-    static int v = [] {
-        const char* e = std::getenv("ENS_A1_PREFETCH");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v != 0;
-}
 
 template <int VEC, bool APPLY>
 static cudaError_t launch_a1s(const StepArgs& a, cudaStream_t st) {
