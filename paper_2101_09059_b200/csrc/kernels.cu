@@ -438,21 +438,72 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     }
 }
 
-template <int VEC, bool APPLY, int BATCH, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
+template <int VEC>
+__device__ __forceinline__ void cp_async_vec_s(uint32_t dst, const double* src) {
+    if constexpr (VEC == 1) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(dst), "l"(src) : "memory");
+    } else if constexpr (VEC == 2) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+    } else {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst + 16), "l"(src + 2) : "memory");
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> lds_vec(const double* p) {
+    Vec<VEC> r;
+    if constexpr (VEC == 1) {
+        r.v[0] = *p;
+    } else if constexpr (VEC == 2) {
+        const double2 t = *reinterpret_cast<const double2*>(p);
+        r.v[0] = t.x; r.v[1] = t.y;
+    } else {
+        const double2 t0 = *reinterpret_cast<const double2*>(p), t1 = *reinterpret_cast<const double2*>(p + 2);
+        r.v[0] = t0.x; r.v[1] = t0.y; r.v[2] = t1.x; r.v[3] = t1.y;
+    }
+    return r;
+}
+
+// A CTA owns R consecutive rows (RCM order) and a chunk of W = G * VEC realisations.  Before
+// any arithmetic it stages everything its rows touch into shared memory:
+//   * one thread: K^ rows (224 B per incidence) + incidence records by 1-D TMA bulk copies
+//     completing on an mbarrier (contiguous: the CTA's rows are contiguous);
+//   * all threads: cp.async (LDGSTS) of the u_n rows of the CTA's node set (own rows first,
+//     then every neighbour its incidences reach), alpha of its elements, and the update
+//     operands (c1 [c2 c3], u_{n-1}, F_k) of its own rows.
+// The gather then runs entirely out of shared memory.
+template <int VEC, bool APPLY>
+__global__ void __launch_bounds__(kThreads)
 k_step_matrix_free(const StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double s_coef[kMaxFields];
     __shared__ __align__(8) uint64_t s_bar;
 
     const StepCtx sc = step_ctx(a);
-    const int G = a.mf_groups, R = a.mf_rows;
-    const int64_t r0 = a.row0 + int64_t(blockIdx.x) * R;
+    const int G = a.mf_groups, R = a.mf_rows, W = G * VEC;
+    const int n_s = a.n_s;
+    const int sbase = int(blockIdx.y) * W;
+    const int wv = min(W, n_s - sbase);                  // realisations of this chunk
+    const int64_t cta = a.row0 / R + blockIdx.x;          // launch ranges are R-aligned
+    const int64_t r0 = cta * R;
     const int64_t r1 = min(r0 + R, a.row0 + a.V);
+    const int nr = int(r1 - r0);
     const int32_t k0 = __ldg(a.inc_ptr + r0), k1 = __ldg(a.inc_ptr + r1);
     const uint32_t n_inc = uint32_t(k1 - k0);
+    const int32_t nd0 = __ldg(a.mf_node_ptr + cta), n_nodes = __ldg(a.mf_node_ptr + cta + 1) - nd0;
+    const int32_t el0 = __ldg(a.mf_el_ptr + cta), n_els = __ldg(a.mf_el_ptr + cta + 1) - el0;
+    const bool c23 = a.c2a != nullptr;
+
+    // shared-memory carve-up (sizes use the per-launch maxima)
     double* sK = reinterpret_cast<double*>(smem);
-    const int4* sRec = reinterpret_cast<const int4*>(smem + size_t(a.mf_smem_inc) * 224);
+    int4* sRec = reinterpret_cast<int4*>(sK + size_t(a.mf_smem_inc) * 28);
+    double* sU = reinterpret_cast<double*>(sRec + a.mf_smem_inc);
+    double* sA = sU + size_t(a.mf_nodes_max) * 3 * W;
+    double* sC = sA + size_t(a.mf_els_max) * W;            // c1 [, c2, c3] of own rows
+    double* sO = sC + size_t(R) * (c23 ? 3 : 1) * W;       // u_{n-1} of own rows
+    double* sF = sO + size_t(R) * 3 * W;                   // F_k of own rows
+
     const uint32_t bar = uint32_t(__cvta_generic_to_shared(&s_bar));
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
@@ -463,90 +514,122 @@ k_step_matrix_free(const StepArgs a) {
         }
         if (!APPLY) load_coeffs(a, double(sc.step) * a.dt, s_coef);
     }
+    // cooperative LDGSTS staging
+    const int nvw = wv / VEC;                              // vectors per (node, component)
+    const int nthr = int(blockDim.x);
+    for (int idx = int(threadIdx.x); idx < n_nodes * 3 * nvw; idx += nthr) {
+        const int k = idx / (3 * nvw), rem = idx - k * 3 * nvw, c = rem / nvw, j = rem - c * nvw;
+        const int64_t node = __ldg(a.mf_nodes + nd0 + k);
+        cp_async_vec_s<VEC>(uint32_t(__cvta_generic_to_shared(sU + (size_t(k) * 3 + c) * W + j * VEC)),
+                            sc.un + (node * 3 + c) * n_s + sbase + j * VEC);
+    }
+    for (int idx = int(threadIdx.x); idx < n_els * nvw; idx += nthr) {
+        const int k = idx / nvw, j = idx - k * nvw;
+        const int64_t e = __ldg(a.mf_els + el0 + k);
+        cp_async_vec_s<VEC>(uint32_t(__cvta_generic_to_shared(sA + size_t(k) * W + j * VEC)),
+                            a.alpha + e * n_s + sbase + j * VEC);
+    }
+    if (!APPLY) {
+        for (int idx = int(threadIdx.x); idx < nr * nvw; idx += nthr) {
+            const int r = idx / nvw, j = idx - r * nvw;
+            const int64_t row = r0 + r;
+            cp_async_vec_s<VEC>(uint32_t(__cvta_generic_to_shared(sC + size_t(r) * W + j * VEC)),
+                                a.c1 + row * n_s + sbase + j * VEC);
+            if (c23) {
+                cp_async_vec_s<VEC>(uint32_t(__cvta_generic_to_shared(sC + size_t(R + r) * W + j * VEC)),
+                                    a.c2a + row * n_s + sbase + j * VEC);
+                cp_async_vec_s<VEC>(uint32_t(__cvta_generic_to_shared(sC + size_t(2 * R + r) * W + j * VEC)),
+                                    a.c3a + row * n_s + sbase + j * VEC);
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                cp_async_vec_s<VEC>(uint32_t(__cvta_generic_to_shared(sO + (size_t(r) * 3 + c) * W + j * VEC)),
+                                    sc.uo + (row * 3 + c) * n_s + sbase + j * VEC);
+        }
+        for (int idx = int(threadIdx.x); idx < nr * 3 * a.n_fields; idx += nthr) {
+            const int r = idx / (3 * a.n_fields), rem = idx - r * 3 * a.n_fields, k = rem / 3, c = rem - k * 3;
+            sF[idx] = __ldg(a.Fk + (int64_t(k) * a.fk_rows + r0 + r) * 3 + c);
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    if (n_inc) mbar_wait(bar, 0);
 
-    const int P = a.n_s / VEC;
     const int lr = int(threadIdx.x) / G;
-    const int g = int(blockIdx.y) * G + int(threadIdx.x) % G;
+    const int g = int(threadIdx.x) % G;
+    if (lr >= nr || g >= nvw) return;
     const int64_t i = r0 + lr;
-    const bool valid = lr < R && i < r1 && g < P;
-    const int n_s = a.n_s;
-    const int s0 = g * VEC;
-    const double* un_base = sc.un + s0;
+    const int w0 = g * VEC;
 
     double y[3][VEC];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int v = 0; v < VEC; ++v) y[c][v] = 0.0;
-    Vec<VEC> uo[3], up[3];
-    if (valid) {
+    Vec<VEC> uo[3];
 #pragma unroll
-        for (int d = 0; d < 3; ++d) uo[d] = ld_ro<VEC>(un_base + (i * 3 + d) * n_s);
-    }
-    double* slot = reinterpret_cast<double*>(smem + size_t(a.mf_smem_inc) * 240) + size_t(threadIdx.x) * 6 * VEC;
-    if (!APPLY && valid) upd_load_async<VEC>(a, sc, i, s0, slot);
-    if (n_inc) mbar_wait(bar, 0);
-    if (!valid) return;
+    for (int d = 0; d < 3; ++d) uo[d] = lds_vec<VEC>(sU + (size_t(lr) * 3 + d) * W + w0);   // own row = slot lr
 
     const int32_t kb = __ldg(a.inc_ptr + i) - k0, ke = __ldg(a.inc_ptr + i + 1) - k0;
-    if (kb < ke) {                               // the row's first chain starts at kb
-        const int4 r = sRec[kb];
+    for (int32_t k = kb; k < ke; ++k) {
+        const int4 rec = sRec[k];
+        const double* K = sK + size_t(k) * 28;
+        const double* Up = sU + size_t(rec.y) * 3 * W + w0;
+        const double* Un = sU + size_t(rec.z) * 3 * W + w0;
+        const Vec<VEC> al = lds_vec<VEC>(sA + size_t(rec.x) * W + w0);
 #pragma unroll
-        for (int d = 0; d < 3; ++d) up[d] = ld_ro<VEC>(un_base + (int64_t(r.y) * 3 + d) * n_s);
-    }
-    for (int32_t k = kb; k < ke; k += BATCH) {
-        // gather phase: every load of the batch in flight before any arithmetic
-        int4 rec[BATCH];
-        Vec<VEC> un[BATCH][3], al[BATCH];
+        for (int c = 0; c < 3; ++c) {
+            double t[VEC];
 #pragma unroll
-        for (int j = 0; j < BATCH; ++j) {
-            if (k + j < ke) {
-                rec[j] = sRec[k + j];
+            for (int v = 0; v < VEC; ++v) t[v] = 0.0;
 #pragma unroll
-                for (int d = 0; d < 3; ++d) un[j][d] = ld_ro<VEC>(un_base + (int64_t(rec[j].z) * 3 + d) * n_s);
-                al[j] = ld_ro<VEC>(a.alpha + int64_t(rec[j].x) * n_s + s0);
-            }
-        }
+            for (int d = 0; d < 3; ++d) {
+                const Vec<VEC> up = lds_vec<VEC>(Up + d * W), un = lds_vec<VEC>(Un + d * W);
+                const double k_own = K[9 * c + d], k_prev = K[9 * c + 3 + d], k_next = K[9 * c + 6 + d];
 #pragma unroll
-        for (int j = 0; j < BATCH; ++j) {
-            if (k + j >= ke) break;
-            if (rec[j].w && k + j != kb) {       // a further chain (non-manifold vertex): rare
-#pragma unroll
-                for (int d = 0; d < 3; ++d) up[d] = ld_ro<VEC>(un_base + (int64_t(rec[j].y) * 3 + d) * n_s);
-            }
-            const double* K = sK + size_t(k + j) * 28;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                double t[VEC];
-#pragma unroll
-                for (int v = 0; v < VEC; ++v) t[v] = 0.0;
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const double k_own = K[9 * c + d], k_prev = K[9 * c + 3 + d], k_next = K[9 * c + 6 + d];
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) {
-                        t[v] = fma(k_own, uo[d].v[v], t[v]);
-                        t[v] = fma(k_prev, up[d].v[v], t[v]);
-                        t[v] = fma(k_next, un[j][d].v[v], t[v]);
-                    }
+                for (int v = 0; v < VEC; ++v) {
+                    t[v] = fma(k_own, uo[d].v[v], t[v]);
+                    t[v] = fma(k_prev, up.v[v], t[v]);
+                    t[v] = fma(k_next, un.v[v], t[v]);
                 }
-#pragma unroll
-                for (int v = 0; v < VEC; ++v) y[c][v] = fma(al[j].v[v], t[v], y[c][v]);
             }
 #pragma unroll
-            for (int d = 0; d < 3; ++d) up[d] = un[j][d];
+            for (int v = 0; v < VEC; ++v) y[c][v] = fma(al.v[v], t[v], y[c][v]);
         }
     }
+    const int s0 = sbase + w0;
     if constexpr (APPLY) {
         store_y<VEC>(a, i, s0, y);
     } else {
-        Upd<VEC> upd;
-        upd_collect<VEC>(a, s_coef, i, slot, upd);
+        Upd<VEC> u;
+        u.fx = a.fixed ? __ldg(a.fixed + i) : uint8_t(0);
+        u.c1 = lds_vec<VEC>(sC + size_t(lr) * W + w0);
+        if (c23) {
+            u.c2 = lds_vec<VEC>(sC + size_t(R + lr) * W + w0);
+            u.c3 = lds_vec<VEC>(sC + size_t(2 * R + lr) * W + w0);
+        } else {
 #pragma unroll
-        for (int d = 0; d < 3; ++d) upd.un[d] = uo[d];
-        upd_store<VEC>(a, sc, i, s0, y, upd);
+            for (int v = 0; v < VEC; ++v) { u.c2.v[v] = a.c2; u.c3.v[v] = a.c3; }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            u.un[c] = uo[c];
+            u.uo[c] = lds_vec<VEC>(sO + (size_t(lr) * 3 + c) * W + w0);
+            double f = 0.0;
+            for (int k = 0; k < a.n_fields; ++k) f = fma(s_coef[k], sF[(lr * a.n_fields + k) * 3 + c], f);
+            u.f[c] = f;
+        }
+        upd_store<VEC>(a, sc, i, s0, y, u);
     }
+}
+
+size_t mf_smem_bytes_impl(const StepArgs& a, int vec) {
+    const size_t W = size_t(a.mf_groups) * vec, R = size_t(a.mf_rows);
+    const bool c23 = a.c2a != nullptr;
+    return size_t(a.mf_smem_inc) * 240 + (size_t(a.mf_nodes_max) * 3 * W + size_t(a.mf_els_max) * W +
+                                          R * (c23 ? 3 : 1) * W + R * 3 * W) * sizeof(double) +
+           R * 3 * kMaxFields * sizeof(double);
 }
 
 __global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
@@ -635,20 +718,20 @@ static cudaError_t launch_a1(const StepArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int VEC, bool APPLY, int BATCH, int MINB>
+template <int VEC, bool APPLY>
 static cudaError_t launch_a2(const StepArgs& a, cudaStream_t st) {
     if (a.V == 0) return cudaSuccess;
     const int P = a.n_s / VEC;
-    const size_t smem = size_t(a.mf_smem_inc) * 240 + size_t(a.mf_rows * a.mf_groups) * 6 * VEC * sizeof(double);
+    const size_t smem = mf_smem_bytes_impl(a, VEC);
     static bool attr_set = false;      // per template instance
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free<VEC, APPLY, BATCH, MINB>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free<VEC, APPLY>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     dim3 grid(unsigned((a.V + a.mf_rows - 1) / a.mf_rows), unsigned((P + a.mf_groups - 1) / a.mf_groups));
-    k_step_matrix_free<VEC, APPLY, BATCH, MINB><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(a);
+    k_step_matrix_free<VEC, APPLY><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -689,33 +772,14 @@ cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st) {
     }
 }
 
-// Matrix-free variants (tuning knob ENS_MF_VARIANT = 0..3):
-//   0: VEC 2, batch 1, >= 2 CTAs/SM   1: VEC 2, batch 2, >= 2 CTAs/SM
-//   2: VEC 1, batch 2, >= 3 CTAs/SM   3: VEC 1, batch 1, >= 4 CTAs/SM
-int mf_variant() {
-    static int v = [] {
-        const char* e = std::getenv("ENS_MF_VARIANT");
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
-}
+int pick_vec_mf(int32_t n_s) { return n_s % 2 ? 1 : 2; }
 
-int pick_vec_mf(int32_t n_s) {
-    const int v = mf_variant();
-    if (v >= 2 || n_s % 2) return 1;
-    return 2;
-}
+size_t mf_smem_bytes(const StepArgs& a, int vec) { return mf_smem_bytes_impl(a, vec); }
 
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
     const bool ap = a.y_out != nullptr;
-    const int vec = pick_vec_mf(a.n_s);
-    const int var = mf_variant();
-    if (vec == 2) {
-        if (var == 1) return ap ? launch_a2<2, true, 2, 2>(a, st) : launch_a2<2, false, 2, 2>(a, st);
-        return ap ? launch_a2<2, true, 1, 2>(a, st) : launch_a2<2, false, 1, 2>(a, st);
-    }
-    if (var == 3) return ap ? launch_a2<1, true, 1, 4>(a, st) : launch_a2<1, false, 1, 4>(a, st);
-    return ap ? launch_a2<1, true, 2, 3>(a, st) : launch_a2<1, false, 2, 3>(a, st);
+    if (pick_vec_mf(a.n_s) == 2) return ap ? launch_a2<2, true>(a, st) : launch_a2<2, false>(a, st);
+    return ap ? launch_a2<1, true>(a, st) : launch_a2<1, false>(a, st);
 }
 
 cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st) {
