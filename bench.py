@@ -31,7 +31,9 @@ FALLBACK_HBM_GBS = 6650.0      # /opt/skills/guides/B200_PROFILING.md fallback
 
 def _workload_desc(cfg, n_s_total, world):
     m = cfg.mesh
-    return (f"{cfg.name}: ideal cylinder D=4 L=30 cm, {m.meta['n_circ']}x{m.meta['n_axial']} rings "
+    geo = (f"ideal cylinder D=4 L=30 cm, {m.meta['n_circ']}x{m.meta['n_axial']} rings"
+           if m.meta.get("kind") == "cylinder" else "synthetic branched aorta (7 branches)")
+    return (f"{cfg.name}: {geo} "
             f"(V={m.n_nodes}, F={m.n_tris}), N_s={n_s_total} ({cfg.n_s}/GPU), "
             + ("steady 13 mmHg" if len(cfg.traction.tab_t) == 0 else "pulsatile 13+27 mmHg")
             + (f", mode-1 damping {cfg.c_d:g}/s" if cfg.damping == 1 else ", undamped"))
@@ -178,7 +180,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=5000)
     ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--n-s", type=int, default=None, help="realisations per GPU (default: the config's)")
     ap.add_argument("--kernel", default="assembled", choices=["assembled", "assembled_sym", "matrix_free"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -505,18 +505,80 @@ k_step_matrix_free(const StepArgs a) {
     double* sF = sO + size_t(R) * 3 * W;                   // F_k of own rows
 
     const uint32_t bar = uint32_t(__cvta_generic_to_shared(&s_bar));
+    const int nvw = wv / VEC;                              // vectors per (node, component)
+    const bool full = wv == n_s;                           // one chunk covers every realisation
+    // VEC >= 2 (even N_s): every staged segment is a multiple of 16 B -> all by TMA bulk
+    // copies completing on the mbarrier; VEC = 1: u, alpha, c, u_{n-1} by LDGSTS.
+    uint32_t tx = n_inc * 240u;
+    if constexpr (VEC >= 2) {
+        tx += uint32_t(n_nodes * 3 + n_els) * uint32_t(wv) * 8u;
+        if (!APPLY) tx += uint32_t(nr) * uint32_t(wv) * 8u * ((c23 ? 3u : 1u) + 3u);
+    }
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
+        if (tx) mbar_expect_tx(bar, tx);
         if (n_inc) {
-            mbar_expect_tx(bar, n_inc * 240u);
             tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sK)), a.Krow + size_t(k0) * 28, n_inc * 224u, bar);
             tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sRec)), a.fan + k0, n_inc * 16u, bar);
         }
         if (!APPLY) load_coeffs(a, double(sc.step) * a.dt, s_coef);
     }
-    // cooperative LDGSTS staging
-    const int nvw = wv / VEC;                              // vectors per (node, component)
+    __syncthreads();                                       // barrier initialised, tx expected
+    const int warp = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
+    const int nwarps = int(blockDim.x) >> 5;
+    if constexpr (VEC >= 2) {
+        const uint32_t seg = uint32_t(wv) * 8u;
+        if (warp == 0) {                                   // u_n of the CTA's node set
+            for (int k = lane; k < n_nodes; k += 32) {
+                const int64_t node = __ldg(a.mf_nodes + nd0 + k);
+                const uint32_t dst = uint32_t(__cvta_generic_to_shared(sU + size_t(k) * 3 * W));
+                if (full) {
+                    tma_bulk_g2s(dst, sc.un + node * 3 * n_s, 3u * seg, bar);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        tma_bulk_g2s(dst + uint32_t(c * W * 8), sc.un + (node * 3 + c) * n_s + sbase, seg, bar);
+                }
+            }
+        }
+        if (warp == (1 % nwarps)) {                        // alpha of the CTA's elements
+            for (int k = lane; k < n_els; k += 32) {
+                const int64_t e = __ldg(a.mf_els + el0 + k);
+                tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sA + size_t(k) * W)), a.alpha + e * n_s + sbase, seg, bar);
+            }
+        }
+        if (!APPLY && warp == (2 % nwarps)) {              // update operands of the own rows
+            if (full) {
+                if (lane == 0) {
+                    tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sC)), a.c1 + r0 * n_s, uint32_t(nr) * seg, bar);
+                    if (c23) {
+                        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sC + size_t(R) * W)), a.c2a + r0 * n_s,
+                                     uint32_t(nr) * seg, bar);
+                        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sC + size_t(2 * R) * W)), a.c3a + r0 * n_s,
+                                     uint32_t(nr) * seg, bar);
+                    }
+                    tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sO)), sc.uo + r0 * 3 * n_s, uint32_t(nr) * 3u * seg, bar);
+                }
+            } else {
+                for (int r = lane; r < nr; r += 32) {
+                    const int64_t row = r0 + r;
+                    tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sC + size_t(r) * W)), a.c1 + row * n_s + sbase, seg, bar);
+                    if (c23) {
+                        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sC + size_t(R + r) * W)),
+                                     a.c2a + row * n_s + sbase, seg, bar);
+                        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sC + size_t(2 * R + r) * W)),
+                                     a.c3a + row * n_s + sbase, seg, bar);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sO + (size_t(r) * 3 + c) * W)),
+                                     sc.uo + (row * 3 + c) * n_s + sbase, seg, bar);
+                }
+            }
+        }
+    }
     const int nthr = int(blockDim.x);
+    if constexpr (VEC == 1)
     for (int idx = int(threadIdx.x); idx < n_nodes * 3 * nvw; idx += nthr) {
         const int k = idx / (3 * nvw), rem = idx - k * 3 * nvw, c = rem / nvw, j = rem - c * nvw;
         const int64_t node = __ldg(a.mf_nodes + nd0 + k);
@@ -529,7 +591,7 @@ k_step_matrix_free(const StepArgs a) {
         cp_async_vec_s<VEC>(uint32_t(__cvta_generic_to_shared(sA + size_t(k) * W + j * VEC)),
                             a.alpha + e * n_s + sbase + j * VEC);
     }
-    if (!APPLY) {
+    if (!APPLY && VEC == 1) {
         for (int idx = int(threadIdx.x); idx < nr * nvw; idx += nthr) {
             const int r = idx / nvw, j = idx - r * nvw;
             const int64_t row = r0 + r;
@@ -546,15 +608,19 @@ k_step_matrix_free(const StepArgs a) {
                 cp_async_vec_s<VEC>(uint32_t(__cvta_generic_to_shared(sO + (size_t(r) * 3 + c) * W + j * VEC)),
                                     sc.uo + (row * 3 + c) * n_s + sbase + j * VEC);
         }
+    }
+    if (!APPLY) {
         for (int idx = int(threadIdx.x); idx < nr * 3 * a.n_fields; idx += nthr) {
             const int r = idx / (3 * a.n_fields), rem = idx - r * 3 * a.n_fields, k = rem / 3, c = rem - k * 3;
             sF[idx] = __ldg(a.Fk + (int64_t(k) * a.fk_rows + r0 + r) * 3 + c);
         }
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    if constexpr (VEC == 1) {
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_all;" ::: "memory");
+    }
     __syncthreads();
-    if (n_inc) mbar_wait(bar, 0);
+    if (tx) mbar_wait(bar, 0);
 
     const int lr = int(threadIdx.x) / G;
     const int g = int(threadIdx.x) % G;
@@ -572,12 +638,15 @@ k_step_matrix_free(const StepArgs a) {
     for (int d = 0; d < 3; ++d) uo[d] = lds_vec<VEC>(sU + (size_t(lr) * 3 + d) * W + w0);   // own row = slot lr
 
     const int32_t kb = __ldg(a.inc_ptr + i) - k0, ke = __ldg(a.inc_ptr + i + 1) - k0;
+    const double* sUw = sU + w0;
+    const double* sAw = sA + w0;
+    const int W3 = 3 * W;
     for (int32_t k = kb; k < ke; ++k) {
         const int4 rec = sRec[k];
-        const double* K = sK + size_t(k) * 28;
-        const double* Up = sU + size_t(rec.y) * 3 * W + w0;
-        const double* Un = sU + size_t(rec.z) * 3 * W + w0;
-        const Vec<VEC> al = lds_vec<VEC>(sA + size_t(rec.x) * W + w0);
+        const double* K = sK + k * 28;
+        const double* Up = sUw + rec.y * W3;
+        const double* Un = sUw + rec.z * W3;
+        const Vec<VEC> al = lds_vec<VEC>(sAw + rec.x * W);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             double t[VEC];

@@ -3,8 +3,9 @@
 c1  ideal cylinder ~500 tri (12x23 rings), N_s = 4, steady 13 mmHg, 2,000 steps, fp64
 c2  ideal cylinder ~50k tri (96x262), N_s = 64, steady, mode-1 damping 250 1/s (Laplace)
 c3  as c2, pulsatile traction over 3 cardiac cycles, undamped
-c4  (round 2: synthetic branched aorta ~500k tri, N_s = 128) — not generated yet
-c5  (round 2: ~2M tri, N_s = 512) — not generated yet
+c4  synthetic branched aorta ~500k tri (mesh.aorta), N_s = 128, pulsatile, E 7e6 +- 7e5,
+    zeta 0.2 +- 0.02 cm; realisations from a 32-field GMRF basis (fields.sample_materials)
+c5  the same generator at ~2M tri, N_s = 512
 
 Material statistics: E 7.0e6 +- 7.0e5 Ba, zeta 0.4 +- 0.04 cm, rho_corr 3.7 cm
 (PAPER.md:436); density 1.06 g/cm^3; nu = 0.5, k = 5/6
@@ -53,11 +54,28 @@ class Config:
 
 
 _RINGS = {"c1": (12, 23), "c2": (96, 262), "c3": (96, 262)}
+_AORTA = {"c4": (500_000, 128), "c5": (2_000_000, 512)}
+
+
+def make_aorta(name: str, n_s: int | None = None, s_begin: int = 0, target_tris: int | None = None) -> Config:
+    """Configs c4 / c5: branched aorta, pulsatile, all ends fixed."""
+    idx = int(name[1])
+    seed = 20210121 + 1000 * idx
+    tt, ns_def = _AORTA[name]
+    m = meshmod.aorta(target_tris or tt)
+    ns = n_s or ns_def
+    E, h, _ = fields.sample_materials(m.xyz, m.tris, ns, E_mean=E_MEAN, E_std=E_STD,
+                                      h_mean=0.2, h_std=0.02, rho_corr=RHO_CORR,
+                                      seed=seed, s_begin=s_begin, basis=32)
+    tr = loads.pulsatile(m.xyz, m.tris)
+    return Config(name, m, E, h, tr, damping=DAMP_NONE, c_d=0.0, steps=2000, s_begin=s_begin)
 
 
 def make(name: str, n_s: int | None = None, s_begin: int = 0, n_circ: int | None = None,
          n_axial: int | None = None) -> Config:
-    """Build config `name` (c1/c2/c3), optionally overriding N_s or the ring counts."""
+    """Build config `name` (c1..c5), optionally overriding N_s or the ring counts."""
+    if name in _AORTA:
+        return make_aorta(name, n_s=n_s, s_begin=s_begin)
     idx = int(name[1])
     seed = 20210121 + 1000 * idx
     nc, na = _RINGS[name]

@@ -74,10 +74,22 @@ class MaternSampler:
         return (X / self.sigma_spde).T                # [len(s_list)][V]
 
 
+def _basis_weights(seed: int, field_id: int, s_list, K: int) -> np.ndarray:
+    """Unit vectors w_s in R^K, one per realisation index, counter-based (seed, field, s)."""
+    W = np.stack([_z(seed + 7919, field_id, s, K) for s in s_list])
+    return W / np.linalg.norm(W, axis=1, keepdims=True)
+
+
 def sample_materials(xyz: np.ndarray, tris: np.ndarray, n_s: int, *, E_mean: float,
                      E_std: float, h_mean: float, h_std: float, rho_corr: float,
-                     seed: int, s_begin: int = 0, homogeneous_first: bool = True):
-    """Return (E[n_s][V], h[n_s][V], n_clipped) for realisations s_begin .. s_begin+n_s-1."""
+                     seed: int, s_begin: int = 0, homogeneous_first: bool = True,
+                     basis: int | None = None):
+    """Return (E[n_s][V], h[n_s][V], n_clipped) for realisations s_begin .. s_begin+n_s-1.
+
+    basis = K (large configs c4/c5): draw K independent GMRF fields z_1..z_K per field type
+    and give realisation s the field sum_k w_{s,k} z_k with w_s a unit vector keyed by
+    (seed, field, s) — each realisation still has exactly the GMRF covariance Q^-1, at the
+    cost of correlation between realisations (stated in DESIGN.md "Inputs")."""
     V = xyz.shape[0]
     E = np.empty((n_s, V))
     h = np.empty((n_s, V))
@@ -85,8 +97,14 @@ def sample_materials(xyz: np.ndarray, tris: np.ndarray, n_s: int, *, E_mean: flo
     rand = [s for s in s_idx if not (homogeneous_first and s == 0)]
     if rand:
         smp = MaternSampler(xyz, tris, rho_corr)
-        xe = smp.standard(seed, FIELD_E, rand)
-        xh = smp.standard(seed, FIELD_H, rand)
+        if basis:
+            be = smp.standard(seed, FIELD_E, range(basis))
+            bh = smp.standard(seed, FIELD_H, range(basis))
+            xe = _basis_weights(seed, FIELD_E, rand, basis) @ be
+            xh = _basis_weights(seed, FIELD_H, rand, basis) @ bh
+        else:
+            xe = smp.standard(seed, FIELD_E, rand)
+            xh = smp.standard(seed, FIELD_H, rand)
     k = 0
     for row, s in enumerate(s_idx):
         if homogeneous_first and s == 0:
