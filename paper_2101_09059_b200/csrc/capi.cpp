@@ -576,7 +576,9 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
         const int Pg = c->n_s / vec;
         P.mf_groups = std::min(Pg, 32);
         const int64_t W = int64_t(P.mf_groups) * vec;
-        P.mf_rows = std::max(1, std::min(256 / P.mf_groups, 64));
+        const int max_threads = vec == 2 ? 512 : 256;
+        P.mf_rows = std::max(1, std::min(max_threads / P.mf_groups, 64));
+        if (const char* e = std::getenv("ENS_MF_ROWS")) P.mf_rows = std::max(1, std::min(P.mf_rows, std::atoi(e)));
         std::vector<int32_t> nptr, nodes, eptr, els;
         std::vector<ens::FanRec> crec;
         for (;;) {
@@ -625,10 +627,10 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
             P.mf_smem_inc = mx_inc;
             P.mf_nodes_max = mx_nodes;
             P.mf_els_max = mx_els;
+            // one stage of the two-stage shared-memory ring (kernels.cu stage_doubles)
             const int64_t bytes = int64_t(mx_inc) * 240 +
-                                  (int64_t(mx_nodes) * 3 * W + int64_t(mx_els) * W + R * 3 * W + R * 3 * W) * 8 +
-                                  R * 3 * ens::kMaxFields * 8;
-            if (bytes <= 110 * 1024 || P.mf_rows == 1) break;
+                                  (int64_t(mx_nodes) * 3 * W + int64_t(mx_els) * W + R * 3 * W + R * 3 * W) * 8;
+            if (vec == 1 || bytes <= 108 * 1024 || P.mf_rows == 1) break;
             P.mf_rows = std::max(1, P.mf_rows / 2);
         }
         static_assert(sizeof(ens::FanRec) == sizeof(int4), "FanRec layout");
