@@ -849,8 +849,9 @@ static cudaError_t launch_a2_pipe(const StepArgs& a, cudaStream_t st) {
     static int occ = -1;                 // CTAs per SM at this smem size (per instance)
     static size_t occ_smem = 0;
     if (occ < 0 || occ_smem != smem) {
+        // dynamic + static shared memory must stay within the 227 KB per-CTA limit
         cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free_pipe<APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024);
+                                             int(smem));
         if (e != cudaSuccess) return e;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step_matrix_free_pipe<APPLY>,
                                                           a.mf_rows * a.mf_groups, smem);
