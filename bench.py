@@ -174,6 +174,40 @@ def run_reference(args):
     return 0
 
 
+def _node_partition_run(args, cfg, base, m, tr, rank, world, local, stream, barrier, n_s):
+    """Node partition (strong scaling of the full config): every rank holds the same N_s
+    realisations, the RCM rows are split across ranks, NCCL halo of the interface rows."""
+    import torch
+    from paper_2101_09059_b200 import solver
+    comm = solver.nccl_comm_of()
+    npar = solver.Ensemble(m.xyz, m.tris, m.fixed, base.E, base.h, rho=cfg.rho, nu=cfg.nu,
+                           k_shear=cfg.k_shear, damping=cfg.damping, c_d=cfg.c_d,
+                           kernel=args.kernel, dist="node", rank=rank, world=world,
+                           nccl_comm=comm, device=local)
+    npar.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    npar.step(max(3, args.warmup))
+    npar.sync()
+    barrier()
+    n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0.record(stream)
+    npar.step(args.steps)
+    n1.record(stream)
+    n1.synchronize()
+    barrier()
+    npar.sync()
+    t = torch.tensor([n0.elapsed_time(n1) / 1e3], device="cuda", dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ninf = npar.info()
+    node = {"value": n_s * 3 * m.n_nodes * args.steps / float(t.item()), "unit": "DOF-updates/s",
+            "ms_per_step": 1e3 * float(t.item()) / args.steps, "scaling": "strong",
+            "n_s_total": n_s, "rows_rank0": ninf["n_owned"],
+            "halo_bytes_per_step_rank0": ninf["halo_bytes_per_step"],
+            "launches_per_step": ninf["launches_per_step"]}
+    npar.close()
+
+    return node
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -184,7 +218,8 @@ def main(argv=None):
     ap.add_argument("--n-s", type=int, default=None, help="realisations per GPU (default: the config's)")
     ap.add_argument("--kernel", default="assembled", choices=["assembled", "assembled_sym", "matrix_free"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-node", action="store_true", help="skip the node-partitioned run at N > 1")
+    ap.add_argument("--node-partition", action="store_true",
+                    help="at N > 1 also time ENS_DIST_NODE (RCM rows split, NCCL halo; strong scaling)")
     ap.add_argument("--e2e-windows", type=int, default=10)
     ap.add_argument("--obs-every", type=int, default=100)
     args = ap.parse_args(argv)
@@ -276,32 +311,11 @@ def main(argv=None):
     # node partition (strong scaling of the full config): the same N_s realisations on
     # every rank, RCM rows split across ranks, NCCL halo of the interface rows per step
     node = None
-    if world > 1 and not args.no_node:
-        comm = solver.nccl_comm_of()
-        npar = solver.Ensemble(m.xyz, m.tris, m.fixed, base.E, base.h, rho=cfg.rho, nu=cfg.nu,
-                               k_shear=cfg.k_shear, damping=cfg.damping, c_d=cfg.c_d,
-                               kernel=args.kernel, dist="node", rank=rank, world=world,
-                               nccl_comm=comm, device=local)
-        npar.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
-        npar.step(max(3, args.warmup))
-        npar.sync()
-        barrier()
-        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n0.record(stream)
-        npar.step(args.steps)
-        n1.record(stream)
-        n1.synchronize()
-        barrier()
-        npar.sync()
-        t = torch.tensor([n0.elapsed_time(n1) / 1e3], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ninf = npar.info()
-        node = {"value": n_s * 3 * m.n_nodes * args.steps / float(t.item()), "unit": "DOF-updates/s",
-                "ms_per_step": 1e3 * float(t.item()) / args.steps, "scaling": "strong",
-                "n_s_total": n_s, "rows_rank0": ninf["n_owned"],
-                "halo_bytes_per_step_rank0": ninf["halo_bytes_per_step"],
-                "launches_per_step": ninf["launches_per_step"]}
-        npar.close()
+    if world > 1 and args.node_partition:
+        try:
+            node = _node_partition_run(args, cfg, base, m, tr, rank, world, local, stream, barrier, n_s)
+        except Exception as e:          # reported, never fatal for the primary (sharded) line
+            node = {"error": repr(e)[:300]}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:

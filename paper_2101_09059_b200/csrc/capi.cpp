@@ -41,8 +41,7 @@ struct Part {
     int32_t* d_inc_ptr = nullptr;
     int4* d_fan = nullptr;
     double *d_Krow = nullptr, *d_alpha = nullptr;
-    int32_t mf_rows = 1, mf_groups = 1, mf_smem_inc = 0, mf_nodes_max = 0, mf_els_max = 0;
-    int32_t *d_mf_node_ptr = nullptr, *d_mf_nodes = nullptr, *d_mf_el_ptr = nullptr, *d_mf_els = nullptr;
+    int32_t mf_rows = 1, mf_groups = 1, mf_smem_inc = 0;
     int32_t *d_sym_lptr = nullptr, *d_sym_lidx = nullptr, *d_sym_lcol = nullptr, *d_sym_scol = nullptr;
     int2* d_sym_urange = nullptr;
     int64_t n_stored = 0;                                  // value blocks held (assembled kernels)
@@ -241,12 +240,6 @@ ens::StepArgs part_args(const ens_ctx* c, const Part& p) {
     a.mf_rows = p.mf_rows;
     a.mf_groups = p.mf_groups;
     a.mf_smem_inc = p.mf_smem_inc;
-    a.mf_node_ptr = p.d_mf_node_ptr;
-    a.mf_nodes = p.d_mf_nodes;
-    a.mf_el_ptr = p.d_mf_el_ptr;
-    a.mf_els = p.d_mf_els;
-    a.mf_nodes_max = p.mf_nodes_max;
-    a.mf_els_max = p.mf_els_max;
     a.sym_lptr = p.d_sym_lptr;
     a.sym_lidx = p.d_sym_lidx;
     a.sym_lcol = p.d_sym_lcol;
@@ -285,24 +278,6 @@ cudaError_t launch_rows(const ens_ctx* c, ens::StepArgs a, int64_t row0, int64_t
     }
 }
 
-// Boundary launch ranges [0, blo) and [n_own - bhi, n_own): the plan's, widened so that
-// for the matrix-free kernel every launch starts on a CTA boundary (multiple of mf_rows).
-void boundary_ranges(const ens_ctx* c, const Part& p, int64_t* blo, int64_t* bhi) {
-    int64_t lo = p.plan.b_lo, hi = p.plan.b_hi;
-    if (c->kernel == ENS_KERNEL_MATRIX_FREE) {
-        const int64_t R = p.mf_rows;
-        lo = (lo + R - 1) / R * R;
-        const int64_t start_hi = (p.n_own - hi) / R * R;
-        hi = p.n_own - start_hi;
-    }
-    if (lo + hi >= p.n_own) {
-        lo = p.n_own;
-        hi = 0;
-    }
-    *blo = lo;
-    *bhi = hi;
-}
-
 // ---- one time step of every part (step index = ctx step + k) ---------------------------
 int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
     const int64_t step = c->step + k;            // host mirror of *d_step + k
@@ -316,10 +291,8 @@ int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
     for (Part& p : c->parts) {
         ens::StepArgs a = part_args(c, p);
         a.step_off = k;
-        int64_t blo, bhi;
-        boundary_ranges(c, p, &blo, &bhi);
-        CUDA_TRY(c, launch_rows(c, a, 0, blo, st));
-        CUDA_TRY(c, launch_rows(c, a, p.n_own - bhi, bhi, st));
+        CUDA_TRY(c, launch_rows(c, a, 0, p.plan.b_lo, st));
+        CUDA_TRY(c, launch_rows(c, a, p.n_own - p.plan.b_hi, p.plan.b_hi, st));
         CUDA_TRY(c, ens::launch_pack(int64_t(p.plan.send_rows.size()), c->n_s, p.d_send_rows, c->d_step, k, p.d_u0,
                                      p.d_u1, p.d_sendbuf, st));
     }
@@ -360,9 +333,7 @@ int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
     for (Part& p : c->parts) {
         ens::StepArgs a = part_args(c, p);
         a.step_off = k;
-        int64_t blo, bhi;
-        boundary_ranges(c, p, &blo, &bhi);
-        CUDA_TRY(c, launch_rows(c, a, blo, p.n_own - blo - bhi, st));
+        CUDA_TRY(c, launch_rows(c, a, p.plan.b_lo, p.n_own - p.plan.b_lo - p.plan.b_hi, st));
     }
     // (4) the next step's boundary rows read the ghosts: join the exchange
     if (c->nccl_comm) CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
@@ -569,79 +540,26 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
             r.n_prev = local(r.n_prev);
             r.n_next = local(r.n_next);
         }
-        // CTA geometry: G threads per row (a chunk of W = G * VEC realisations), R rows.
-        // Per CTA: its node set (own rows first, then every other node its incidences
-        // reach) and element set; records re-indexed to those slots (DESIGN.md §5 F2).
-        const int vec = ens::pick_vec_mf(c->n_s);
-        const int Pg = c->n_s / vec;
-        P.mf_groups = std::min(Pg, 32);
-        const int64_t W = int64_t(P.mf_groups) * vec;
-        const int max_threads = vec == 2 ? 512 : 256;
-        P.mf_rows = std::max(1, std::min(max_threads / P.mf_groups, 64));
-        if (const char* e = std::getenv("ENS_MF_ROWS")) P.mf_rows = std::max(1, std::min(P.mf_rows, std::atoi(e)));
-        std::vector<int32_t> nptr, nodes, eptr, els;
-        std::vector<ens::FanRec> crec;
+        const int Pg = c->n_s / ens::pick_vec_mf(c->n_s);
+        P.mf_groups = std::min(Pg, 256);
+        P.mf_rows = std::max(1, std::min(256 / P.mf_groups, 32));
         for (;;) {
-            const int64_t R = P.mf_rows, n_cta = (P.n_own + R - 1) / R;
-            nptr.assign(1, 0);
-            eptr.assign(1, 0);
-            nodes.clear();
-            els.clear();
-            crec = rec;
-            int32_t mx_inc = 0, mx_nodes = 0, mx_els = 0;
-            std::vector<int32_t> tmp_n, tmp_e;
-            for (int64_t t = 0; t < n_cta; ++t) {
-                const int64_t a0 = t * R, a1 = std::min(a0 + R, P.n_own);
-                tmp_n.clear();
-                tmp_e.clear();
-                for (int32_t k = ip[size_t(a0)]; k < ip[size_t(a1)]; ++k) {
-                    for (int32_t v : {rec[size_t(k)].n_prev, rec[size_t(k)].n_next})
-                        if (!(v >= a0 && v < a1)) tmp_n.push_back(v);
-                    tmp_e.push_back(rec[size_t(k)].e);
-                }
-                std::sort(tmp_n.begin(), tmp_n.end());
-                tmp_n.erase(std::unique(tmp_n.begin(), tmp_n.end()), tmp_n.end());
-                std::sort(tmp_e.begin(), tmp_e.end());
-                tmp_e.erase(std::unique(tmp_e.begin(), tmp_e.end()), tmp_e.end());
-                auto slot_n = [&](int32_t v) -> int32_t {
-                    if (v >= a0 && v < a1) return int32_t(v - a0);
-                    return int32_t((a1 - a0) + (std::lower_bound(tmp_n.begin(), tmp_n.end(), v) - tmp_n.begin()));
-                };
-                for (int32_t k = ip[size_t(a0)]; k < ip[size_t(a1)]; ++k) {
-                    ens::FanRec& r = crec[size_t(k)];
-                    const ens::FanRec& o = rec[size_t(k)];
-                    r.e = int32_t(std::lower_bound(tmp_e.begin(), tmp_e.end(), o.e) - tmp_e.begin());
-                    r.n_prev = slot_n(o.n_prev);
-                    r.n_next = slot_n(o.n_next);
-                    r.restart = 0;
-                }
-                for (int64_t v = a0; v < a1; ++v) nodes.push_back(int32_t(v));
-                nodes.insert(nodes.end(), tmp_n.begin(), tmp_n.end());
-                els.insert(els.end(), tmp_e.begin(), tmp_e.end());
-                nptr.push_back(int32_t(nodes.size()));
-                eptr.push_back(int32_t(els.size()));
-                mx_inc = std::max(mx_inc, ip[size_t(a1)] - ip[size_t(a0)]);
-                mx_nodes = std::max<int32_t>(mx_nodes, int32_t((a1 - a0) + int64_t(tmp_n.size())));
-                mx_els = std::max<int32_t>(mx_els, int32_t(tmp_e.size()));
+            int32_t mx = 0;
+            for (int64_t r0 = 0; r0 < P.n_own; r0 += P.mf_rows) {
+                const int64_t r1 = std::min<int64_t>(r0 + P.mf_rows, P.n_own);
+                mx = std::max(mx, ip[size_t(r1)] - ip[size_t(r0)]);
             }
-            P.mf_smem_inc = mx_inc;
-            P.mf_nodes_max = mx_nodes;
-            P.mf_els_max = mx_els;
-            // one stage of the two-stage shared-memory ring (kernels.cu stage_doubles)
-            const int64_t bytes = int64_t(mx_inc) * 240 +
-                                  (int64_t(mx_nodes) * 3 * W + int64_t(mx_els) * W + R * 3 * W + R * 3 * W) * 8;
-            if (vec == 1 || bytes <= 108 * 1024 || P.mf_rows == 1) break;
+            P.mf_smem_inc = mx;
+            if (int64_t(mx) * 240 <= 96 * 1024 || P.mf_rows == 1) break;
             P.mf_rows = std::max(1, P.mf_rows / 2);
         }
+        if (int64_t(P.mf_smem_inc) * 240 > 200 * 1024)
+            return fail(c, ENS_E_UNSUPPORTED, "a node has too many incident elements for the matrix-free kernel");
         static_assert(sizeof(ens::FanRec) == sizeof(int4), "FanRec layout");
         RC_TRY(upload(c, &P.d_inc_ptr, ip.data(), ip.size()));
-        RC_TRY(upload(c, &P.d_fan, reinterpret_cast<const int4*>(crec.data()), crec.size()));
+        RC_TRY(upload(c, &P.d_fan, reinterpret_cast<const int4*>(rec.data()), rec.size()));
         RC_TRY(upload(c, &P.d_Krow, fans.Krow.data() + size_t(k0) * 28, size_t(k1 - k0) * 28));
         RC_TRY(upload(c, &P.d_alpha, al.data(), al.size()));
-        RC_TRY(upload(c, &P.d_mf_node_ptr, nptr.data(), nptr.size()));
-        RC_TRY(upload(c, &P.d_mf_nodes, nodes.data(), nodes.size()));
-        RC_TRY(upload(c, &P.d_mf_el_ptr, eptr.data(), eptr.size()));
-        RC_TRY(upload(c, &P.d_mf_els, els.data(), els.size()));
     }
     const size_t ns = size_t(n_loc) * 3 * size_t(n_s);
     RC_TRY(dalloc(c, &P.d_u0, ns));

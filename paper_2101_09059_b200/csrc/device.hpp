@@ -32,14 +32,9 @@ struct StepArgs {
     const int4* fan = nullptr;          // [3F] {e, n_prev, n_next, restart}
     const double* Krow = nullptr;       // [3F][28]
     const double* alpha = nullptr;      // [F][n_s]
-    int32_t mf_rows = 1;                // rows per CTA (launch ranges are multiples of it)
+    int32_t mf_rows = 1;                // rows per CTA
     int32_t mf_groups = 1;              // realisation groups (threads) per row per CTA
     int32_t mf_smem_inc = 0;            // max incidences staged by one CTA
-    const int32_t* mf_node_ptr = nullptr;   // [n_cta + 1] node set of each CTA (own rows first)
-    const int32_t* mf_nodes = nullptr;
-    const int32_t* mf_el_ptr = nullptr;     // [n_cta + 1] elements of each CTA
-    const int32_t* mf_els = nullptr;
-    int32_t mf_nodes_max = 0, mf_els_max = 0;
     // update coefficients
     const double* c1 = nullptr;
     const double* c2a = nullptr;        // null => scalars c2, c3
@@ -74,7 +69,6 @@ cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st);
 // realisations per thread of the step kernels for a given N_s (4, 2 or 1)
 int pick_vec(int32_t n_s);      // assembled kernel
 int pick_vec_mf(int32_t n_s);   // matrix-free kernel
-size_t mf_smem_bytes(const StepArgs& a, int vec);   // dynamic smem of one matrix-free CTA
 // *step_base += n (after n steps were enqueued)
 cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st);
 

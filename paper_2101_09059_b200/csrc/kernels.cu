@@ -11,7 +11,6 @@
 // accumulates its realisations sequentially in CSR block order then d = 0,1,2 with explicit
 // fma(): the per-realisation arithmetic is identical whatever N_s, VEC or the launch
 // geometry, which makes ensemble runs bit-identical to single-realisation runs.
-#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
@@ -439,321 +438,118 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     }
 }
 
-template <int VEC>
-__device__ __forceinline__ void cp_async_vec_s(uint32_t dst, const double* src) {
-    if constexpr (VEC == 1) {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(dst), "l"(src) : "memory");
-    } else if constexpr (VEC == 2) {
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
-    } else {
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst + 16), "l"(src + 2) : "memory");
-    }
-}
-
-template <int VEC>
-__device__ __forceinline__ Vec<VEC> lds_vec(const double* p) {
-    Vec<VEC> r;
-    if constexpr (VEC == 1) {
-        r.v[0] = *p;
-    } else if constexpr (VEC == 2) {
-        const double2 t = *reinterpret_cast<const double2*>(p);
-        r.v[0] = t.x; r.v[1] = t.y;
-    } else {
-        const double2 t0 = *reinterpret_cast<const double2*>(p), t1 = *reinterpret_cast<const double2*>(p + 2);
-        r.v[0] = t0.x; r.v[1] = t0.y; r.v[2] = t1.x; r.v[3] = t1.y;
-    }
-    return r;
-}
-
-// ---- tile geometry shared by the matrix-free kernels ------------------------------------
-// A tile = R consecutive rows (RCM order; launch ranges are R-aligned) x a chunk of
-// W = G * VEC realisations.  Host-side lists give each row block its node set (own rows
-// first, then every node its incidences reach) and element set; incidence records hold
-// slots into those sets.
-struct Tile {
-    int64_t rb;          // global row-block index (= first row / R)
-    int64_t r0;          // first row
-    int nr;              // rows in the tile
-    int32_t k0, n_inc;   // incidences [k0, k0 + n_inc)
-    int32_t nd0, n_nodes, el0, n_els;
-    int sbase, wv;       // realisation chunk
-};
-
-__device__ __forceinline__ Tile tile_of(const StepArgs& a, int64_t t, int64_t n_rb) {
-    Tile T;
-    const int R = a.mf_rows, W = a.mf_groups * 2;
-    const int64_t chunk = t / n_rb;
-    T.rb = a.row0 / R + (t - chunk * n_rb);
-    T.r0 = T.rb * R;
-    const int64_t r_end = a.row0 + a.V;
-    T.nr = int((T.r0 + R < r_end ? T.r0 + R : r_end) - T.r0);
-    T.k0 = __ldg(a.inc_ptr + T.r0);
-    T.n_inc = __ldg(a.inc_ptr + T.r0 + T.nr) - T.k0;
-    T.nd0 = __ldg(a.mf_node_ptr + T.rb);
-    T.n_nodes = __ldg(a.mf_node_ptr + T.rb + 1) - T.nd0;
-    T.el0 = __ldg(a.mf_el_ptr + T.rb);
-    T.n_els = __ldg(a.mf_el_ptr + T.rb + 1) - T.el0;
-    T.sbase = int(chunk) * W;
-    T.wv = min(W, a.n_s - T.sbase);
-    return T;
-}
-
-// One stage of the shared-memory ring (sizes from the per-launch maxima).
-struct Stage {
-    double* K;
-    int4* rec;
-    double* U;      // [nodes][3][W]
-    double* A;      // [els][W]
-    double* C;      // c1 [, c2, c3] of own rows: [1 or 3][R][W]
-    double* O;      // u_{n-1} of own rows: [R][3][W]
-};
-
-__host__ __device__ __forceinline__ size_t stage_doubles(const StepArgs& a, bool c23) {
-    const size_t W = size_t(a.mf_groups) * 2, R = size_t(a.mf_rows);
-    return size_t(a.mf_smem_inc) * 30 + size_t(a.mf_nodes_max) * 3 * W + size_t(a.mf_els_max) * W +
-           R * (c23 ? 3 : 1) * W + R * 3 * W;        // K 28 + rec 2 doubles per incidence
-}
-
-__device__ __forceinline__ Stage stage_at(const StepArgs& a, double* base, bool c23) {
-    const int W = a.mf_groups * 2, R = a.mf_rows;
-    Stage S;
-    S.K = base;
-    S.rec = reinterpret_cast<int4*>(S.K + size_t(a.mf_smem_inc) * 28);
-    S.U = reinterpret_cast<double*>(S.rec + a.mf_smem_inc);
-    S.A = S.U + size_t(a.mf_nodes_max) * 3 * W;
-    S.C = S.A + size_t(a.mf_els_max) * W;
-    S.O = S.C + size_t(R) * (c23 ? 3 : 1) * W;
-    return S;
-}
-
-// Warp 0 stages tile T into S: lane 0 posts the byte count on the stage's mbarrier, then
-// the lanes issue 1-D TMA bulk copies (every segment is a multiple of 16 B: N_s even).
-template <bool APPLY>
-__device__ __forceinline__ void stage_tile(const StepArgs& a, const StepCtx& sc, const Tile& T, const Stage& S,
-                                           uint32_t bar, bool c23) {
-    const int lane = int(threadIdx.x) & 31;
-    const int W = a.mf_groups * 2, R = a.mf_rows, n_s = a.n_s;
-    const bool full = T.wv == n_s;
-    const uint32_t seg = uint32_t(T.wv) * 8u;
-    if (lane == 0) {
-        uint32_t tx = uint32_t(T.n_inc) * 240u + uint32_t(T.n_nodes * 3 + T.n_els) * seg;
-        if (!APPLY) tx += uint32_t(T.nr) * seg * ((c23 ? 3u : 1u) + 3u);
-        mbar_expect_tx(bar, tx);
-        if (T.n_inc) {
-            tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(S.K)), a.Krow + size_t(T.k0) * 28, uint32_t(T.n_inc) * 224u, bar);
-            tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(S.rec)), a.fan + T.k0, uint32_t(T.n_inc) * 16u, bar);
-        }
-        if (!APPLY && full) {
-            const int64_t r0 = T.r0;
-            tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(S.C)), a.c1 + r0 * n_s, uint32_t(T.nr) * seg, bar);
-            if (c23) {
-                tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(S.C + size_t(R) * W)), a.c2a + r0 * n_s, uint32_t(T.nr) * seg, bar);
-                tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(S.C + size_t(2 * R) * W)), a.c3a + r0 * n_s, uint32_t(T.nr) * seg, bar);
-            }
-            tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(S.O)), sc.uo + r0 * 3 * n_s, uint32_t(T.nr) * 3u * seg, bar);
-        }
-    }
-    __syncwarp();
-    for (int k = lane; k < T.n_nodes; k += 32) {
-        const int64_t node = __ldg(a.mf_nodes + T.nd0 + k);
-        const uint32_t dst = uint32_t(__cvta_generic_to_shared(S.U + size_t(k) * 3 * W));
-        if (full) {
-            tma_bulk_g2s(dst, sc.un + node * 3 * n_s, 3u * seg, bar);
-        } else {
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                tma_bulk_g2s(dst + uint32_t(c * W * 8), sc.un + (node * 3 + c) * n_s + T.sbase, seg, bar);
-        }
-    }
-    for (int k = lane; k < T.n_els; k += 32) {
-        const int64_t e = __ldg(a.mf_els + T.el0 + k);
-        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(S.A + size_t(k) * W)), a.alpha + e * n_s + T.sbase, seg, bar);
-    }
-    if (!APPLY && !full) {
-        for (int r = lane; r < T.nr; r += 32) {
-            const int64_t row = T.r0 + r;
-            tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(S.C + size_t(r) * W)), a.c1 + row * n_s + T.sbase, seg, bar);
-            if (c23) {
-                tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(S.C + size_t(R + r) * W)), a.c2a + row * n_s + T.sbase, seg, bar);
-                tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(S.C + size_t(2 * R + r) * W)), a.c3a + row * n_s + T.sbase, seg, bar);
-            }
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(S.O + (size_t(r) * 3 + c) * W)),
-                             sc.uo + (row * 3 + c) * n_s + T.sbase, seg, bar);
-        }
-    }
-}
-
-constexpr int kMfThreads = 512;
-
-// F2 (even N_s): persistent CTAs walk the tiles with a two-stage shared-memory ring.  While
-// tile i is computed from stage i & 1, warp 0 has already issued the TMA copies of tile
-// i + 1 into the other stage; one __syncthreads per tile frees a stage for reuse.  The
-// gather and the update read only shared memory (plus F_k and the Dirichlet byte).
-template <bool APPLY>
-__global__ void __launch_bounds__(kMfThreads)
-k_step_matrix_free_pipe(const StepArgs a) {
-    constexpr int VEC = 2;
+template <int VEC, bool APPLY, int BATCH, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+k_step_matrix_free(const StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ double s_coef[kMaxFields];
-    __shared__ __align__(8) uint64_t s_full[2];
+    __shared__ __align__(8) uint64_t s_bar;
 
     const StepCtx sc = step_ctx(a);
-    const bool c23 = a.c2a != nullptr;
-    const int G = a.mf_groups, W = G * VEC, R = a.mf_rows, n_s = a.n_s;
-    const int64_t n_rb = (a.V + R - 1) / R;
-    const int64_t n_chunks = (n_s + W - 1) / W;
-    const int64_t n_tiles = n_rb * n_chunks;
-    const size_t sd = stage_doubles(a, c23);
-    double* base = reinterpret_cast<double*>(smem);
-    const uint32_t bar0 = uint32_t(__cvta_generic_to_shared(&s_full[0]));   // bar1 = bar0 + 8
+    const int G = a.mf_groups, R = a.mf_rows;
+    const int64_t r0 = a.row0 + int64_t(blockIdx.x) * R;
+    const int64_t r1 = min(r0 + R, a.row0 + a.V);
+    const int32_t k0 = __ldg(a.inc_ptr + r0), k1 = __ldg(a.inc_ptr + r1);
+    const uint32_t n_inc = uint32_t(k1 - k0);
+    double* sK = reinterpret_cast<double*>(smem);
+    const int4* sRec = reinterpret_cast<const int4*>(smem + size_t(a.mf_smem_inc) * 224);
+    const uint32_t bar = uint32_t(__cvta_generic_to_shared(&s_bar));
     if (threadIdx.x == 0) {
-        mbar_init(bar0, 1);
-        mbar_init(bar0 + 8, 1);
+        mbar_init(bar, 1);
+        if (n_inc) {
+            mbar_expect_tx(bar, n_inc * 240u);
+            tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sK)), a.Krow + size_t(k0) * 28, n_inc * 224u, bar);
+            tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sRec)), a.fan + k0, n_inc * 16u, bar);
+        }
         if (!APPLY) load_coeffs(a, double(sc.step) * a.dt, s_coef);
     }
     __syncthreads();
-    int64_t t = blockIdx.x;
-    if (t < n_tiles && threadIdx.x < 32) stage_tile<APPLY>(a, sc, tile_of(a, t, n_rb), stage_at(a, base, c23), bar0, c23);
 
-    const int lr = int(threadIdx.x) / G, g = int(threadIdx.x) % G, w0 = g * VEC;
-    for (int it = 0; t < n_tiles; ++it, t += gridDim.x) {
-        const int st = it & 1;
-        const int64_t tn = t + gridDim.x;
-        if (tn < n_tiles && threadIdx.x < 32)
-            stage_tile<APPLY>(a, sc, tile_of(a, tn, n_rb), stage_at(a, base + (st ^ 1) * sd, c23), bar0 + 8u * uint32_t(st ^ 1), c23);
-        const Tile T = tile_of(a, t, n_rb);
-        mbar_wait(bar0 + 8u * uint32_t(st), uint32_t(it >> 1) & 1u);
-        const Stage X = stage_at(a, base + st * sd, c23);
-        if (lr < T.nr && w0 < T.wv) {
-            const int64_t i = T.r0 + lr;
-            double y[3][VEC];
+    const int P = a.n_s / VEC;
+    const int lr = int(threadIdx.x) / G;
+    const int g = int(blockIdx.y) * G + int(threadIdx.x) % G;
+    const int64_t i = r0 + lr;
+    const bool valid = lr < R && i < r1 && g < P;
+    const int n_s = a.n_s;
+    const int s0 = g * VEC;
+    const double* un_base = sc.un + s0;
+
+    double y[3][VEC];
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
+    for (int c = 0; c < 3; ++c)
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) y[c][v] = 0.0;
-            const double* Uw = X.U + w0;
-            const double* Aw = X.A + w0;
-            const int W3 = 3 * W;
-            Vec<VEC> uo[3];
+        for (int v = 0; v < VEC; ++v) y[c][v] = 0.0;
+    Vec<VEC> uo[3], up[3];
+    if (valid) {
 #pragma unroll
-            for (int d = 0; d < 3; ++d) uo[d] = lds_vec<VEC>(Uw + lr * W3 + d * W);     // own row = slot lr
-            const int32_t kb = __ldg(a.inc_ptr + i) - T.k0, ke = __ldg(a.inc_ptr + i + 1) - T.k0;
-            for (int32_t k = kb; k < ke; ++k) {
-                const int4 rec = X.rec[k];
-                const double* K = X.K + k * 28;
-                const double* Up = Uw + rec.y * W3;
-                const double* Un = Uw + rec.z * W3;
-                const Vec<VEC> al = lds_vec<VEC>(Aw + rec.x * W);
-                double tt[3][VEC];
+        for (int d = 0; d < 3; ++d) uo[d] = ld_ro<VEC>(un_base + (i * 3 + d) * n_s);
+    }
+    double* slot = reinterpret_cast<double*>(smem + size_t(a.mf_smem_inc) * 240) + size_t(threadIdx.x) * 6 * VEC;
+    if (!APPLY && valid) upd_load_async<VEC>(a, sc, i, s0, slot);
+    if (n_inc) mbar_wait(bar, 0);
+    if (!valid) return;
+
+    // 32-bit element offsets (V * 3 * N_s and F * N_s stay below 2^31 up to config c5)
+    const int W3 = 3 * n_s;
+    const double* al_base = a.alpha + s0;
+    const int32_t kb = __ldg(a.inc_ptr + i) - k0, ke = __ldg(a.inc_ptr + i + 1) - k0;
+    if (kb < ke) {                               // the row's first chain starts at kb
+        const int4 r = sRec[kb];
 #pragma unroll
-                for (int c = 0; c < 3; ++c)
+        for (int d = 0; d < 3; ++d) up[d] = ld_ro<VEC>(un_base + (r.y * W3 + d * n_s));
+    }
+    for (int32_t k = kb; k < ke; k += BATCH) {
+        // gather phase: every load of the batch in flight before any arithmetic
+        int4 rec[BATCH];
+        Vec<VEC> un[BATCH][3], al[BATCH];
 #pragma unroll
-                    for (int v = 0; v < VEC; ++v) tt[c][v] = 0.0;
+        for (int j = 0; j < BATCH; ++j) {
+            if (k + j < ke) {
+                rec[j] = sRec[k + j];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) un[j][d] = ld_ro<VEC>(un_base + (rec[j].z * W3 + d * n_s));
+                al[j] = ld_ro<VEC>(al_base + rec[j].x * n_s);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < BATCH; ++j) {
+            if (k + j >= ke) break;
+            if (rec[j].w && k + j != kb) {       // a further chain (non-manifold vertex): rare
+#pragma unroll
+                for (int d = 0; d < 3; ++d) up[d] = ld_ro<VEC>(un_base + (rec[j].y * W3 + d * n_s));
+            }
+            const double* K = sK + (k + j) * 28;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double t[VEC];
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) t[v] = 0.0;
 #pragma unroll
                 for (int d = 0; d < 3; ++d) {
-                    const Vec<VEC> up = lds_vec<VEC>(Up + d * W), un = lds_vec<VEC>(Un + d * W);
+                    const double k_own = K[9 * c + d], k_prev = K[9 * c + 3 + d], k_next = K[9 * c + 6 + d];
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const double k_own = K[9 * c + d], k_prev = K[9 * c + 3 + d], k_next = K[9 * c + 6 + d];
-#pragma unroll
-                        for (int v = 0; v < VEC; ++v) {
-                            tt[c][v] = fma(k_own, uo[d].v[v], tt[c][v]);
-                            tt[c][v] = fma(k_prev, up.v[v], tt[c][v]);
-                            tt[c][v] = fma(k_next, un.v[v], tt[c][v]);
-                        }
+                    for (int v = 0; v < VEC; ++v) {
+                        t[v] = fma(k_own, uo[d].v[v], t[v]);
+                        t[v] = fma(k_prev, up[d].v[v], t[v]);
+                        t[v] = fma(k_next, un[j][d].v[v], t[v]);
                     }
                 }
 #pragma unroll
-                for (int c = 0; c < 3; ++c)
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) y[c][v] = fma(al.v[v], tt[c][v], y[c][v]);
+                for (int v = 0; v < VEC; ++v) y[c][v] = fma(al[j].v[v], t[v], y[c][v]);
             }
-            const int s0 = T.sbase + w0;
-            if constexpr (APPLY) {
-                store_y<VEC>(a, i, s0, y);
-            } else {
-                Upd<VEC> u;
-                u.fx = a.fixed ? __ldg(a.fixed + i) : uint8_t(0);
-                u.c1 = lds_vec<VEC>(X.C + lr * W + w0);
-                if (c23) {
-                    u.c2 = lds_vec<VEC>(X.C + (R + lr) * W + w0);
-                    u.c3 = lds_vec<VEC>(X.C + (2 * R + lr) * W + w0);
-                } else {
 #pragma unroll
-                    for (int v = 0; v < VEC; ++v) { u.c2.v[v] = a.c2; u.c3.v[v] = a.c3; }
-                }
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    u.un[c] = uo[c];
-                    u.uo[c] = lds_vec<VEC>(X.O + lr * W3 + c * W + w0);
-                    double f = 0.0;
-                    for (int k = 0; k < a.n_fields; ++k) f = fma(s_coef[k], __ldg(a.Fk + (int64_t(k) * a.fk_rows + i) * 3 + c), f);
-                    u.f[c] = f;
-                }
-                upd_store<VEC>(a, sc, i, s0, y, u);
-            }
+            for (int d = 0; d < 3; ++d) up[d] = un[j][d];
         }
-        __syncthreads();                    // stage st is free for tile it + 2
-    }
-}
-
-// F2 (odd N_s): direct gather from global memory, one thread per (row, realisation).
-template <bool APPLY>
-__global__ void __launch_bounds__(kThreads)
-k_step_matrix_free_direct(const StepArgs a) {
-    __shared__ double s_coef[kMaxFields];
-    const StepCtx sc = step_ctx(a);
-    if (!APPLY && threadIdx.x == 0) load_coeffs(a, double(sc.step) * a.dt, s_coef);
-    if (!APPLY) __syncthreads();
-    const int n_s = a.n_s;
-    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= a.V * n_s) return;
-    const int64_t i = a.row0 + tid / n_s;
-    const int s = int(tid % n_s);
-    const int R = a.mf_rows;
-    const int64_t rb = i / R;                            // records hold slots of the row block
-    const int32_t nd0 = __ldg(a.mf_node_ptr + rb), el0 = __ldg(a.mf_el_ptr + rb);
-    double y[3][1] = {{0.0}, {0.0}, {0.0}};
-    double uo[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) uo[d] = __ldg(sc.un + (i * 3 + d) * n_s + s);
-    for (int32_t k = __ldg(a.inc_ptr + i); k < __ldg(a.inc_ptr + i + 1); ++k) {
-        const int4 rec = a.fan[k];
-        const int64_t np = __ldg(a.mf_nodes + nd0 + rec.y), nn = __ldg(a.mf_nodes + nd0 + rec.z);
-        const int64_t e = __ldg(a.mf_els + el0 + rec.x);
-        const double* K = a.Krow + int64_t(k) * 28;
-        const double al = __ldg(a.alpha + e * n_s + s);
-        double tt[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            const double up = __ldg(sc.un + (np * 3 + d) * n_s + s), un = __ldg(sc.un + (nn * 3 + d) * n_s + s);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                tt[c] = fma(__ldg(K + 9 * c + d), uo[d], tt[c]);
-                tt[c] = fma(__ldg(K + 9 * c + 3 + d), up, tt[c]);
-                tt[c] = fma(__ldg(K + 9 * c + 6 + d), un, tt[c]);
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) y[c][0] = fma(al, tt[c], y[c][0]);
     }
     if constexpr (APPLY) {
-        store_y<1>(a, i, s, y);
+        store_y<VEC>(a, i, s0, y);
     } else {
-        Upd<1> u;
-        upd_load<1>(a, sc, s_coef, i, s, u, false);
+        Upd<VEC> upd;
+        upd_collect<VEC>(a, s_coef, i, slot, upd);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) u.un[c].v[0] = uo[c];
-        upd_store<1>(a, sc, i, s, y, u);
+        for (int d = 0; d < 3; ++d) upd.un[d] = uo[d];
+        upd_store<VEC>(a, sc, i, s0, y, upd);
     }
-}
-
-size_t mf_smem_bytes_impl(const StepArgs& a, int vec) {
-    if (vec == 1) return 0;
-    return 2 * stage_doubles(a, a.c2a != nullptr) * sizeof(double);
 }
 
 __global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
@@ -842,41 +638,20 @@ static cudaError_t launch_a1(const StepArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <bool APPLY>
-static cudaError_t launch_a2_pipe(const StepArgs& a, cudaStream_t st) {
+template <int VEC, bool APPLY, int BATCH, int MINB>
+static cudaError_t launch_a2(const StepArgs& a, cudaStream_t st) {
     if (a.V == 0) return cudaSuccess;
-    const size_t smem = mf_smem_bytes_impl(a, 2);
-    static int occ = -1;                 // CTAs per SM at this smem size (per instance)
-    static size_t occ_smem = 0;
-    if (occ < 0 || occ_smem != smem) {
-        // dynamic + static shared memory must stay within the 227 KB per-CTA limit
-        cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free_pipe<APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(smem));
+    const int P = a.n_s / VEC;
+    const size_t smem = size_t(a.mf_smem_inc) * 240 + size_t(a.mf_rows * a.mf_groups) * 6 * VEC * sizeof(double);
+    static bool attr_set = false;      // per template instance
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free<VEC, APPLY, BATCH, MINB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_step_matrix_free_pipe<APPLY>,
-                                                          a.mf_rows * a.mf_groups, smem);
-        if (e != cudaSuccess) return e;
-        occ = occ < 1 ? 1 : occ;
-        occ_smem = smem;
+        attr_set = true;
     }
-    static int n_sm = 0;
-    if (!n_sm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int P = a.n_s / 2;
-    const int64_t n_tiles = ((a.V + a.mf_rows - 1) / a.mf_rows) * ((P + a.mf_groups - 1) / a.mf_groups);
-    const int64_t grid = std::min<int64_t>(n_tiles, int64_t(n_sm) * occ);
-    k_step_matrix_free_pipe<APPLY><<<unsigned(grid), unsigned(a.mf_rows * a.mf_groups), smem, st>>>(a);
-    return cudaGetLastError();
-}
-
-template <bool APPLY>
-static cudaError_t launch_a2_direct(const StepArgs& a, cudaStream_t st) {
-    const int64_t n = a.V * a.n_s;
-    if (n == 0) return cudaSuccess;
-    k_step_matrix_free_direct<APPLY><<<grid_for(n), kThreads, 0, st>>>(a);
+    dim3 grid(unsigned((a.V + a.mf_rows - 1) / a.mf_rows), unsigned((P + a.mf_groups - 1) / a.mf_groups));
+    k_step_matrix_free<VEC, APPLY, BATCH, MINB><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -917,14 +692,33 @@ cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st) {
     }
 }
 
-int pick_vec_mf(int32_t n_s) { return n_s % 2 ? 1 : 2; }
+// Matrix-free variants (tuning knob ENS_MF_VARIANT = 0..3):
+//   0: VEC 2, batch 1, >= 2 CTAs/SM   1: VEC 2, batch 2, >= 2 CTAs/SM
+//   2: VEC 1, batch 2, >= 3 CTAs/SM   3: VEC 1, batch 1, >= 4 CTAs/SM
+int mf_variant() {
+    static int v = [] {
+        const char* e = std::getenv("ENS_MF_VARIANT");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
 
-size_t mf_smem_bytes(const StepArgs& a, int vec) { return mf_smem_bytes_impl(a, vec); }
+int pick_vec_mf(int32_t n_s) {
+    const int v = mf_variant();
+    if (v >= 2 || n_s % 2) return 1;
+    return 2;
+}
 
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
     const bool ap = a.y_out != nullptr;
-    if (pick_vec_mf(a.n_s) == 2) return ap ? launch_a2_pipe<true>(a, st) : launch_a2_pipe<false>(a, st);
-    return ap ? launch_a2_direct<true>(a, st) : launch_a2_direct<false>(a, st);
+    const int vec = pick_vec_mf(a.n_s);
+    const int var = mf_variant();
+    if (vec == 2) {
+        if (var == 1) return ap ? launch_a2<2, true, 2, 2>(a, st) : launch_a2<2, false, 2, 2>(a, st);
+        return ap ? launch_a2<2, true, 1, 2>(a, st) : launch_a2<2, false, 1, 2>(a, st);
+    }
+    if (var == 3) return ap ? launch_a2<1, true, 1, 4>(a, st) : launch_a2<1, false, 1, 4>(a, st);
+    return ap ? launch_a2<1, true, 2, 3>(a, st) : launch_a2<1, false, 2, 3>(a, st);
 }
 
 cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st) {
