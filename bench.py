@@ -208,6 +208,39 @@ def _node_partition_run(args, cfg, base, m, tr, rank, world, local, stream, barr
     return node
 
 
+def _time_kernel(kernel, args, cfg, m, tr, world, rank, local, stream, barrier, peak):
+    """Time `kernel` on the same workload exactly like the headline (CUDA events around
+    ens_step(K) on the context stream, max over ranks)."""
+    import torch
+    from paper_2101_09059_b200 import solver
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=cfg.rho, nu=cfg.nu,
+                          k_shear=cfg.k_shear, damping=cfg.damping, c_d=cfg.c_d, kernel=kernel,
+                          dist="ensemble" if world > 1 else "single", s_begin=cfg.s_begin,
+                          rank=rank, world=world, device=local)
+    ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    info = ens.info()
+    ens.step(max(3, args.warmup))
+    ens.sync()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ens.step(args.steps)
+    e1.record(stream)
+    e1.synchronize()
+    barrier()
+    ens.sync()
+    el = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        t = torch.tensor([el], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        el = float(t.item())
+    ens.close()
+    ach = info["bytes_per_step"] / (el / args.steps) / 1e9
+    return {"value": world * cfg.n_s * 3 * m.n_nodes * args.steps / el, "unit": "DOF-updates/s",
+            "ms_per_step": 1e3 * el / args.steps, "achieved_GBs": ach, "frac": ach / peak,
+            "algorithmic_bytes_per_launch": info["bytes_per_step"]}
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -218,6 +251,7 @@ def main(argv=None):
     ap.add_argument("--n-s", type=int, default=None, help="realisations per GPU (default: the config's)")
     ap.add_argument("--kernel", default="assembled", choices=["assembled", "assembled_sym", "matrix_free"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-alternatives", action="store_true", help="do not time the other kernels")
     ap.add_argument("--node-partition", action="store_true",
                     help="at N > 1 also time ENS_DIST_NODE (RCM rows split, NCCL halo; strong scaling)")
     ap.add_argument("--e2e-windows", type=int, default=10)
@@ -317,6 +351,18 @@ def main(argv=None):
         except Exception as e:          # reported, never fatal for the primary (sharded) line
             node = {"error": repr(e)[:300]}
 
+    # the other kernels of the same step, same inputs, same launch protocol (reported
+    # alongside; the headline is --kernel)
+    alts = {}
+    if not args.no_alternatives:
+        for k in ("assembled", "assembled_sym", "matrix_free"):
+            if k == args.kernel:
+                continue
+            try:
+                alts[k] = _time_kernel(k, args, cfg, m, tr, world, rank, local, stream, barrier, peak)
+            except Exception as e:
+                alts[k] = {"error": repr(e)[:200]}
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = _cpu_baseline(base)
@@ -337,6 +383,7 @@ def main(argv=None):
                                     "matrix_free": "k_step_matrix_free"}[args.kernel],
                          "algorithmic_bytes_per_launch": info["bytes_per_step"]},
             "cpu_baseline": cpu,
+            "alternatives": alts,
             "node_partition": node,
             "e2e": {"value": e2e_value, "unit": "DOF-updates/s", "h2d_bytes_per_step": h2d / win,
                     "d2h_bytes_per_step": d2h / win,
