@@ -438,7 +438,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     }
 }
 
-template <int VEC, bool APPLY, int BATCH, int MINB>
+template <int VEC, bool APPLY, int BATCH, int MINB, int NS>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_step_matrix_free(const StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -470,7 +470,7 @@ k_step_matrix_free(const StepArgs a) {
     const int g = int(blockIdx.y) * G + int(threadIdx.x) % G;
     const int64_t i = r0 + lr;
     const bool valid = lr < R && i < r1 && g < P;
-    const int n_s = a.n_s;
+    const int n_s = NS ? NS : a.n_s;      // compile-time for the common N_s: immediate offsets
     const int s0 = g * VEC;
     const double* un_base = sc.un + s0;
 
@@ -638,21 +638,30 @@ static cudaError_t launch_a1(const StepArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int VEC, bool APPLY, int BATCH, int MINB>
-static cudaError_t launch_a2(const StepArgs& a, cudaStream_t st) {
+template <int VEC, bool APPLY, int BATCH, int MINB, int NS>
+static cudaError_t launch_a2_ns(const StepArgs& a, cudaStream_t st) {
     if (a.V == 0) return cudaSuccess;
     const int P = a.n_s / VEC;
     const size_t smem = size_t(a.mf_smem_inc) * 240 + size_t(a.mf_rows * a.mf_groups) * 6 * VEC * sizeof(double);
     static bool attr_set = false;      // per template instance
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free<VEC, APPLY, BATCH, MINB>,
+        cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     dim3 grid(unsigned((a.V + a.mf_rows - 1) / a.mf_rows), unsigned((P + a.mf_groups - 1) / a.mf_groups));
-    k_step_matrix_free<VEC, APPLY, BATCH, MINB><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(a);
+    k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(a);
     return cudaGetLastError();
+}
+
+template <int VEC, bool APPLY, int BATCH, int MINB>
+static cudaError_t launch_a2(const StepArgs& a, cudaStream_t st) {
+    if constexpr (VEC == 2) {
+        if (a.n_s == 64) return launch_a2_ns<VEC, APPLY, BATCH, MINB, 64>(a, st);
+        if (a.n_s == 128) return launch_a2_ns<VEC, APPLY, BATCH, MINB, 128>(a, st);
+    }
+    return launch_a2_ns<VEC, APPLY, BATCH, MINB, 0>(a, st);
 }
 
 int pick_vec(int32_t n_s) {

@@ -54,7 +54,7 @@ def report(path):
                 return v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1.0)
             t = float(r[hdr.index("gpu__time_duration.sum")].replace(",", ""))
             tu = units[hdr.index("gpu__time_duration.sum")]
-            t_us = t * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(tu, 1.0)
+            t_us = t * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(tu, 1.0)
             tot = mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum")
             out.append(f"  => dram traffic {tot:.1f} MB per launch, {tot / t_us:.3f} TB/s over the launch")
     return "\n".join(out)
