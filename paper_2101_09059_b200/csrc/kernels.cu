@@ -73,6 +73,22 @@ __device__ __forceinline__ Vec<VEC> ld_once_l1(const double* p) {
     return r;
 }
 
+// Same as ld_once_l1 with an explicit L2 policy (createpolicy): used by the symmetric kernel
+// to keep a stored block in L2 until its transposed second use, then drop it.
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ld_pol_l1(const double* p, uint64_t pol) {
+    Vec<VEC> r;
+    if constexpr (VEC == 1) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r.v[0]) : "l"(p), "l"(pol));
+    } else if constexpr (VEC == 2) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                     : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p), "l"(pol));
+    } else {
+        r = ld_once_l1<VEC>(p);
+    }
+    return r;
+}
+
 // u_n and the coefficient arrays: read-only within a launch, re-used across rows via L1/L2.
 template <int VEC>
 __device__ __forceinline__ Vec<VEC> ld_ro(const double* p) {
@@ -341,7 +357,7 @@ k_step_assembled(const StepArgs a) {
 // bandwidth, so still in L2).  Lower references (j ascending) then the row's own upper
 // blocks (j ascending) visit the columns in exactly the order of the full CSR row, and
 // K^_e is exactly symmetric, so the result is bit-identical to F1 with ~half the bytes.
-template <int VEC, bool APPLY, bool PREF>
+template <int VEC, bool APPLY, bool PREF, int HINT>
 __global__ void __launch_bounds__(kThreads)
 k_step_assembled_sym(const StepArgs a) {
     __shared__ double s_coef[kMaxFields];
@@ -356,6 +372,12 @@ k_step_assembled_sym(const StepArgs a) {
     const int s0 = int(tid % P) * VEC;
     const int n_s = a.n_s;
 
+    // HINT 1: first (own-row) read evict_last, second (transposed) read evict_first;
+    // HINT 2: first read normal, second read evict_first; HINT 0: no policy
+    uint64_t pol_keep = 0, pol_drop = 0;
+    if constexpr (HINT == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    if constexpr (HINT == 2) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
+    if constexpr (HINT != 0) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_drop));
     Upd<VEC> upd;
     if constexpr (!APPLY && PREF) upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
 
@@ -376,7 +398,7 @@ k_step_assembled_sym(const StepArgs a) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) u[d] = ld_ro<VEC>(up + d * n_s);
 #pragma unroll
-        for (int e = 0; e < 9; ++e) kk[e] = ld_once_l1<VEC>(kp + e * n_s);
+        for (int e = 0; e < 9; ++e) kk[e] = HINT ? ld_pol_l1<VEC>(kp + e * n_s, pol_drop) : ld_once_l1<VEC>(kp + e * n_s);
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -394,7 +416,7 @@ k_step_assembled_sym(const StepArgs a) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) u[d] = ld_ro<VEC>(up + d * n_s);
 #pragma unroll
-        for (int e = 0; e < 9; ++e) kk[e] = ld_once_l1<VEC>(kp + e * n_s);
+        for (int e = 0; e < 9; ++e) kk[e] = HINT ? ld_pol_l1<VEC>(kp + e * n_s, pol_keep) : ld_once_l1<VEC>(kp + e * n_s);
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -678,8 +700,14 @@ template <int VEC, bool APPLY>
 static cudaError_t launch_a1s(const StepArgs& a, cudaStream_t st) {
     const int64_t n = a.V * (a.n_s / VEC);
     if (n == 0) return cudaSuccess;
-    if (a1_prefetch()) k_step_assembled_sym<VEC, APPLY, true><<<grid_for(n), kThreads, 0, st>>>(a);
-    else k_step_assembled_sym<VEC, APPLY, false><<<grid_for(n), kThreads, 0, st>>>(a);
+    static int hint = [] {
+        const char* e = std::getenv("ENS_A1S_HINTS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (hint == 1) k_step_assembled_sym<VEC, APPLY, false, 1><<<grid_for(n), kThreads, 0, st>>>(a);
+    else if (hint == 2) k_step_assembled_sym<VEC, APPLY, false, 2><<<grid_for(n), kThreads, 0, st>>>(a);
+    else if (a1_prefetch()) k_step_assembled_sym<VEC, APPLY, true, 0><<<grid_for(n), kThreads, 0, st>>>(a);
+    else k_step_assembled_sym<VEC, APPLY, false, 0><<<grid_for(n), kThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -295,3 +295,68 @@ def test_symmetric_storage_bitexact_vs_full():
     (a, ia), (b, ib) = out
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert ib["bytes_per_step"] < 0.7 * ia["bytes_per_step"]
+
+
+def test_c3_pulsatile_three_cycles_stable():
+    """Config c3: pulsatile traction over 3 cardiac cycles (0.8 s each), undamped, at the
+    CFL step — no divergence, displacement follows the load, and a sampled
+    realisation matches the oracle after the first 2,000 steps (ramp still active)."""
+    cfg = configs.make("c3", n_s=8)
+    m = cfg.mesh
+    tr = cfg.traction
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS)
+    dt = ens.info()["dt"]
+    ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    ens.step(2000)
+    u, _, _, _ = ens.get_state(want_prev=False)
+    om = oracle.OracleModel(m.xyz, m.tris, m.fixed, cfg.E[3:4], cfg.h[3:4], rho=RHO, nu=NU, k_shear=KS, dt=dt)
+    om.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    om.run(2000)
+    assert np.linalg.norm(u[3] - om.u_n[0]) <= 1e-9 * np.linalg.norm(om.u_n[0])
+    n_total = int(round(3 * 0.8 / dt))
+    ring = 131
+    nodes = np.arange(ring * 96, (ring + 1) * 96)
+    rhat = m.xyz[nodes, :2] / np.linalg.norm(m.xyz[nodes, :2], axis=1, keepdims=True)
+    rad = []
+    done = 2000
+    while done < n_total:
+        k = min(2000, n_total - done)
+        ens.step(k)
+        done += k
+        u, _, t, _ = ens.get_state(want_prev=False)
+        assert np.all(np.isfinite(u))
+        rad.append((t, np.mean(np.einsum("ij,ij->i", u[0, nodes, :2], rhat))))
+    rad = np.array(rad)
+    static = 13 * 1333.22 * 4 / (7e6 * 0.4)          # Laplace scale of the 13 mmHg baseline
+    assert np.all(np.abs(rad[:, 1]) < 10 * static)
+    # peak systole (40 mmHg) vs diastole (13 mmHg): the radius follows the load
+    tau = rad[:, 0] % 0.8
+    sys_ = rad[(tau > 0.12) & (tau < 0.18) & (rad[:, 0] > 0.8), 1]
+    dia = rad[(tau > 0.5) & (tau < 0.75) & (rad[:, 0] > 0.8), 1]
+    assert sys_.mean() > 1.5 * dia.mean() > 0
+    ens.close()
+
+
+def test_c4_aorta_sampled_parity():
+    """Config c4 mesh (synthetic branched aorta, ~500k triangles) with N_s = 8: every
+    kernel against the oracle on sampled realisations after 100 steps."""
+    cfg = configs.make("c4", n_s=8)
+    m = cfg.mesh
+    tr = cfg.traction
+    out = {}
+    for kernel in ("assembled", "assembled_sym", "matrix_free"):
+        ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS, kernel=kernel)
+        dt = ens.info()["dt"]
+        ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+        ens.step(100)
+        out[kernel] = ens.get_state(want_prev=False)[0]
+        ens.close()
+    assert np.array_equal(out["assembled"], out["assembled_sym"])
+    for s in (1, 6):
+        om = oracle.OracleModel(m.xyz, m.tris, m.fixed, cfg.E[s:s + 1], cfg.h[s:s + 1], rho=RHO, nu=NU,
+                                k_shear=KS, dt=dt)
+        om.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+        om.run(100)
+        for kernel in out:
+            ref = om.u_n[0]
+            assert np.linalg.norm(out[kernel][s] - ref) <= 1e-9 * np.linalg.norm(ref), kernel
