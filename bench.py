@@ -208,6 +208,25 @@ def _node_partition_run(args, cfg, base, m, tr, rank, world, local, stream, barr
     return node
 
 
+def _read_stream_gbs(gib: float = 4.0, reps: int = 10) -> float:
+    """Practical ceiling of a read-dominated kernel on this box: torch.sum over a 4 GiB fp64
+    tensor, best of `reps`, CUDA events."""
+    import torch
+    x = torch.ones(int(gib * (1 << 30)) // 8, dtype=torch.float64, device="cuda")
+    best = float("inf")
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        x.sum()
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    n = x.numel() * 8
+    del x
+    torch.cuda.empty_cache()
+    return n / best / 1e9
+
+
 def _time_kernel(kernel, args, cfg, m, tr, world, rank, local, stream, barrier, peak):
     """Time `kernel` on the same workload exactly like the headline (CUDA events around
     ens_step(K) on the context stream, max over ranks)."""
@@ -363,6 +382,8 @@ def main(argv=None):
             except Exception as e:
                 alts[k] = {"error": repr(e)[:200]}
 
+    read_gbs = _read_stream_gbs() if rank == 0 else None
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = _cpu_baseline(base)
@@ -381,7 +402,8 @@ def main(argv=None):
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": {"assembled": "k_step_assembled", "assembled_sym": "k_step_assembled_sym",
                                     "matrix_free": "k_step_matrix_free"}[args.kernel],
-                         "algorithmic_bytes_per_launch": info["bytes_per_step"]},
+                         "algorithmic_bytes_per_launch": info["bytes_per_step"],
+                         "read_stream_GBs": read_gbs, "frac_of_read_stream": achieved / read_gbs if read_gbs else None},
             "cpu_baseline": cpu,
             "alternatives": alts,
             "node_partition": node,

@@ -732,6 +732,7 @@ cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st) {
 // Matrix-free variants (tuning knob ENS_MF_VARIANT = 0..3):
 //   0: VEC 2, batch 1, >= 2 CTAs/SM   1: VEC 2, batch 2, >= 2 CTAs/SM
 //   2: VEC 1, batch 2, >= 3 CTAs/SM   3: VEC 1, batch 1, >= 4 CTAs/SM
+//   4: VEC 2, batch 1, >= 3 CTAs/SM   5: VEC 2, batch 2, >= 3 CTAs/SM
 int mf_variant() {
     static int v = [] {
         const char* e = std::getenv("ENS_MF_VARIANT");
@@ -752,6 +753,8 @@ cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
     const int var = mf_variant();
     if (vec == 2) {
         if (var == 1) return ap ? launch_a2<2, true, 2, 2>(a, st) : launch_a2<2, false, 2, 2>(a, st);
+        if (var == 4) return ap ? launch_a2<2, true, 1, 3>(a, st) : launch_a2<2, false, 1, 3>(a, st);
+        if (var == 5) return ap ? launch_a2<2, true, 2, 3>(a, st) : launch_a2<2, false, 2, 3>(a, st);
         return ap ? launch_a2<2, true, 1, 2>(a, st) : launch_a2<2, false, 1, 2>(a, st);
     }
     if (var == 3) return ap ? launch_a2<1, true, 1, 4>(a, st) : launch_a2<1, false, 1, 4>(a, st);
