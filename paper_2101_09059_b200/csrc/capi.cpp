@@ -962,16 +962,13 @@ int ens_query(const ens_ctx* c, ens_info* info) {
     // algorithmic HBM bytes of the rows this context advances: values +
     // u_n, u_{n-1} read, u_{n+1} written, c1 (+ c2, c3) per node per realisation
     const int64_t ns = c->n_s, per_node = 3 * 8 * 3 + 8 + (c->damping == ENS_DAMP_IDENTITY ? 16 : 0);
-    int64_t own = 0, blocks = 0, inc = 0, halo = 0, launches = 0;
+    int64_t own = 0, halo = 0, launches = 0;
     for (const Part& p : c->parts) {
         own += p.n_own;
-        blocks += (c->kernel == ENS_KERNEL_ASSEMBLED) ? 0 : 0;
         halo += int64_t(p.plan.send_rows.size());
         for (const auto& pe : p.plan.peers) halo += pe.recv_n;
         launches += c->has_halo() ? (1 + (p.plan.b_lo > 0) + (p.plan.b_hi > 0) + !p.plan.send_rows.empty()) : 1;
     }
-    (void)blocks;
-    (void)inc;
     info->n_owned = own;
     info->halo_bytes_per_step = halo * 3 * 8 * ns;
     info->launches_per_step = int32_t(launches);

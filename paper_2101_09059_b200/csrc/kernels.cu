@@ -22,8 +22,6 @@ namespace {
 
 constexpr int kThreads = 256;
 
-struct d4 { double x, y, z, w; };
-
 template <int VEC> struct Vec;
 template <> struct Vec<1> { double v[1]; };
 template <> struct Vec<2> { double v[2]; };
@@ -733,6 +731,7 @@ cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st) {
 //   0: VEC 2, batch 1, >= 2 CTAs/SM   1: VEC 2, batch 2, >= 2 CTAs/SM
 //   2: VEC 1, batch 2, >= 3 CTAs/SM   3: VEC 1, batch 1, >= 4 CTAs/SM
 //   4: VEC 2, batch 1, >= 3 CTAs/SM   5: VEC 2, batch 2, >= 3 CTAs/SM
+//   6: VEC 4 (256-bit loads, half a warp per row), batch 1
 int mf_variant() {
     static int v = [] {
         const char* e = std::getenv("ENS_MF_VARIANT");
@@ -743,7 +742,8 @@ int mf_variant() {
 
 int pick_vec_mf(int32_t n_s) {
     const int v = mf_variant();
-    if (v >= 2 || n_s % 2) return 1;
+    if (v == 6 && n_s % 4 == 0) return 4;
+    if (v == 2 || v == 3 || n_s % 2) return 1;
     return 2;
 }
 
@@ -751,6 +751,7 @@ cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
     const bool ap = a.y_out != nullptr;
     const int vec = pick_vec_mf(a.n_s);
     const int var = mf_variant();
+    if (vec == 4) return ap ? launch_a2<4, true, 1, 1>(a, st) : launch_a2<4, false, 1, 1>(a, st);
     if (vec == 2) {
         if (var == 1) return ap ? launch_a2<2, true, 2, 2>(a, st) : launch_a2<2, false, 2, 2>(a, st);
         if (var == 4) return ap ? launch_a2<2, true, 1, 3>(a, st) : launch_a2<2, false, 1, 3>(a, st);
