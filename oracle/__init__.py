@@ -58,6 +58,7 @@ def lib():
             "orc_run": (i64, [i64, vp, vp, i32, vp, vp, vp, vp, vp, i32, vp, i32, vp, vp, f64, f64,
                               f64, i64, i64, vp, vp]),
             "orc_partition_bounds": (None, [i64, vp, i32, vp]),
+            "orc_stress": (None, [i64, i64, vp, vp, i32, vp, vp, f64, f64, i32, vp, i32, vp]),
             "orc_ghosts": (i64, [i64, vp, vp, i64, i64, vp]),
         }
         for name, (res, args) in sig.items():
@@ -199,6 +200,32 @@ def spmm(row_ptr, col, Kval, u):
     y = np.zeros_like(u)
     lib().orc_spmm(len(row_ptr) - 1, _p(row_ptr), _p(col), u.shape[0], _p(Kval), _p(u), _p(y))
     return y
+
+
+def stress(xyz, tris, E, u, nu, k_shear, frame=1, centerline=None):
+    """Element stresses [n_s][F][6] (orc_stress; frame 0 local shell, 1 cylindrical)."""
+    xyz, tris, E, u = _c(xyz, np.float64), _c(tris, np.int32), _c(E, np.float64), _c(u, np.float64)
+    cl = None if centerline is None else _c(centerline, np.float64)
+    n_s, F = E.shape[0], tris.shape[0]
+    out = np.zeros((n_s, F, 6))
+    lib().orc_stress(xyz.shape[0], F, _p(xyz), _p(tris), n_s, _p(E), _p(u), nu, k_shear, frame,
+                     _p(cl), 0 if cl is None else cl.shape[0], _p(out))
+    return out
+
+
+def ensemble_stats(values, q=(0.05, 0.95)):
+    """Mean and quantiles over realisations (axis 0).  Quantile p of n sorted values v:
+    h = (n - 1) p, v[floor h] + (h - floor h) (v[floor h + 1] - v[floor h]) (the 5%-95%
+    bands of PAPER.md:452; linear interpolation between order statistics)."""
+    v = np.sort(np.asarray(values, dtype=np.float64), axis=0)
+    n = v.shape[0]
+    out = [v.mean(axis=0)]
+    for p in q:
+        h = (n - 1) * p
+        lo = int(np.floor(h))
+        hi = min(lo + 1, n - 1)
+        out.append(v[lo] + (h - lo) * (v[hi] - v[lo]))
+    return out
 
 
 def run_raw(row_ptr, col, Kval, c1, c2, c3, fixed, u_n, u_nm1, *, dt, nsteps, step0=0,

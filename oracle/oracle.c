@@ -620,3 +620,140 @@ int64_t orc_ghosts(int64_t V, const int64_t* row_ptr, const int32_t* col, int64_
     free(mark);
     return n;
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* Stress recovery (Eq. 7-9).  For element e and   */
+/* realisation s: local strain eps = B (T u_e) (Eq. 8, constant on the element), stress  */
+/* sigma = C(Ebar) eps (Eq. 7, 9) with Ebar the element mean of the nodal E (= the mean  */
+/* over the three Gauss points, sigma being linear in E).  frame 0: local shell frame,   */
+/* out = (s_xx, s_yy, t_xy, t_xz, t_yz, 0).  frame 1: "cylindrical" frame of PAPER.md:320: */
+/* r = the element normal, z = tangent of the centreline at its point closest to the     */
+/* element centroid (made orthogonal to r), theta = r x z;                                */
+/* out = (s_rr, s_tt, s_zz, s_tz, s_rz, s_rt) of the 3-D tensor [[s_xx t_xy t_xz],        */
+/* [t_xy s_yy t_yz], [t_xz t_yz 0]] (eps_zz = 0) rotated from the local     */
+/* basis.  centerline: [n_c][3] polyline, or NULL for the z axis.  out: [n_s][F][6].       */
+/* ------------------------------------------------------------------------------------ */
+static void closest_tangent(const double* c, const double* cl, int32_t n_c, double* tz) {
+    if (!cl || n_c < 2) { tz[0] = 0.0; tz[1] = 0.0; tz[2] = 1.0; return; }
+    double best = INFINITY;
+    for (int32_t k = 0; k + 1 < n_c; k++) {
+        const double* A = cl + 3 * k;
+        const double* B = cl + 3 * (k + 1);
+        double d[3] = {B[0] - A[0], B[1] - A[1], B[2] - A[2]};
+        double dd = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+        double t = ((c[0] - A[0]) * d[0] + (c[1] - A[1]) * d[1] + (c[2] - A[2]) * d[2]) / dd;
+        if (t < 0.0) t = 0.0;
+        if (t > 1.0) t = 1.0;
+        double q[3] = {A[0] + t * d[0] - c[0], A[1] + t * d[1] - c[1], A[2] + t * d[2] - c[2]};
+        double dist = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
+        if (dist < best) {
+            best = dist;
+            double nd = sqrt(dd);
+            tz[0] = d[0] / nd; tz[1] = d[1] / nd; tz[2] = d[2] / nd;
+        }
+    }
+}
+
+void orc_stress(int64_t V, int64_t F, const double* xyz, const int32_t* tris, int32_t n_s,
+                const double* E, const double* u, double nu, double kshear, int32_t frame,
+                const double* centerline, int32_t n_c, double* out) {
+    for (int64_t e = 0; e < F; e++) {
+        const int32_t* t = tris + 3 * e;
+        const double* X1 = xyz + 3 * (int64_t)t[0];
+        const double* X2 = xyz + 3 * (int64_t)t[1];
+        const double* X3 = xyz + 3 * (int64_t)t[2];
+        double d21[3], d31[3], n[3], e1[3], e2[3], e3[3];
+        for (int c = 0; c < 3; c++) { d21[c] = X2[c] - X1[c]; d31[c] = X3[c] - X1[c]; }
+        n[0] = d21[1] * d31[2] - d21[2] * d31[1];
+        n[1] = d21[2] * d31[0] - d21[0] * d31[2];
+        n[2] = d21[0] * d31[1] - d21[1] * d31[0];
+        double nn = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+        double A = 0.5 * nn;
+        double l21 = sqrt(d21[0] * d21[0] + d21[1] * d21[1] + d21[2] * d21[2]);
+        for (int c = 0; c < 3; c++) { e1[c] = d21[c] / l21; e3[c] = n[c] / nn; }
+        e2[0] = e3[1] * e1[2] - e3[2] * e1[1];
+        e2[1] = e3[2] * e1[0] - e3[0] * e1[2];
+        e2[2] = e3[0] * e1[1] - e3[1] * e1[0];
+        const double* Xs[3] = {X1, X2, X3};
+        double x[3], y[3];
+        for (int a = 0; a < 3; a++) {
+            double d[3] = {Xs[a][0] - X1[0], Xs[a][1] - X1[1], Xs[a][2] - X1[2]};
+            x[a] = d[0] * e1[0] + d[1] * e1[1] + d[2] * e1[2];
+            y[a] = d[0] * e2[0] + d[1] * e2[1] + d[2] * e2[2];
+        }
+        double y23 = y[1] - y[2], y31 = y[2] - y[0], y12 = y[0] - y[1];
+        double x32 = x[2] - x[1], x13 = x[0] - x[2], x21 = x[1] - x[0];
+        double Bm[5][9];
+        memset(Bm, 0, sizeof(Bm));
+        Bm[0][0] = y23; Bm[0][3] = y31; Bm[0][6] = y12;
+        Bm[1][1] = x32; Bm[1][4] = x13; Bm[1][7] = x21;
+        Bm[2][0] = x32; Bm[2][1] = y23; Bm[2][3] = x13; Bm[2][4] = y31; Bm[2][6] = x21; Bm[2][7] = y12;
+        Bm[3][2] = y23; Bm[3][5] = y31; Bm[3][8] = y12;
+        Bm[4][2] = x32; Bm[4][5] = x13; Bm[4][8] = x21;
+        /* output basis (rows b_p in global coordinates) */
+        double b[3][3];
+        if (frame == 1) {
+            double cen[3] = {(X1[0] + X2[0] + X3[0]) / 3.0, (X1[1] + X2[1] + X3[1]) / 3.0, (X1[2] + X2[2] + X3[2]) / 3.0};
+            double tz[3];
+            closest_tangent(cen, centerline, n_c, tz);
+            double dz = tz[0] * e3[0] + tz[1] * e3[1] + tz[2] * e3[2];
+            double z[3] = {tz[0] - dz * e3[0], tz[1] - dz * e3[1], tz[2] - dz * e3[2]};
+            double zn = sqrt(z[0] * z[0] + z[1] * z[1] + z[2] * z[2]);
+            for (int c = 0; c < 3; c++) { b[0][c] = e3[c]; b[2][c] = z[c] / zn; }
+            b[1][0] = b[0][1] * b[2][2] - b[0][2] * b[2][1];   /* theta = r x z */
+            b[1][1] = b[0][2] * b[2][0] - b[0][0] * b[2][2];
+            b[1][2] = b[0][0] * b[2][1] - b[0][1] * b[2][0];
+        }
+        for (int32_t s = 0; s < n_s; s++) {
+            const double* us = u + (int64_t)s * V * 3;
+            double ul[9];
+            for (int a = 0; a < 3; a++) {
+                const double* ug = us + 3 * (int64_t)t[a];
+                ul[3 * a + 0] = e1[0] * ug[0] + e1[1] * ug[1] + e1[2] * ug[2];
+                ul[3 * a + 1] = e2[0] * ug[0] + e2[1] * ug[1] + e2[2] * ug[2];
+                ul[3 * a + 2] = e3[0] * ug[0] + e3[1] * ug[1] + e3[2] * ug[2];
+            }
+            double eps[5];
+            for (int r = 0; r < 5; r++) {
+                double acc = 0.0;
+                for (int k = 0; k < 9; k++) acc += Bm[r][k] * ul[k];
+                eps[r] = acc / (2.0 * A);
+            }
+            double Eb = (E[(int64_t)s * V + t[0]] + E[(int64_t)s * V + t[1]] + E[(int64_t)s * V + t[2]]) / 3.0;
+            double pre = Eb / (1.0 - nu * nu);
+            double sg[5];
+            sg[0] = pre * (eps[0] + nu * eps[1]);
+            sg[1] = pre * (nu * eps[0] + eps[1]);
+            sg[2] = pre * 0.5 * (1.0 - nu) * eps[2];
+            sg[3] = pre * 0.5 * kshear * (1.0 - nu) * eps[3];
+            sg[4] = pre * 0.5 * kshear * (1.0 - nu) * eps[4];
+            double* o = out + ((int64_t)s * F + e) * 6;
+            if (frame == 0) {
+                for (int k = 0; k < 5; k++) o[k] = sg[k];
+                o[5] = 0.0;
+                continue;
+            }
+            /* S_local -> global -> cylindrical */
+            double Sl[3][3] = {{sg[0], sg[2], sg[3]}, {sg[2], sg[1], sg[4]}, {sg[3], sg[4], 0.0}};
+            double R[3][3] = {{e1[0], e1[1], e1[2]}, {e2[0], e2[1], e2[2]}, {e3[0], e3[1], e3[2]}};
+            double Sg[3][3];
+            for (int i = 0; i < 3; i++)
+                for (int j = 0; j < 3; j++) {
+                    double acc = 0.0;
+                    for (int p = 0; p < 3; p++)
+                        for (int q = 0; q < 3; q++) acc += R[p][i] * Sl[p][q] * R[q][j];
+                    Sg[i][j] = acc;
+                }
+            double Sc[3][3];
+            for (int i = 0; i < 3; i++)
+                for (int j = 0; j < 3; j++) {
+                    double acc = 0.0;
+                    for (int p = 0; p < 3; p++)
+                        for (int q = 0; q < 3; q++) acc += b[i][p] * Sg[p][q] * b[j][q];
+                    Sc[i][j] = acc;
+                }
+            o[0] = Sc[0][0]; o[1] = Sc[1][1]; o[2] = Sc[2][2];
+            o[3] = Sc[1][2]; o[4] = Sc[0][2]; o[5] = Sc[0][1];
+        }
+    }
+}
