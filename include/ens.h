@@ -177,6 +177,24 @@ int ens_set_state(ens_ctx* ctx, const double* u_n, const double* u_nm1, double t
  * and summation order as ens_step).  u: full [n_s][V][3]; y: [n_s][R][3] as ens_get_state. */
 int ens_apply_stiffness(ens_ctx* ctx, const double* u, double* y);
 
+/* Element stresses of u_n and their ensemble statistics (the step after the hot path,
+ * SURVEY.md §8(f) N1).  Per element e and realisation s: eps = B T u_e (Eq. 8), sigma =
+ * C(Ebar_{e,s}) eps (Eq. 7, 9; Ebar = element mean of the nodal E = the mean over the three
+ * Gauss points).  frame 0: local shell frame, (s_xx, s_yy, t_xy, t_xz, t_yz, 0);
+ * frame 1: the paper's frame: r = element normal, z = tangent of the
+ * centreline polyline at its point closest to the centroid (orthogonalised to r),
+ * theta = r x z; (s_rr, s_tt, s_zz, s_tz, s_rz, s_rt).  centerline [n_c][3] (n_c >= 2) or
+ * NULL for the z axis.  Outputs (host, each may be NULL): sigma [n_s][F][6];
+ * mean, q05, q95 [F][6] over the realisations: quantile p of the n
+ * sorted values v is v[lo] + (h - lo)(v[lo+1] - v[lo]), h = (n-1) p, lo = floor(h).
+ * Single-part contexts (not NODE on NCCL).  Synchronises. */
+int ens_stress(ens_ctx* ctx, int32_t frame, const double* centerline, int32_t n_c, double* sigma,
+               double* mean, double* q05, double* q95);
+
+/* Ensemble statistics of u_n per node (caller numbering): mean, q05, q95 [V][4] =
+ * (u_x, u_y, u_z, |u|), same quantile definition.  Single-part contexts.  Synchronises. */
+int ens_displacement_stats(ens_ctx* ctx, double* mean, double* q05, double* q95);
+
 /* Sizes, dt and algorithmic traffic of the context. */
 int ens_query(const ens_ctx* ctx, ens_info* info);
 

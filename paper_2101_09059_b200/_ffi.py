@@ -53,7 +53,8 @@ EXPORTS = [
     "ens_create", "ens_set_traction", "ens_step", "ens_sync", "ens_get_state", "ens_set_state",
     "ens_apply_stiffness", "ens_query", "ens_destroy", "ens_last_error", "ens_host_validate",
     "ens_host_pattern", "ens_host_partition", "ens_host_ghosts", "ens_host_element_stiffness",
-    "ens_host_materials", "ens_create_csr", "ens_get_owned", "ens_host_halo_plan",
+    "ens_host_materials", "ens_create_csr", "ens_get_owned", "ens_host_halo_plan", "ens_stress",
+    "ens_displacement_stats",
 ]
 
 _lib = None
@@ -97,6 +98,8 @@ def lib():
         "ens_host_materials": (C.c_int, [i64, i64, vp, vp, i32, vp, vp, f64, f64, vp, vp, P(f64)]),
         "ens_create_csr": (C.c_int, [i64, vp, vp, i32, vp, vp, vp, vp, vp, f64, P(EnsOptions), P(vp)]),
         "ens_get_owned": (C.c_int, [vp, vp, P(i64)]),
+        "ens_stress": (C.c_int, [vp, i32, vp, i32, vp, vp, vp, vp]),
+        "ens_displacement_stats": (C.c_int, [vp, vp, vp, vp]),
         "ens_host_halo_plan": (C.c_int, [i64, vp, vp, i32, i32, vp, vp, vp, vp, i64, P(i64), P(i64)]),
     }
     for name, (res, args) in sig.items():

@@ -17,6 +17,7 @@
 #include "device.hpp"
 #include "host_setup.hpp"
 #include "nccl_dl.hpp"
+#include "observe.hpp"
 
 namespace {
 
@@ -84,6 +85,14 @@ struct ens_ctx {
 
     int64_t step = 0;
     bool latched = false;
+
+    // observation (stresses, statistics): host mesh copy, element E means, lazy operators
+    std::vector<double> h_xyz;
+    std::vector<int32_t> h_tris;
+    double nu = 0.0, k_shear = 0.0;
+    double* d_Ebar = nullptr;               // [F][n_s]
+    double* d_G = nullptr;                  // [F][45]
+    int32_t* d_etri = nullptr;              // [F][3] RCM ids
 
     int32_t graph_steps = 64;               // CUDA graph of this many steps (single part, no halo)
     cudaGraphExec_t graph = nullptr;
@@ -656,6 +665,21 @@ int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, cons
         for (size_t k = 0; k < plans.size(); ++k) c->parts[k].plan = plans[k];
     }
     for (Part& p : c->parts) RC_TRY(build_part(c, p, G));
+    // element means of E per realisation (stress recovery, ens_stress)
+    c->h_xyz.assign(mesh->xyz, mesh->xyz + 3 * V);
+    c->h_tris.assign(mesh->tris, mesh->tris + 3 * F);
+    c->nu = mat->nu;
+    c->k_shear = mat->k_shear;
+    {
+        std::vector<double> eb(size_t(F) * size_t(mat->n_s));
+        for (int64_t e = 0; e < F; ++e)
+            for (int64_t s = 0; s < mat->n_s; ++s) {
+                const double* Es = mat->E + s * V;
+                eb[size_t(e * mat->n_s + s)] =
+                    (Es[mesh->tris[3 * e]] + Es[mesh->tris[3 * e + 1]] + Es[mesh->tris[3 * e + 2]]) / 3.0;
+            }
+        RC_TRY(upload(c, &c->d_Ebar, eb.data(), eb.size()));
+    }
     return finish_create(c);
 }
 
@@ -941,6 +965,118 @@ int ens_apply_stiffness(ens_ctx* c, const double* u, double* y) {
                                 cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return ENS_OK;
+}
+
+static int observe_check(ens_ctx* c) {
+    if (c->parts.size() != 1 || c->nccl_comm || c->h_tris.empty())
+        return fail(c, ENS_E_UNSUPPORTED, "stresses / statistics need a single-part context created by ens_create");
+    return ENS_OK;
+}
+
+int ens_stress(ens_ctx* c, int32_t frame, const double* centerline, int32_t n_c, double* sigma, double* mean,
+               double* q05, double* q95) {
+    if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
+    if (frame < 0 || frame > 1) return fail(c, ENS_E_ARG, "frame must be 0 (local) or 1 (centreline)");
+    if (centerline && n_c < 2) return fail(c, ENS_E_ARG, "centerline needs n_c >= 2 points");
+    RC_TRY(observe_check(c));
+    const int rc = ens_sync(c);
+    if (rc && rc != ENS_E_DIVERGED) return rc;
+    const int64_t F = c->F, n_s = c->n_s;
+    if (!c->d_G) {
+        std::vector<double> Gh(size_t(F) * 45), R(9);
+        std::vector<int32_t> et(size_t(F) * 3);
+        for (int64_t e = 0; e < F; ++e) {
+            const int32_t* t = c->h_tris.data() + 3 * e;
+            ens::element_strain_operator(&c->h_xyz[3 * size_t(t[0])], &c->h_xyz[3 * size_t(t[1])],
+                                         &c->h_xyz[3 * size_t(t[2])], Gh.data() + 45 * e, R.data());
+            for (int a = 0; a < 3; ++a) et[size_t(3 * e + a)] = c->iperm[size_t(t[a])];
+        }
+        RC_TRY(upload(c, &c->d_G, Gh.data(), Gh.size()));
+        RC_TRY(upload(c, &c->d_etri, et.data(), et.size()));
+    }
+    std::vector<double> Mh(size_t(F) * 9), Gtmp(45), R(9);
+    for (int64_t e = 0; e < F; ++e) {
+        const int32_t* t = c->h_tris.data() + 3 * e;
+        const double* X[3] = {&c->h_xyz[3 * size_t(t[0])], &c->h_xyz[3 * size_t(t[1])], &c->h_xyz[3 * size_t(t[2])]};
+        ens::element_strain_operator(X[0], X[1], X[2], Gtmp.data(), R.data());
+        const double cen[3] = {(X[0][0] + X[1][0] + X[2][0]) / 3.0, (X[0][1] + X[1][1] + X[2][1]) / 3.0,
+                               (X[0][2] + X[1][2] + X[2][2]) / 3.0};
+        ens::stress_frame(cen, R.data(), frame, centerline, n_c, Mh.data() + 9 * e);
+    }
+    double *d_M = nullptr, *d_out = nullptr;
+    RC_TRY(upload(c, &d_M, Mh.data(), Mh.size()));
+    RC_TRY(dalloc(c, &d_out, size_t(F) * 6 * size_t(n_s)));
+    const Part& p = c->parts[0];
+    const double* un = (c->step & 1) ? p.d_u1 : p.d_u0;
+    CUDA_TRY(c, ens::launch_stress(F, c->n_s, frame, c->d_etri, c->d_G, d_M, c->d_Ebar, c->nu, c->k_shear, un, d_out,
+                                   c->stream));
+    if (sigma) {
+        double* d_abi = nullptr;
+        RC_TRY(dalloc(c, &d_abi, size_t(F) * 6 * size_t(n_s)));
+        CUDA_TRY(c, ens::launch_to_abi(F, 6, c->n_s, nullptr, d_out, d_abi, c->stream));
+        CUDA_TRY(c, cudaMemcpyAsync(sigma, d_abi, size_t(F) * 6 * size_t(n_s) * sizeof(double), cudaMemcpyDeviceToHost,
+                                    c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        dfree(c, d_abi);
+    }
+    if (mean || q05 || q95) {
+        const int64_t n_seg = F * 6;
+        double *d_sorted = nullptr, *d_st = nullptr;
+        unsigned char* d_tmp = nullptr;
+        const size_t tb = ens::stats_temp_bytes(n_seg, c->n_s);
+        RC_TRY(dalloc(c, &d_sorted, size_t(n_seg) * size_t(n_s)));
+        RC_TRY(dalloc(c, &d_tmp, tb));
+        RC_TRY(dalloc(c, &d_st, size_t(n_seg) * 3));
+        CUDA_TRY(c, ens::ensemble_stats(n_seg, c->n_s, 6, nullptr, 6, 0, d_out, d_sorted, d_tmp, tb, d_st, d_st + n_seg,
+                                        d_st + 2 * n_seg, c->stream));
+        double* outs[3] = {mean, q05, q95};
+        for (int k = 0; k < 3; ++k)
+            if (outs[k])
+                CUDA_TRY(c, cudaMemcpyAsync(outs[k], d_st + k * n_seg, size_t(n_seg) * sizeof(double),
+                                            cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        dfree(c, d_sorted);
+        dfree(c, d_tmp);
+        dfree(c, d_st);
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    dfree(c, d_M);
+    dfree(c, d_out);
+    return rc;
+}
+
+int ens_displacement_stats(ens_ctx* c, double* mean, double* q05, double* q95) {
+    if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
+    RC_TRY(observe_check(c));
+    const int rc = ens_sync(c);
+    if (rc && rc != ENS_E_DIVERGED) return rc;
+    const int64_t V = c->V, n_s = c->n_s;
+    const Part& p = c->parts[0];
+    const double* un = (c->step & 1) ? p.d_u1 : p.d_u0;
+    double *d_mag = nullptr, *d_sorted = nullptr, *d_st = nullptr;
+    unsigned char* d_tmp = nullptr;
+    const size_t tb = ens::stats_temp_bytes(3 * V, c->n_s);
+    RC_TRY(dalloc(c, &d_mag, size_t(V) * size_t(n_s)));
+    RC_TRY(dalloc(c, &d_sorted, size_t(3 * V) * size_t(n_s)));
+    RC_TRY(dalloc(c, &d_tmp, tb));
+    RC_TRY(dalloc(c, &d_st, size_t(V) * 4 * 3));
+    CUDA_TRY(c, ens::launch_magnitude(V, c->n_s, un, d_mag, c->stream));
+    // components: segments (row i, c) of u itself; rows written at the caller's node id
+    CUDA_TRY(c, ens::ensemble_stats(3 * V, c->n_s, 3, p.d_map_own, 4, 0, un, d_sorted, d_tmp, tb, d_st, d_st + 4 * V,
+                                    d_st + 8 * V, c->stream));
+    CUDA_TRY(c, ens::ensemble_stats(V, c->n_s, 1, p.d_map_own, 4, 3, d_mag, d_sorted, d_tmp, tb, d_st, d_st + 4 * V,
+                                    d_st + 8 * V, c->stream));
+    double* outs[3] = {mean, q05, q95};
+    for (int k = 0; k < 3; ++k)
+        if (outs[k])
+            CUDA_TRY(c, cudaMemcpyAsync(outs[k], d_st + k * 4 * V, size_t(V) * 4 * sizeof(double), cudaMemcpyDeviceToHost,
+                                        c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    dfree(c, d_mag);
+    dfree(c, d_sorted);
+    dfree(c, d_tmp);
+    dfree(c, d_st);
+    return rc;
 }
 
 int ens_query(const ens_ctx* c, ens_info* info) {

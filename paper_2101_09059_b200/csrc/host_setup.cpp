@@ -226,6 +226,80 @@ void element_stiffness(const double* X1, const double* X2, const double* X3, dou
 }
 
 // ------------------------------------------------------------------------------------
+// Stress recovery operators.  With b_a, c_a as in element_stiffness:
+// eps_xx = sum b_a ux_a / 2A, eps_yy = sum c_a uy_a / 2A, gamma_xy = sum (c_a ux_a + b_a uy_a)
+// / 2A, gamma_xz = sum b_a uz_a / 2A, gamma_yz = sum c_a uz_a / 2A (Eq. 8), u_local = R u.
+// ------------------------------------------------------------------------------------
+void element_strain_operator(const double* X1, const double* X2, const double* X3, double* G, double* R) {
+    auto d21 = sub(X2, X1), d31 = sub(X3, X1);
+    auto n = cross(d21, d31);
+    const double nn = norm(n), A = 0.5 * nn, l = norm(d21);
+    std::array<double, 3> e1{d21[0] / l, d21[1] / l, d21[2] / l};
+    std::array<double, 3> e3{n[0] / nn, n[1] / nn, n[2] / nn};
+    auto e2 = cross(e3, e1);
+    const double* X[3] = {X1, X2, X3};
+    double x[3], y[3];
+    for (int a = 0; a < 3; ++a) {
+        auto d = sub(X[a], X1);
+        x[a] = dot(d, e1);
+        y[a] = dot(d, e2);
+    }
+    const double b[3] = {y[1] - y[2], y[2] - y[0], y[0] - y[1]};
+    const double c[3] = {x[2] - x[1], x[0] - x[2], x[1] - x[0]};
+    const double f = 1.0 / (2.0 * A);
+    const std::array<double, 3>* E[3] = {&e1, &e2, &e3};
+    for (int a = 0; a < 3; ++a)
+        for (int d = 0; d < 3; ++d) {              // global component d of node a
+            const double ex = e1[d], ey = e2[d], ez = e3[d];
+            G[0 * 9 + 3 * a + d] = f * b[a] * ex;
+            G[1 * 9 + 3 * a + d] = f * c[a] * ey;
+            G[2 * 9 + 3 * a + d] = f * (c[a] * ex + b[a] * ey);
+            G[3 * 9 + 3 * a + d] = f * b[a] * ez;
+            G[4 * 9 + 3 * a + d] = f * c[a] * ez;
+        }
+    for (int r = 0; r < 3; ++r)
+        for (int d = 0; d < 3; ++d) R[3 * r + d] = (*E[r])[d];
+}
+
+void stress_frame(const double* centroid, const double* R, int32_t frame, const double* centerline,
+                  int32_t n_c, double* M) {
+    if (frame == 0) {
+        for (int k = 0; k < 9; ++k) M[k] = (k % 4 == 0) ? 1.0 : 0.0;
+        return;
+    }
+    std::array<double, 3> tz{0.0, 0.0, 1.0};
+    if (centerline && n_c >= 2) {
+        double best = INFINITY;
+        for (int32_t k = 0; k + 1 < n_c; ++k) {
+            const double* P = centerline + 3 * k;
+            const double* Q = centerline + 3 * (k + 1);
+            auto d = sub(Q, P);
+            const double dd = dot(d, d);
+            double t = dot(sub(centroid, P), d) / dd;
+            t = std::min(1.0, std::max(0.0, t));
+            const std::array<double, 3> q{P[0] + t * d[0] - centroid[0], P[1] + t * d[1] - centroid[1],
+                                          P[2] + t * d[2] - centroid[2]};
+            const double dist = dot(q, q);
+            if (dist < best) {
+                best = dist;
+                const double nd = std::sqrt(dd);
+                tz = {d[0] / nd, d[1] / nd, d[2] / nd};
+            }
+        }
+    }
+    const std::array<double, 3> r{R[6], R[7], R[8]};
+    const double rz = dot(tz, r);
+    std::array<double, 3> z{tz[0] - rz * r[0], tz[1] - rz * r[1], tz[2] - rz * r[2]};
+    const double zn = norm(z);
+    z = {z[0] / zn, z[1] / zn, z[2] / zn};
+    const auto th = cross(r, z);
+    const std::array<double, 3>* bas[3] = {&r, &th, &z};
+    for (int p = 0; p < 3; ++p)                     // M = b R^T: M[p][q] = b_p . e_q
+        for (int q = 0; q < 3; ++q)
+            M[3 * p + q] = (*bas[p])[0] * R[3 * q] + (*bas[p])[1] * R[3 * q + 1] + (*bas[p])[2] * R[3 * q + 2];
+}
+
+// ------------------------------------------------------------------------------------
 // alpha_{e,s} = sum_g w_g E_g zeta_g (Eq. 10 with the 3-point rule)
 // = (1/12) [ (sum_a E_a)(sum_a zeta_a) + sum_a E_a zeta_a ] exactly for P1 fields.
 // m_{i,s} = rho sum_{e ni i} A_e zetabar_{e,s} / 3 (lumped).

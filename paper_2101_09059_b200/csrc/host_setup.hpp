@@ -39,6 +39,16 @@ Pattern build_pattern(const MeshView& m);
 void element_stiffness(const double* X1, const double* X2, const double* X3, double nu,
                        double k_shear, double* Khat, double* area);
 
+// Strain operator of element (X1, X2, X3): eps_local[5] = G[5][9] u_global[9] (Eq. 8 with
+// the frame rotation folded in), and R[3][3] = the local basis (rows e1, e2, e3).
+void element_strain_operator(const double* X1, const double* X2, const double* X3, double* G, double* R);
+
+// Output basis of the stress recovery expressed in the local basis:
+// frame 0: identity; frame 1: rows (r, theta, z) with r = e3, z = the centreline tangent
+// closest to the centroid made orthogonal to r, theta = r x z.  M[3][3] = b R^T.
+void stress_frame(const double* centroid, const double* R, int32_t frame, const double* centerline,
+                  int32_t n_c, double* M);
+
 // alpha[s][e] (closed form of the 3-point Gauss rule on P1 fields), mass[s][v], CFL dt.
 void materials(const MeshView& m, int32_t n_s, const double* E, const double* h, double rho,
                double* alpha, double* mass);

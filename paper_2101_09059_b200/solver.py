@@ -162,6 +162,28 @@ class Ensemble:
         check(lib().ens_apply_stiffness(self._ctx, _p(u), _p(y)), self._ctx)
         return y
 
+    def stress(self, frame: int = 1, centerline=None, per_realisation: bool = True, stats: bool = True):
+        """Element stresses of u_n (ens_stress): dict with 'sigma' [n_s][F][6] and/or
+        'mean', 'q05', 'q95' [F][6]."""
+        F = int(self.info()["n_tris"])
+        cl = None if centerline is None else _c(centerline, np.float64)
+        out = {}
+        sig = np.empty((self.n_s, F, 6)) if per_realisation else None
+        st = [np.empty((F, 6)) for _ in range(3)] if stats else [None] * 3
+        check(lib().ens_stress(self._ctx, int(frame), _p(cl), 0 if cl is None else cl.shape[0], _p(sig),
+                               *[_p(a) for a in st]), self._ctx)
+        if per_realisation:
+            out["sigma"] = sig
+        if stats:
+            out["mean"], out["q05"], out["q95"] = st
+        return out
+
+    def displacement_stats(self):
+        """(mean, q05, q95), each [V][4] = (u_x, u_y, u_z, |u|) over the realisations."""
+        st = [np.empty((self.V, 4)) for _ in range(3)]
+        check(lib().ens_displacement_stats(self._ctx, *[_p(a) for a in st]), self._ctx)
+        return tuple(st)
+
     def info(self) -> dict:
         inf = _ffi.EnsInfo()
         check(lib().ens_query(self._ctx, C.byref(inf)), self._ctx)

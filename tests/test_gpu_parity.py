@@ -360,3 +360,49 @@ def test_c4_aorta_sampled_parity():
         for kernel in out:
             ref = om.u_n[0]
             assert np.linalg.norm(out[kernel][s] - ref) <= 1e-9 * np.linalg.norm(ref), kernel
+
+
+@pytest.mark.parametrize("frame,centerline", [(0, None), (1, None), (1, [[0.5, -0.3, -5.0], [-0.2, 0.4, 12.0], [0.1, 0.0, 40.0]])])
+def test_stress_and_statistics_parity(frame, centerline):
+    """ens_stress / ens_displacement_stats against the oracle on a
+    jittered, renumbered mesh with a random state: per-realisation stresses, their
+    ensemble mean and 5%/95% quantiles."""
+    m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(20, 31), 0.03, 4), 4)
+    n_s = 37
+    E, h = _mats(m, n_s, 81)
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS)
+    rng = np.random.default_rng(frame)
+    u = rng.uniform(-1e-2, 1e-2, (n_s, m.n_nodes, 3))
+    ens.set_state(u, u, 0)
+    got = ens.stress(frame=frame, centerline=centerline)
+    ref = oracle.stress(m.xyz, m.tris, E, u, NU, KS, frame=frame, centerline=centerline)
+    scale = np.abs(ref).max()
+    assert np.abs(got["sigma"] - ref).max() <= 1e-12 * scale
+    rm, r5, r95 = oracle.ensemble_stats(ref)
+    for key, r in (("mean", rm), ("q05", r5), ("q95", r95)):
+        assert np.abs(got[key] - r).max() <= 1e-12 * scale, key
+    dm, d5, d95 = ens.displacement_stats()
+    vals = np.concatenate([u, np.linalg.norm(u, axis=2)[..., None]], axis=2)
+    om, o5, o95 = oracle.ensemble_stats(vals)
+    for g, r in ((dm, om), (d5, o5), (d95, o95)):
+        assert np.abs(g - r).max() <= 1e-14
+    ens.close()
+
+
+def test_c2_hoop_stress_statistics_on_gpu():
+    """c2 to static equilibrium: mid-length hoop stress of the homogeneous member = p R /
+    zeta (1e-3); the 5-95% band brackets the ensemble mean."""
+    cfg = configs.make("c2")
+    m = cfg.mesh
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS,
+                          damping="mass", c_d=cfg.c_d)
+    ens.set_traction(cfg.traction.F)
+    ens.step(10_000)
+    st = ens.stress(frame=1)
+    cz = m.xyz[m.tris].mean(1)[:, 2]
+    mid = np.abs(cz - 15.0) < 1.0
+    hoop = loads.P_SUPERPOSED * 2.0 / 0.4
+    assert st["sigma"][0, mid, 1].mean() == pytest.approx(hoop, rel=1e-3)
+    assert np.all(st["q05"][mid, 1] <= st["mean"][mid, 1]) and np.all(st["mean"][mid, 1] <= st["q95"][mid, 1])
+    assert np.all(st["q95"][mid, 1] - st["q05"][mid, 1] > 0)
+    ens.close()
