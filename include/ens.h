@@ -195,6 +195,18 @@ int ens_stress(ens_ctx* ctx, int32_t frame, const double* centerline, int32_t n_
  * (u_x, u_y, u_z, |u|), same quantile definition.  Single-part contexts.  Synchronises. */
 int ens_displacement_stats(ens_ctx* ctx, double* mean, double* q05, double* q95);
 
+/* GPU Matérn sampler (the step before the hot path): for each of the n
+ * standard-normal vectors z[k][V] (caller numbering) returns the unit-variance GMRF draw
+ *   x[k] = A^-1 C~^{1/2} z[k] / sigma,   A = kappa^2 C~ + G,   kappa = sqrt(8) / rho_corr,
+ *   sigma^2 = 1 / (4 pi kappa^2)
+ * (Matérn nu = 1, alpha = 2; Eqs. 2-6: covariance A^-1 C~ A^-1 = Q_2^-1,
+ * the law of Eq. 11's Cholesky route).  C~: lumped P1 mass; G: P1
+ * stiffness.  All n systems are solved together by Jacobi-preconditioned CG until every
+ * relative residual <= tol (or max_iter).  *iters, *max_rel_res may be NULL.  opt supplies
+ * device, stream and allocator (may be NULL).  Synchronous. */
+int ens_matern_fields(const ens_mesh* mesh, double rho_corr, int32_t n, const double* z, double* x, double tol,
+                      int32_t max_iter, const ens_options* opt, int32_t* iters, double* max_rel_res);
+
 /* Sizes, dt and algorithmic traffic of the context. */
 int ens_query(const ens_ctx* ctx, ens_info* info);
 

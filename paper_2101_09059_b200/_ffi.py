@@ -54,7 +54,7 @@ EXPORTS = [
     "ens_apply_stiffness", "ens_query", "ens_destroy", "ens_last_error", "ens_host_validate",
     "ens_host_pattern", "ens_host_partition", "ens_host_ghosts", "ens_host_element_stiffness",
     "ens_host_materials", "ens_create_csr", "ens_get_owned", "ens_host_halo_plan", "ens_stress",
-    "ens_displacement_stats",
+    "ens_displacement_stats", "ens_matern_fields",
 ]
 
 _lib = None
@@ -100,6 +100,7 @@ def lib():
         "ens_get_owned": (C.c_int, [vp, vp, P(i64)]),
         "ens_stress": (C.c_int, [vp, i32, vp, i32, vp, vp, vp, vp]),
         "ens_displacement_stats": (C.c_int, [vp, vp, vp, vp]),
+        "ens_matern_fields": (C.c_int, [P(EnsMesh), f64, i32, vp, vp, f64, i32, P(EnsOptions), P(i32), P(f64)]),
         "ens_host_halo_plan": (C.c_int, [i64, vp, vp, i32, i32, vp, vp, vp, vp, i64, P(i64), P(i64)]),
     }
     for name, (res, args) in sig.items():

@@ -17,6 +17,7 @@
 #include "device.hpp"
 #include "host_setup.hpp"
 #include "nccl_dl.hpp"
+#include "gmrf.hpp"
 #include "observe.hpp"
 
 namespace {
@@ -1076,6 +1077,63 @@ int ens_displacement_stats(ens_ctx* c, double* mean, double* q05, double* q95) {
     dfree(c, d_sorted);
     dfree(c, d_tmp);
     dfree(c, d_st);
+    return rc;
+}
+
+int ens_matern_fields(const ens_mesh* mesh, double rho_corr, int32_t n, const double* z, double* x, double tol,
+                      int32_t max_iter, const ens_options* opt, int32_t* iters, double* max_rel_res) {
+    if (!mesh || !z || !x || n < 1) return fail(nullptr, ENS_E_ARG, "ens_matern_fields: bad arguments");
+    if (!(rho_corr > 0.0) || !std::isfinite(rho_corr)) return fail(nullptr, ENS_E_ARG, "rho_corr must be > 0");
+    if (!(tol > 0.0) || max_iter < 1) return fail(nullptr, ENS_E_ARG, "tol must be > 0 and max_iter >= 1");
+    if (mesh->n_nodes < 1 || mesh->n_tris < 1 || !mesh->xyz || !mesh->tris)
+        return fail(nullptr, ENS_E_ARG, "mesh needs nodes and triangles");
+    ens::MeshView m{mesh->n_nodes, mesh->n_tris, mesh->xyz, mesh->tris};
+    int64_t bad = -1;
+    if (ens::validate_mesh(m, &bad)) return fail(nullptr, ENS_E_MESH, "invalid mesh (element / node " + std::to_string(bad) + ")");
+    ens_ctx tmp;               // allocation plumbing only
+    ens_ctx* c = &tmp;
+    auto body = [&]() -> int {
+        RC_TRY(init_ctx(c, opt));
+        const int64_t V = m.V;
+        const ens::Pattern pat = ens::build_pattern(m);
+        const double kappa = std::sqrt(8.0) / rho_corr;                 // PAPER.md:67, nu = 1
+        std::vector<double> val, diag, lumped;
+        ens::gmrf_system(m, pat, kappa, val, diag, lumped);
+        std::vector<double> dinv(static_cast<size_t>(V)), sq(static_cast<size_t>(V));
+        for (int64_t i = 0; i < V; ++i) {
+            dinv[size_t(i)] = 1.0 / diag[size_t(i)];
+            sq[size_t(i)] = std::sqrt(lumped[size_t(i)]);
+        }
+        std::vector<int32_t> rp(pat.row_ptr.begin(), pat.row_ptr.end());
+        ens::GmrfSystem S;
+        S.V = V;
+        int32_t *d_rp, *d_col, *d_perm;
+        double *d_val, *d_dinv, *d_sq, *d_z, *d_x, *d_w;
+        RC_TRY(upload(c, &d_rp, rp.data(), rp.size()));
+        RC_TRY(upload(c, &d_col, pat.col.data(), pat.col.size()));
+        RC_TRY(upload(c, &d_perm, pat.perm.data(), pat.perm.size()));
+        RC_TRY(upload(c, &d_val, val.data(), val.size()));
+        RC_TRY(upload(c, &d_dinv, dinv.data(), dinv.size()));
+        RC_TRY(upload(c, &d_sq, sq.data(), sq.size()));
+        RC_TRY(upload(c, &d_z, z, size_t(V) * size_t(n)));
+        RC_TRY(dalloc(c, &d_x, size_t(V) * size_t(n)));
+        RC_TRY(dalloc(c, &d_w, ens::gmrf_work_doubles(V, n)));
+        S.rp = d_rp;
+        S.col = d_col;
+        S.val = d_val;
+        S.dinv = d_dinv;
+        S.sqrtC = d_sq;
+        S.perm = d_perm;
+        // unit marginal variance: sigma^2 = Gamma(nu) / (Gamma(nu + d/2) (4 pi)^{d/2} kappa^{2 nu})
+        // = 1 / (4 pi kappa^2) for nu = 1, d = 2
+        const double scale = 1.0 / std::sqrt(1.0 / (4.0 * M_PI * kappa * kappa));
+        CUDA_TRY(c, ens::gmrf_pcg(S, n, d_z, d_x, scale, tol, max_iter, d_w, c->stream, iters, max_rel_res));
+        CUDA_TRY(c, cudaMemcpyAsync(x, d_x, size_t(V) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        return ENS_OK;
+    };
+    const int rc = body();
+    free_all(c);
     return rc;
 }
 

@@ -427,6 +427,40 @@ Fans build_fans(const MeshView& m, const std::vector<int32_t>& iperm, const std:
 }
 
 // ------------------------------------------------------------------------------------
+// SPDE/GMRF system (see host_setup.hpp).
+// ------------------------------------------------------------------------------------
+void gmrf_system(const MeshView& m, const Pattern& pat, double kappa, std::vector<double>& val,
+                 std::vector<double>& diag, std::vector<double>& lumped) {
+    const int64_t V = m.V;
+    val.assign(pat.col.size(), 0.0);
+    lumped.assign(size_t(V), 0.0);
+    for (int64_t e = 0; e < m.F; ++e) {
+        const int32_t* t = m.tris + 3 * e;
+        const double* X[3] = {m.xyz + 3 * int64_t(t[0]), m.xyz + 3 * int64_t(t[1]), m.xyz + 3 * int64_t(t[2])};
+        const double A = 0.5 * norm(cross(sub(X[1], X[0]), sub(X[2], X[0])));
+        const std::array<double, 3> ed[3] = {sub(X[2], X[1]), sub(X[0], X[2]), sub(X[1], X[0])};
+        for (int a = 0; a < 3; ++a) {
+            const int32_t i = pat.iperm[size_t(t[a])];
+            lumped[size_t(i)] += A / 3.0;
+            for (int b = 0; b < 3; ++b) {
+                const int32_t j = pat.iperm[size_t(t[b])];
+                auto first = pat.col.begin() + pat.row_ptr[size_t(i)];
+                auto last = pat.col.begin() + pat.row_ptr[size_t(i) + 1];
+                const int64_t k = int64_t(std::lower_bound(first, last, j) - pat.col.begin());
+                val[size_t(k)] += dot(ed[a], ed[b]) / (4.0 * A);
+            }
+        }
+    }
+    diag.assign(size_t(V), 0.0);
+    for (int64_t i = 0; i < V; ++i)
+        for (int64_t k = pat.row_ptr[size_t(i)]; k < pat.row_ptr[size_t(i) + 1]; ++k)
+            if (pat.col[size_t(k)] == i) {
+                val[size_t(k)] += kappa * kappa * lumped[size_t(i)];
+                diag[size_t(i)] = val[size_t(k)];
+            }
+}
+
+// ------------------------------------------------------------------------------------
 // Partition: bounds[p] = min { r : P row_ptr[r] >= p nnzb }.
 // ------------------------------------------------------------------------------------
 std::vector<int64_t> partition_bounds(const std::vector<int64_t>& row_ptr, int32_t P) {

@@ -54,6 +54,12 @@ void materials(const MeshView& m, int32_t n_s, const double* E, const double* h,
                double* alpha, double* mass);
 double cfl_dt(const MeshView& m, int32_t n_s, const double* E, double rho, double safety);
 
+// SPDE/GMRF system on the wall mesh (N3): scalar CSR values of A = kappa^2 C~ + G on the
+// pattern (RCM order), with C~ the lumped P1 mass and G_ab = e_a . e_b / (4 A_e)
+// (e_a the edge opposite vertex a; Eq. 5-6); diag(A) and C~ per row.
+void gmrf_system(const MeshView& m, const Pattern& pat, double kappa, std::vector<double>& val,
+                 std::vector<double>& diag, std::vector<double>& lumped);
+
 // Matrix-free operator arranged for the node-centric gather: for each
 // row i (RCM order) its incident elements as chains of a fan around i, so that consecutive
 // incidences (i, p_k, p_k+1), (i, p_k+1, p_k+2) share the node p_k+1.

@@ -74,6 +74,11 @@ class MaternSampler:
         return (X / self.sigma_spde).T                # [len(s_list)][V]
 
 
+def standard_normals(seed: int, field_id: int, s_list, V: int) -> np.ndarray:
+    """The counter-based z of realisations s_list: [len(s_list)][V]."""
+    return np.stack([_z(seed, field_id, s, V) for s in s_list])
+
+
 def _basis_weights(seed: int, field_id: int, s_list, K: int) -> np.ndarray:
     """Unit vectors w_s in R^K, one per realisation index, counter-based (seed, field, s)."""
     W = np.stack([_z(seed + 7919, field_id, s, K) for s in s_list])
@@ -83,21 +88,31 @@ def _basis_weights(seed: int, field_id: int, s_list, K: int) -> np.ndarray:
 def sample_materials(xyz: np.ndarray, tris: np.ndarray, n_s: int, *, E_mean: float,
                      E_std: float, h_mean: float, h_std: float, rho_corr: float,
                      seed: int, s_begin: int = 0, homogeneous_first: bool = True,
-                     basis: int | None = None):
+                     basis: int | None = None, device: bool = False):
     """Return (E[n_s][V], h[n_s][V], n_clipped) for realisations s_begin .. s_begin+n_s-1.
 
     basis = K (large configs c4/c5): draw K independent GMRF fields z_1..z_K per field type
     and give realisation s the field sum_k w_{s,k} z_k with w_s a unit vector keyed by
     (seed, field, s) — each realisation still has exactly the GMRF covariance Q^-1, at the
-    cost of correlation between realisations (stated in DESIGN.md "Inputs")."""
+    cost of correlation between realisations (stated in DESIGN.md "Inputs").
+    device = True solves on the GPU (ens_matern_fields) with the same z."""
     V = xyz.shape[0]
     E = np.empty((n_s, V))
     h = np.empty((n_s, V))
     s_idx = list(range(s_begin, s_begin + n_s))
     rand = [s for s in s_idx if not (homogeneous_first and s == 0)]
     if rand:
-        smp = MaternSampler(xyz, tris, rho_corr)
-        if basis:
+        smp = None if device else MaternSampler(xyz, tris, rho_corr)
+        if device:                                    # GPU Jacobi-PCG (ens_matern_fields), same z
+            from .. import solver
+            def draw(fid, idx):
+                return solver.matern_fields(xyz, tris, rho_corr, standard_normals(seed, fid, idx, V))[0]
+            if basis:
+                xe = _basis_weights(seed, FIELD_E, rand, basis) @ draw(FIELD_E, range(basis))
+                xh = _basis_weights(seed, FIELD_H, rand, basis) @ draw(FIELD_H, range(basis))
+            else:
+                xe, xh = draw(FIELD_E, rand), draw(FIELD_H, rand)
+        elif basis:
             be = smp.standard(seed, FIELD_E, range(basis))
             bh = smp.standard(seed, FIELD_H, range(basis))
             xe = _basis_weights(seed, FIELD_E, rand, basis) @ be

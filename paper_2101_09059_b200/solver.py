@@ -311,3 +311,15 @@ def nccl_comm_of(group=None, device=None) -> int:
     pg = group or dist.distributed_c10d._get_default_group()
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     return int(pg._get_backend(dev)._comm_ptr())
+
+
+def matern_fields(xyz, tris, rho_corr, z, tol=1e-13, max_iter=5000, device=None):
+    """GPU GMRF draws x[k] = A^-1 C~^{1/2} z[k] / sigma (ens_matern_fields); z [n][V]."""
+    xyz, tris, z = _c(xyz, np.float64), _c(tris, np.int32), _c(z, np.float64)
+    mesh = _ffi.EnsMesh(xyz.shape[0], tris.shape[0], _p(xyz), _p(tris), None)
+    opt, alloc = _options(0.0, 0.9, 0.0, 0, 0, 0, 0, 1, device, None, True)
+    x = np.empty_like(z)
+    it, res = C.c_int32(), C.c_double()
+    check(lib().ens_matern_fields(C.byref(mesh), float(rho_corr), z.shape[0], _p(z), _p(x), float(tol),
+                                  int(max_iter), C.byref(opt), C.byref(it), C.byref(res)))
+    return x, it.value, res.value

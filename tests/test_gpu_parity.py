@@ -406,3 +406,39 @@ def test_c2_hoop_stress_statistics_on_gpu():
     assert np.all(st["q05"][mid, 1] <= st["mean"][mid, 1]) and np.all(st["mean"][mid, 1] <= st["q95"][mid, 1])
     assert np.all(st["q95"][mid, 1] - st["q05"][mid, 1] > 0)
     ens.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_gpu_matern_sampler_matches_sparse_lu(name):
+    """ens_matern_fields (multi-RHS Jacobi-PCG on the GPU) reproduces the
+    host sampler's draws (scipy sparse LU of A = kappa^2 C~ + G, same z) to 1e-9."""
+    nc, na = {"c1": (12, 23), "c2": (96, 262)}[name]
+    m = meshmod.cylinder(nc, na)
+    smp = fields.MaternSampler(m.xyz, m.tris, 3.7)
+    ref = smp.standard(20210121, fields.FIELD_E, range(1, 17))
+    z = fields.standard_normals(20210121, fields.FIELD_E, range(1, 17), m.n_nodes)
+    x, iters, res = solver.matern_fields(m.xyz, m.tris, 3.7, z)
+    assert res <= 1e-13 and iters > 0
+    assert np.linalg.norm(x - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+def test_gpu_matern_correlation_follows_matern():
+    """Fig. 5: the empirical correlation of the generated field along the
+    cylinder follows the Matérn model r(d) = (kappa d) K_1(kappa d), kappa = sqrt(8)/rho
+    (nu = 1), in the interior of the 96 x 262 cylinder (4,096 draws)."""
+    from scipy.special import k1
+    m = meshmod.cylinder(96, 262)
+    z = fields.standard_normals(7, 0, range(4096), m.n_nodes)
+    x, _, _ = solver.matern_fields(m.xyz, m.tris, 3.7, z)
+    kappa = math.sqrt(8.0) / 3.7
+    nc = 96
+    base_rings = range(100, 160, 6)
+    for dr in (5, 10, 20, 32):                                  # axial ring offsets
+        d = 30.0 * dr / 261
+        cs = []
+        for r0 in base_rings:
+            a = x[:, r0 * nc:(r0 + 1) * nc]
+            b = x[:, (r0 + dr) * nc:(r0 + dr + 1) * nc]
+            cs.append(np.mean([np.corrcoef(a[:, k], b[:, k])[0, 1] for k in range(0, nc, 8)]))
+        model = kappa * d * k1(kappa * d)
+        assert np.mean(cs) == pytest.approx(model, abs=0.06), (d, np.mean(cs), model)
