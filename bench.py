@@ -102,6 +102,18 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def _max_over_ranks(x: float) -> float:
+    """Max of a host float over the ranks (NCCL: a CUDA tensor; gloo: a CPU tensor)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return x
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def _launch_count(n: int, G: int) -> int:
     """Kernels ens_step(n) enqueues: n fused steps + one counter advance per graph replay
     (G steps each) and one for the directly launched remainder."""
@@ -195,11 +207,10 @@ def _node_partition_run(args, cfg, base, m, tr, rank, world, local, stream, barr
     n1.synchronize()
     barrier()
     npar.sync()
-    t = torch.tensor([n0.elapsed_time(n1) / 1e3], device="cuda", dtype=torch.float64)
-    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    tmax = _max_over_ranks(n0.elapsed_time(n1) / 1e3)
     ninf = npar.info()
-    node = {"value": n_s * 3 * m.n_nodes * args.steps / float(t.item()), "unit": "DOF-updates/s",
-            "ms_per_step": 1e3 * float(t.item()) / args.steps, "scaling": "strong",
+    node = {"value": n_s * 3 * m.n_nodes * args.steps / tmax, "unit": "DOF-updates/s",
+            "ms_per_step": 1e3 * tmax / args.steps, "scaling": "strong",
             "n_s_total": n_s, "rows_rank0": ninf["n_owned"],
             "halo_bytes_per_step_rank0": ninf["halo_bytes_per_step"],
             "launches_per_step": ninf["launches_per_step"]}
@@ -249,10 +260,7 @@ def _time_kernel(kernel, args, cfg, m, tr, world, rank, local, stream, barrier, 
     barrier()
     ens.sync()
     el = e0.elapsed_time(e1) / 1e3
-    if world > 1:
-        t = torch.tensor([el], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        el = float(t.item())
+    el = _max_over_ranks(el)
     ens.close()
     ach = info["bytes_per_step"] / (el / args.steps) / 1e9
     return {"value": world * cfg.n_s * 3 * m.n_nodes * args.steps / el, "unit": "DOF-updates/s",
@@ -285,10 +293,17 @@ def main(argv=None):
     world, rank, local = _dist()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    # one process per GPU; ENS_BENCH_BACKEND=gloo lets several ranks share one device to
+    # exercise the multi-process plumbing on a single-GPU box (timings then meaningless)
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("ENS_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2101_09059_b200 import solver
     from paper_2101_09059_b200.inputs import configs
@@ -322,11 +337,7 @@ def main(argv=None):
     barrier()
     ens.sync()                                   # raises on divergence
     el = e0.elapsed_time(e1) / 1e3
-    el_max = el
-    if world > 1:
-        t = torch.tensor([el], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        el_max = float(t.item())
+    el_max = _max_over_ranks(el)
     dof_updates = world * n_s * 3 * m.n_nodes * args.steps
     value = dof_updates / el_max
     per_launch = el / args.steps
@@ -353,10 +364,7 @@ def main(argv=None):
         ens.step(win)
         ens.get_state(u_n=out, want_prev=False)
     e2e_el = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_el], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_el = float(t.item())
+    e2e_el = _max_over_ranks(e2e_el)
     e2e_value = world * n_s * 3 * m.n_nodes * win * args.e2e_windows / e2e_el
     h2d = Fp.numel() * 8 + tr.tab_t.size * 8 + tr.tab_g.size * 8
     d2h = out.numel() * 8
