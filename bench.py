@@ -134,8 +134,8 @@ def _cpu_baseline(cfg, budget_s: float = 12.0, max_steps: int = 40):
     """The oracle as it stands (oracle/oracle.c), timed on this host's cores on a bounded
     sample of the same workload: the same mesh and all N_s realisations, a few steps."""
     cores = len(os.sched_getaffinity(0))
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     import oracle
+    cores = oracle.set_threads(cores)        # torchrun exports OMP_NUM_THREADS=1: override
     m = cfg.mesh
     om = oracle.OracleModel(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=cfg.rho, nu=cfg.nu,
                             k_shear=cfg.k_shear, damping=cfg.damping, c_d=cfg.c_d)
@@ -148,7 +148,7 @@ def _cpu_baseline(cfg, budget_s: float = 12.0, max_steps: int = 40):
         n += 1
     el = time.perf_counter() - t0
     return {"value": cfg.n_s * 3 * m.n_nodes * n / el, "unit": "DOF-updates/s",
-            "cores": int(os.environ.get("OMP_NUM_THREADS", cores)), "kind": "oracle",
+            "cores": cores, "kind": "oracle",
             "sample": f"{cfg.name} mesh, all {cfg.n_s} realisations, {n} steps ({el:.1f} s)",
             "s_per_step": el / n}
 
@@ -161,9 +161,8 @@ def run_reference(args):
     cfg = configs.make(args.config, n_s=args.n_s)
     # each "step" of this arm is one oracle time step on the full workload (bounded: the
     # oracle steps a few hundred ms per step on 16 cores)
-    cores = len(os.sched_getaffinity(0))
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     import oracle
+    cores = oracle.set_threads(len(os.sched_getaffinity(0)))   # all host cores (torchrun sets 1)
     m = cfg.mesh
     om = oracle.OracleModel(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=cfg.rho, nu=cfg.nu,
                             k_shear=cfg.k_shear, damping=cfg.damping, c_d=cfg.c_d)
@@ -179,7 +178,7 @@ def run_reference(args):
             "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": _workload_desc(cfg, cfg.n_s, 1), "impl_detail": "oracle/oracle.c, OpenMP over realisations"},
-            "cpu_baseline": {"value": value, "unit": "DOF-updates/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
+            "cpu_baseline": {"value": value, "unit": "DOF-updates/s", "cores": cores,
                              "kind": "oracle", "sample": f"{cfg.name}, all {cfg.n_s} realisations, {args.steps} steps"},
             "e2e": {"value": value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

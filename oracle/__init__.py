@@ -60,6 +60,7 @@ def lib():
             "orc_partition_bounds": (None, [i64, vp, i32, vp]),
             "orc_stress": (None, [i64, i64, vp, vp, i32, vp, vp, f64, f64, i32, vp, i32, vp]),
             "orc_ghosts": (i64, [i64, vp, vp, i64, i64, vp]),
+            "orc_set_threads": (C.c_int, [C.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -67,6 +68,11 @@ def lib():
             fn.argtypes = args
         _lib = L
     return _lib
+
+
+def set_threads(n: int) -> int:
+    """OpenMP threads of the oracle's loops over realisations (results are independent)."""
+    return int(lib().orc_set_threads(int(n)))
 
 
 def _p(a: np.ndarray | None):

@@ -757,3 +757,18 @@ void orc_stress(int64_t V, int64_t F, const double* xyz, const int32_t* tris, in
         }
     }
 }
+
+/* Thread count of the OpenMP loops over realisations (timing only; results do not depend
+ * on it).  Returns the count in effect. */
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+int orc_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
+}
