@@ -61,6 +61,7 @@ def lib():
             "orc_stress": (None, [i64, i64, vp, vp, i32, vp, vp, f64, f64, i32, vp, i32, vp]),
             "orc_ghosts": (i64, [i64, vp, vp, i64, i64, vp]),
             "orc_set_threads": (C.c_int, [C.c_int]),
+            "orc_reassemble": (C.c_int, [i64, i64, vp, vp, vp, vp, f64, f64, i32, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -291,7 +292,30 @@ class OracleModel:
         self.tab_g = _c(np.asarray(tab_g).reshape(self.Fk.shape[0], len(self.tab_t)), np.float64)
         self.period, self.ramp_T = float(period), float(ramp_T)
 
-    def run(self, n: int) -> int:
+    def reassemble(self):
+        """Kval from the deformed geometry X + u_n (orc_reassemble)."""
+        rc = lib().orc_reassemble(self.V, self.F, _p(self.xyz), _p(self.tris), _p(self.row_ptr), _p(self.col),
+                                  self.nu, self.k_shear, self.n_s, _p(self.alpha), _p(self.u_n), _p(self.Kval))
+        assert rc == 0
+
+    def run(self, n: int, reassemble_every: int = 0) -> int:
+        """n steps; with reassemble_every = k > 0 the stiffness is rebuilt on X + u_m
+        before every step index m >= 1 with m % k == 0."""
+        if reassemble_every <= 0:
+            return self._run(n)
+        bad, done = -1, 0
+        while done < n:
+            m = self.step
+            if m > 0 and m % reassemble_every == 0:
+                self.reassemble()
+            nxt = (m // reassemble_every + 1) * reassemble_every
+            chunk = min(n - done, nxt - m)
+            b = self._run(chunk)
+            bad = b if bad < 0 else bad
+            done += chunk
+        return bad
+
+    def _run(self, n: int) -> int:
         bad = lib().orc_run(self.V, _p(self.row_ptr), _p(self.col), self.n_s, _p(self.Kval),
                             _p(self.c1), _p(self.c2), _p(self.c3), _p(self.fixed),
                             self.Fk.shape[0], _p(self.Fk), len(self.tab_t), _p(self.tab_t),

@@ -772,3 +772,41 @@ int orc_set_threads(int n) {
     return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* Selective stiffness re-assembly on the updated geometry (SURVEY.md §8(f) N4;         */
+/* "the geometry of the vessel lumen is updated at every step by adding    */
+/* u_{n+1} ... we provide the option to selectively update the stiffness matrix after a  */
+/* prescribed number of iterations").  Realisation s deforms on its own, so             */
+/*   Kval_s[i,j] = sum_{e, ascending} alpha_{e,s} K^_e(X + u_n^s)[a(i), b(j)]            */
+/* with K^_e(.) = orc_element_khat at the deformed node positions; alpha (material) and  */
+/* the lumped mass stay as built ("fixed nodal mass over time").            */
+/* ------------------------------------------------------------------------------------ */
+int orc_reassemble(int64_t V, int64_t F, const double* xyz, const int32_t* tris, const int64_t* row_ptr,
+                   const int32_t* col, double nu, double kshear, int32_t n_s, const double* alpha,
+                   const double* u_n, double* Kval) {
+    int64_t nnzb = row_ptr[V];
+    for (int32_t s = 0; s < n_s; s++) {
+        double* K = Kval + (int64_t)s * nnzb * 9;
+        const double* us = u_n + (int64_t)s * V * 3;
+        for (int64_t t = 0; t < nnzb * 9; t++) K[t] = 0.0;
+        for (int64_t e = 0; e < F; e++) {
+            double X[9], Kh[81], A;
+            for (int a = 0; a < 3; a++)
+                for (int c = 0; c < 3; c++) {
+                    int64_t node = tris[3 * e + a];
+                    X[3 * a + c] = xyz[3 * node + c] + us[3 * node + c];
+                }
+            orc_element_khat(X, nu, kshear, Kh, &A);
+            double al = alpha[(int64_t)s * F + e];
+            for (int a = 0; a < 3; a++)
+                for (int b = 0; b < 3; b++) {
+                    int64_t blk = find_block(row_ptr, col, tris[3 * e + a], tris[3 * e + b]);
+                    if (blk < 0) return -1;
+                    for (int c = 0; c < 3; c++)
+                        for (int d = 0; d < 3; d++) K[blk * 9 + 3 * c + d] += al * Kh[9 * (3 * a + c) + (3 * b + d)];
+                }
+        }
+    }
+    return 0;
+}
