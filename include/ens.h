@@ -110,6 +110,10 @@ typedef struct {
     void (*dev_free)(void* ptr, void* user);
     void* alloc_user;
     int32_t device;         /* CUDA device ordinal; < 0 => current device */
+    int32_t reassemble_every; /* k > 0: before every step index m >= 1 with m % k == 0 rebuild each
+                               realisation's stiffness on its deformed geometry X + u_m (
+                               assembled kernels only; mass and loads stay on the reference
+                               geometry); 0 = linear, K fixed */
 } ens_options;
 
 typedef struct ens_ctx ens_ctx;
@@ -126,6 +130,7 @@ typedef struct {
     int64_t n_owned;                    /* rows advanced by this context (V unless NODE with NCCL) */
     int64_t halo_bytes_per_step;        /* bytes sent + received by the halo exchange per step */
     int32_t launches_per_step;          /* kernels per time step (1 without a halo) */
+    int32_t reassemble_every;           /* ens_options.reassemble_every */
     int32_t graph_steps;                /* ens_step replays a CUDA graph of this many steps + 1 counter
                                            advance (env ENS_GRAPH_STEPS; 0 = direct launches) */
 } ens_info;

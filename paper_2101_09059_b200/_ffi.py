@@ -36,7 +36,7 @@ class EnsOptions(C.Structure):
                 ("damping", C.c_int32), ("kernel", C.c_int32), ("dist", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("nccl_comm", C.c_void_p),
                 ("stream", C.c_void_p), ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE),
-                ("alloc_user", C.c_void_p), ("device", C.c_int32)]
+                ("alloc_user", C.c_void_p), ("device", C.c_int32), ("reassemble_every", C.c_int32)]
 
 
 class EnsInfo(C.Structure):
@@ -46,7 +46,7 @@ class EnsInfo(C.Structure):
                 ("step", C.c_int64), ("bytes_per_step", C.c_int64), ("flops_per_step", C.c_int64),
                 ("device_bytes", C.c_int64), ("rcm_bandwidth", C.c_int32),
                 ("n_owned", C.c_int64), ("halo_bytes_per_step", C.c_int64),
-                ("launches_per_step", C.c_int32), ("graph_steps", C.c_int32)]
+                ("launches_per_step", C.c_int32), ("reassemble_every", C.c_int32), ("graph_steps", C.c_int32)]
 
 
 EXPORTS = [

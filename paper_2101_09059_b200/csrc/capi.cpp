@@ -19,6 +19,7 @@
 #include "nccl_dl.hpp"
 #include "gmrf.hpp"
 #include "observe.hpp"
+#include "reassemble.hpp"
 
 namespace {
 
@@ -47,6 +48,9 @@ struct Part {
     int32_t *d_sym_lptr = nullptr, *d_sym_lidx = nullptr, *d_sym_lcol = nullptr, *d_sym_scol = nullptr;
     int2* d_sym_urange = nullptr;
     int64_t n_stored = 0;                                  // value blocks held (assembled kernels)
+    // geometry-updated re-assembly (reassemble_every > 0): F0 inputs kept on the device
+    int32_t *d_rcp = nullptr, *d_rcc = nullptr, *d_retri = nullptr;
+    double *d_ral = nullptr, *d_rxyz = nullptr;
     double *d_scratch_u = nullptr, *d_scratch_y = nullptr;
     std::vector<int32_t> map_own;                          // host copy (ens_get_owned)
 };
@@ -86,6 +90,7 @@ struct ens_ctx {
 
     int64_t step = 0;
     bool latched = false;
+    int32_t reassemble_every = 0;
 
     // observation (stresses, statistics): host mesh copy, element E means, lazy operators
     std::vector<double> h_xyz;
@@ -100,6 +105,7 @@ struct ens_ctx {
     bool graph_dirty = true;
 
     bool has_halo() const { return parts.size() > 1 || nccl_comm != nullptr; }
+    bool use_graphs() const { return graph_steps > 0 && !has_halo() && reassemble_every == 0; }
 };
 
 namespace {
@@ -196,6 +202,10 @@ int check_opts(const ens_options* opt) {
     if (opt->kernel < 0 || opt->kernel > 2) return fail(nullptr, ENS_E_ARG, "opt->kernel must be 0, 1 or 2");
     if (!(opt->c_d >= 0.0) || !std::isfinite(opt->c_d)) return fail(nullptr, ENS_E_ARG, "opt->c_d must be finite and >= 0");
     if (opt->dist < 0 || opt->dist > 2) return fail(nullptr, ENS_E_ARG, "opt->dist must be 0, 1 or 2");
+    if (opt->reassemble_every < 0) return fail(nullptr, ENS_E_ARG, "opt->reassemble_every must be >= 0");
+    if (opt->reassemble_every > 0 && opt->kernel == ENS_KERNEL_MATRIX_FREE)
+        return fail(nullptr, ENS_E_UNSUPPORTED,
+                    "reassemble_every needs an assembled kernel (per-realisation geometry breaks the shared K^_e)");
     if (opt->dist == ENS_DIST_NODE) {
         if (opt->world < 1) return fail(nullptr, ENS_E_ARG, "opt->world must be >= 1");
         if (opt->nccl_comm && (opt->rank < 0 || opt->rank >= opt->world))
@@ -221,6 +231,7 @@ int init_ctx(ens_ctx* c, const ens_options* opt) {
     c->c_d = opt->c_d;
     c->rank = opt->rank;
     c->world = opt->world > 0 ? opt->world : 1;
+    c->reassemble_every = opt->reassemble_every;
     c->nccl_comm = opt->dist == ENS_DIST_NODE ? opt->nccl_comm : nullptr;
     if (c->nccl_comm) {
         std::string why;
@@ -291,6 +302,10 @@ cudaError_t launch_rows(const ens_ctx* c, ens::StepArgs a, int64_t row0, int64_t
 // ---- one time step of every part (step index = ctx step + k) ---------------------------
 int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
     const int64_t step = c->step + k;            // host mirror of *d_step + k
+    if (c->reassemble_every > 0 && step > 0 && step % c->reassemble_every == 0)
+        for (Part& p : c->parts)                 // K_s(X + u_step) for every realisation
+            CUDA_TRY(c, ens::launch_reassemble(p.n_stored, c->n_s, p.d_rcp, p.d_rcc, p.d_ral, p.d_retri, p.d_rxyz,
+                                               (step & 1) ? p.d_u1 : p.d_u0, c->nu, c->k_shear, p.d_Kval, st));
     if (!c->has_halo()) {
         ens::StepArgs a = part_args(c, c->parts[0]);
         a.step_off = k;
@@ -535,10 +550,25 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
         RC_TRY(dalloc(c, &P.d_Kval, blocks.size() * 9 * size_t(n_s)));
         CUDA_TRY(c, ens::launch_assemble(int64_t(blocks.size()), c->n_s, d_cp, d_cc, d_al, d_kh, P.d_Kval, c->stream));
         CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-        dfree(c, d_cp);
-        dfree(c, d_cc);
-        dfree(c, d_al);
         dfree(c, d_kh);
+        if (c->reassemble_every > 0) {          // keep what the geometry-updated rebuild needs
+            std::vector<int32_t> et(size_t(Fl) * 3);
+            for (int64_t k = 0; k < Fl; ++k)
+                for (int a = 0; a < 3; ++a)
+                    et[size_t(3 * k + a)] = local(pat.iperm[size_t(G.m->tris[3 * int64_t(elems[size_t(k)]) + a])]);
+            std::vector<double> xl(size_t(n_loc) * 3);
+            for (int64_t r = 0; r < n_loc; ++r)
+                for (int d = 0; d < 3; ++d) xl[size_t(3 * r + d)] = G.m->xyz[3 * int64_t(map_all[size_t(r)]) + d];
+            RC_TRY(upload(c, &P.d_retri, et.data(), et.size()));
+            RC_TRY(upload(c, &P.d_rxyz, xl.data(), xl.size()));
+            P.d_rcp = d_cp;
+            P.d_rcc = d_cc;
+            P.d_ral = d_al;
+        } else {
+            dfree(c, d_cp);
+            dfree(c, d_cc);
+            dfree(c, d_al);
+        }
     } else {
         const ens::Fans& fans = *G.fans;
         const int32_t k0 = fans.ptr[size_t(lo)], k1 = fans.ptr[size_t(hi)];
@@ -755,6 +785,7 @@ int ens_create_csr(int64_t n_nodes, const int64_t* row_ptr, const int32_t* col, 
         RC_TRY(init_ctx(c, opt));
         c->kernel = ENS_KERNEL_ASSEMBLED;
         c->damping = ENS_DAMP_IDENTITY;      // arbitrary per-DOF c2, c3 arrays
+        c->reassemble_every = 0;             // no geometry behind a synthetic operator
         c->V = V;
         c->F = 0;
         c->nnzb = nnzb;
@@ -852,7 +883,7 @@ int ens_step(ens_ctx* c, int64_t n) {
     if (n < 0) return fail(c, ENS_E_ARG, "n must be >= 0");
     if (c->latched) return fail(c, ENS_E_STATE, "context diverged: call ens_set_state before stepping again");
     int64_t left = n;
-    if (c->graph_steps > 0 && n >= c->graph_steps && !c->has_halo()) {
+    if (c->use_graphs() && n >= c->graph_steps) {
         if (c->graph_dirty) RC_TRY(build_graph(c));
         for (; left >= c->graph_steps; left -= c->graph_steps) {
             CUDA_TRY(c, cudaGraphLaunch(c->graph, c->stream));
@@ -1152,7 +1183,8 @@ int ens_query(const ens_ctx* c, ens_info* info) {
     info->step = c->step;
     info->device_bytes = c->device_bytes;
     info->rcm_bandwidth = c->bandwidth;
-    info->graph_steps = c->has_halo() ? 0 : c->graph_steps;
+    info->graph_steps = c->use_graphs() ? c->graph_steps : 0;
+    info->reassemble_every = c->reassemble_every;
     // algorithmic HBM bytes of the rows this context advances: values +
     // u_n, u_{n-1} read, u_{n+1} written, c1 (+ c2, c3) per node per realisation
     const int64_t ns = c->n_s, per_node = 3 * 8 * 3 + 8 + (c->damping == ENS_DAMP_IDENTITY ? 16 : 0);

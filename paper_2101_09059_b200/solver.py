@@ -59,7 +59,7 @@ class Ensemble:
     def __init__(self, xyz, tris, fixed, E, h, *, rho, nu, k_shear=5.0 / 6.0, dt=0.0,
                  cfl_safety=0.9, c_d=0.0, damping="none", kernel="assembled", dist="single",
                  s_begin=0, rank=0, world=1, nccl_comm=None, device=None, stream=None,
-                 torch_alloc=True, _ctx=None):
+                 torch_alloc=True, reassemble_every=0, _ctx=None):
         self._ctx = None
         self._alloc = None
         if _ctx is not None:                      # from_csr
@@ -75,6 +75,7 @@ class Ensemble:
                                     device, stream, torch_alloc)
         if nccl_comm is not None:
             opt.nccl_comm = C.c_void_p(int(nccl_comm))
+        opt.reassemble_every = int(reassemble_every)
         ctx = C.c_void_p()
         check(lib().ens_create(C.byref(mesh), C.byref(mat), C.byref(opt), C.byref(ctx)))
         self._ctx = ctx

@@ -442,3 +442,40 @@ def test_gpu_matern_correlation_follows_matern():
             cs.append(np.mean([np.corrcoef(a[:, k], b[:, k])[0, 1] for k in range(0, nc, 8)]))
         model = kappa * d * k1(kappa * d)
         assert np.mean(cs) == pytest.approx(model, abs=0.06), (d, np.mean(cs), model)
+
+
+@pytest.mark.parametrize("kernel", ["assembled", "assembled_sym"])
+def test_geometry_reassembly_parity(kernel):
+    """reassemble_every = k: every k steps each
+    realisation's stiffness is rebuilt on X + u; a large pressure makes the geometric
+    update visible.  GPU vs oracle <= 1e-9; full vs half storage bit-identical."""
+    m = meshmod.shuffle_nodes(meshmod.cylinder(16, 25), 6)
+    E, h = _mats(m, 4, 91)
+    tr = loads.steady(m.xyz, m.tris, p=40 * loads.P_SUPERPOSED)
+    dt, k, n = 1e-4, 25, 400
+    outs = {}
+    for kern in ("assembled", kernel):
+        ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, kernel=kern, dt=dt,
+                              damping="mass", c_d=100.0, reassemble_every=k)
+        assert ens.info()["reassemble_every"] == k and ens.info()["graph_steps"] == 0
+        ens.set_traction(tr.F)
+        ens.step(n)
+        outs[kern] = ens.get_state()[0]
+        ens.close()
+    assert np.array_equal(outs["assembled"], outs[kernel])
+    om = oracle.OracleModel(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, damping=1, c_d=100.0, dt=dt)
+    om.set_traction(tr.F, tr.tab_t, tr.tab_g, 0.0, 0.0)
+    om.run(n, reassemble_every=k)
+    assert np.linalg.norm(outs[kernel] - om.u_n) <= 1e-9 * np.linalg.norm(om.u_n)
+    lin = oracle.OracleModel(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, damping=1, c_d=100.0, dt=dt)
+    lin.set_traction(tr.F, tr.tab_t, tr.tab_g, 0.0, 0.0)
+    lin.run(n)
+    assert np.linalg.norm(om.u_n - lin.u_n) > 1e-6 * np.linalg.norm(lin.u_n)    # the update matters
+
+
+def test_reassembly_rejected_for_matrix_free():
+    m = meshmod.cylinder(8, 5)
+    E, h = _mats(m, 2, 1)
+    with pytest.raises(EnsError):
+        solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, kernel="matrix_free",
+                        reassemble_every=10)
