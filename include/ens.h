@@ -84,6 +84,7 @@ typedef struct {
 enum { ENS_DAMP_NONE = 0, ENS_DAMP_MASS = 1, ENS_DAMP_IDENTITY = 2 };
 enum { ENS_KERNEL_ASSEMBLED = 0, ENS_KERNEL_MATRIX_FREE = 1, ENS_KERNEL_ASSEMBLED_SYM = 2 };
 enum { ENS_DIST_SINGLE = 0, ENS_DIST_NODE = 1, ENS_DIST_ENSEMBLE = 2 };
+enum { ENS_HALO_NCCL = 0, ENS_HALO_P2P = 1 };
 
 typedef struct {
     double dt;              /* time step, s; <= 0 => cfl_safety * l_min / sqrt(E_max / rho) */
@@ -114,6 +115,18 @@ typedef struct {
                                realisation's stiffness on its deformed geometry X + u_m (
                                assembled kernels only; mass and loads stay on the reference
                                geometry); 0 = linear, K fixed */
+    int32_t halo;           /* dist == NODE: how the interface rows travel (SURVEY.md
+                               §8(f) N2).  ENS_HALO_NCCL: boundary rows, send-pack, NCCL send/recv on
+                               a comm stream (or device copies when this context holds every part).
+                               ENS_HALO_P2P: the boundary-row kernel stores each u_{n+1} send row
+                               straight into the neighbours' ghost rows (peer memory over NVLink /
+                               the same device), then a one-thread kernel publishes a per-neighbour
+                               step counter (st.release.sys) that the neighbour's next step waits for
+                               (ld.acquire.sys); no pack, no NCCL, and the step loop is captured in
+                               CUDA graphs.  With p2p_procs == 0 this context holds all `world` parts;
+                               with p2p_procs == 1 it holds part `rank` and must be connected to the
+                               other ranks with ens_p2p_export / ens_p2p_connect before ens_step. */
+    int32_t p2p_procs;      /* halo == P2P: 1 = one part per process (CUDA IPC), 0 = all parts here */
 } ens_options;
 
 typedef struct ens_ctx ens_ctx;
@@ -133,6 +146,7 @@ typedef struct {
     int32_t reassemble_every;           /* ens_options.reassemble_every */
     int32_t graph_steps;                /* ens_step replays a CUDA graph of this many steps + 1 counter
                                            advance (env ENS_GRAPH_STEPS; 0 = direct launches) */
+    int32_t halo;                       /* ens_options.halo (NODE contexts) */
 } ens_info;
 
 /* Create a context: validate the mesh, build the RCM-ordered block-CSR pattern, the
@@ -211,6 +225,24 @@ int ens_displacement_stats(ens_ctx* ctx, double* mean, double* q05, double* q95)
  * device, stream and allocator (may be NULL).  Synchronous. */
 int ens_matern_fields(const ens_mesh* mesh, double rho_corr, int32_t n, const double* z, double* x, double tol,
                       int32_t max_iter, const ens_options* opt, int32_t* iters, double* max_rel_res);
+
+/* ---- ENS_HALO_P2P with one part per process (opt.p2p_procs = 1) ---------------------
+ * ens_create allocates this part's state buffers and its neighbour flags with cudaMalloc
+ * (IPC-exportable) and zeroes them.  ens_p2p_export writes ENS_P2P_BLOB_BYTES describing
+ * them (CUDA IPC handles of u buffer 0, u buffer 1 and the flags, plus rank / world / row
+ * counts) into blob.  The caller all-gathers the blobs of every rank over any host
+ * channel (the Python binding uses torch.distributed) and passes the concatenation
+ * blobs[world][ENS_P2P_BLOB_BYTES] to ens_p2p_connect, which opens the neighbours' buffers
+ * (cudaIpcOpenMemHandle; peer access over NVLink when the devices differ) and checks their
+ * sizes.  Collective: no rank may step before every rank has connected (the all-gather
+ * orders this), and ens_set_state must be followed by a barrier before the next ens_step.
+ * Errors: ENS_E_STATE (not such a context / already connected), ENS_E_ARG (blob of a
+ * different world, rank or size), ENS_E_CUDA (IPC failure).  A neighbour that stops
+ * stepping makes the waiting rank's flag wait time out after ~10 s; the next synchronising
+ * call then returns ENS_E_CUDA naming the step and the neighbour. */
+#define ENS_P2P_BLOB_BYTES 256
+int ens_p2p_export(const ens_ctx* ctx, void* blob);
+int ens_p2p_connect(ens_ctx* ctx, const void* blobs);
 
 /* Sizes, dt and algorithmic traffic of the context. */
 int ens_query(const ens_ctx* ctx, ens_info* info);

@@ -36,7 +36,8 @@ class EnsOptions(C.Structure):
                 ("damping", C.c_int32), ("kernel", C.c_int32), ("dist", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("nccl_comm", C.c_void_p),
                 ("stream", C.c_void_p), ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE),
-                ("alloc_user", C.c_void_p), ("device", C.c_int32), ("reassemble_every", C.c_int32)]
+                ("alloc_user", C.c_void_p), ("device", C.c_int32), ("reassemble_every", C.c_int32),
+                ("halo", C.c_int32), ("p2p_procs", C.c_int32)]
 
 
 class EnsInfo(C.Structure):
@@ -46,7 +47,8 @@ class EnsInfo(C.Structure):
                 ("step", C.c_int64), ("bytes_per_step", C.c_int64), ("flops_per_step", C.c_int64),
                 ("device_bytes", C.c_int64), ("rcm_bandwidth", C.c_int32),
                 ("n_owned", C.c_int64), ("halo_bytes_per_step", C.c_int64),
-                ("launches_per_step", C.c_int32), ("reassemble_every", C.c_int32), ("graph_steps", C.c_int32)]
+                ("launches_per_step", C.c_int32), ("reassemble_every", C.c_int32), ("graph_steps", C.c_int32),
+                ("halo", C.c_int32)]
 
 
 EXPORTS = [
@@ -54,8 +56,9 @@ EXPORTS = [
     "ens_apply_stiffness", "ens_query", "ens_destroy", "ens_last_error", "ens_host_validate",
     "ens_host_pattern", "ens_host_partition", "ens_host_ghosts", "ens_host_element_stiffness",
     "ens_host_materials", "ens_create_csr", "ens_get_owned", "ens_host_halo_plan", "ens_stress",
-    "ens_displacement_stats", "ens_matern_fields",
+    "ens_displacement_stats", "ens_matern_fields", "ens_p2p_export", "ens_p2p_connect",
 ]
+P2P_BLOB_BYTES = 256
 
 _lib = None
 
@@ -102,6 +105,8 @@ def lib():
         "ens_displacement_stats": (C.c_int, [vp, vp, vp, vp]),
         "ens_matern_fields": (C.c_int, [P(EnsMesh), f64, i32, vp, vp, f64, i32, P(EnsOptions), P(i32), P(f64)]),
         "ens_host_halo_plan": (C.c_int, [i64, vp, vp, i32, i32, vp, vp, vp, vp, i64, P(i64), P(i64)]),
+        "ens_p2p_export": (C.c_int, [vp, vp]),
+        "ens_p2p_connect": (C.c_int, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -53,6 +53,16 @@ struct Part {
     double *d_ral = nullptr, *d_rxyz = nullptr;
     double *d_scratch_u = nullptr, *d_scratch_y = nullptr;
     std::vector<int32_t> map_own;                          // host copy (ens_get_owned)
+    // P2P halo (ENS_HALO_P2P): forward lists, neighbour tables, own flags
+    unsigned long long* d_hflags = nullptr;                // [world]: step published by neighbour q
+    int32_t* d_fwd_ptr = nullptr;                          // [n_own + 1]
+    int2* d_fwd_dst = nullptr;                             // {slot, peer local row}
+    double** d_peer_buf = nullptr;                         // [2 n_out]
+    unsigned long long** d_out_flag = nullptr;             // [n_out]: &flags_q[p] of neighbour q
+    int32_t* d_in_q = nullptr;                             // [n_in] neighbours this part waits for
+    int32_t n_out = 0, n_in = 0;
+    std::vector<int32_t> out_q;                            // neighbour rank of each slot
+    std::vector<int64_t> out_rows;                         // its local row count (owned + ghosts)
 };
 
 }  // namespace
@@ -77,9 +87,15 @@ struct ens_ctx {
     int32_t bandwidth = 0;
     std::vector<int32_t> perm, iperm;       // perm[new] = old (global)
 
-    std::vector<Part> parts;                // 1 (single / ensemble / NCCL rank) or world (emulation)
+    std::vector<Part> parts;                // 1 (single / ensemble / one rank) or world (emulation)
     const ens::Nccl* nccl = nullptr;
     void* nccl_comm = nullptr;
+    int32_t halo = ENS_HALO_NCCL;
+    bool multi = false;                     // this process holds one part of `world` (NCCL or IPC)
+    bool p2p_connected = true;              // IPC peers opened (ens_p2p_connect)
+    unsigned long long* d_herr = nullptr;   // P2P wait timeout: step << 16 | neighbour
+    std::vector<void*> raw_bufs;            // cudaMalloc'd (IPC-exported) buffers
+    std::vector<void*> ipc_opened;          // neighbours' buffers opened by ens_p2p_connect
 
     double* d_stage = nullptr;              // [n_s][V][3] ABI staging
     unsigned long long* d_flag = nullptr;
@@ -104,8 +120,9 @@ struct ens_ctx {
     cudaGraphExec_t graph = nullptr;
     bool graph_dirty = true;
 
-    bool has_halo() const { return parts.size() > 1 || nccl_comm != nullptr; }
-    bool use_graphs() const { return graph_steps > 0 && !has_halo() && reassemble_every == 0; }
+    bool has_halo() const { return parts.size() > 1 || multi; }
+    bool p2p() const { return has_halo() && halo == ENS_HALO_P2P; }
+    bool use_graphs() const { return graph_steps > 0 && (!has_halo() || p2p()) && reassemble_every == 0; }
 };
 
 namespace {
@@ -152,6 +169,19 @@ int dalloc(ens_ctx* c, T** out, size_t count) {
 }
 
 template <typename T>
+int rawalloc(ens_ctx* c, T** out, size_t count) {
+    *out = nullptr;
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc (IPC-exported buffer)");
+    c->raw_bufs.push_back(p);
+    c->device_bytes += int64_t(bytes);
+    *out = static_cast<T*>(p);
+    return ENS_OK;
+}
+
+template <typename T>
 void dfree(ens_ctx* c, T*& p) {
     if (!p) return;
     for (size_t k = 0; k < c->bufs.size(); ++k)
@@ -182,6 +212,10 @@ void drop_graph(ens_ctx* c) {
 void free_all(ens_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     drop_graph(c);
+    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+    c->ipc_opened.clear();
+    for (void* p : c->raw_bufs) cudaFree(p);
+    c->raw_bufs.clear();
     for (auto& b : c->bufs) {
         if (c->dev_free) c->dev_free(b.p, c->alloc_user);
         else cudaFreeAsync(b.p, c->stream);
@@ -206,9 +240,14 @@ int check_opts(const ens_options* opt) {
     if (opt->reassemble_every > 0 && opt->kernel == ENS_KERNEL_MATRIX_FREE)
         return fail(nullptr, ENS_E_UNSUPPORTED,
                     "reassemble_every needs an assembled kernel (per-realisation geometry breaks the shared K^_e)");
+    if (opt->halo < 0 || opt->halo > 1) return fail(nullptr, ENS_E_ARG, "opt->halo must be 0 (NCCL) or 1 (P2P)");
+    if (opt->p2p_procs && (opt->halo != ENS_HALO_P2P || opt->dist != ENS_DIST_NODE))
+        return fail(nullptr, ENS_E_ARG, "opt->p2p_procs needs dist = NODE and halo = P2P");
+    if (opt->halo == ENS_HALO_P2P && opt->nccl_comm)
+        return fail(nullptr, ENS_E_ARG, "opt->halo = P2P takes no nccl_comm");
     if (opt->dist == ENS_DIST_NODE) {
         if (opt->world < 1) return fail(nullptr, ENS_E_ARG, "opt->world must be >= 1");
-        if (opt->nccl_comm && (opt->rank < 0 || opt->rank >= opt->world))
+        if ((opt->nccl_comm || opt->p2p_procs) && (opt->rank < 0 || opt->rank >= opt->world))
             return fail(nullptr, ENS_E_ARG, "opt->rank must lie in [0, world)");
     }
     return ENS_OK;
@@ -233,6 +272,9 @@ int init_ctx(ens_ctx* c, const ens_options* opt) {
     c->world = opt->world > 0 ? opt->world : 1;
     c->reassemble_every = opt->reassemble_every;
     c->nccl_comm = opt->dist == ENS_DIST_NODE ? opt->nccl_comm : nullptr;
+    c->halo = opt->dist == ENS_DIST_NODE ? opt->halo : ENS_HALO_NCCL;
+    c->multi = c->nccl_comm != nullptr || (c->halo == ENS_HALO_P2P && opt->p2p_procs != 0 && c->world > 1);
+    c->p2p_connected = !(c->multi && c->halo == ENS_HALO_P2P);
     if (c->nccl_comm) {
         std::string why;
         c->nccl = ens::nccl_load(&why);
@@ -300,12 +342,44 @@ cudaError_t launch_rows(const ens_ctx* c, ens::StepArgs a, int64_t row0, int64_t
 }
 
 // ---- one time step of every part (step index = ctx step + k) ---------------------------
+int reassemble_if_due(ens_ctx* c, Part& p, int64_t step, cudaStream_t st) {
+    if (c->reassemble_every > 0 && step > 0 && step % c->reassemble_every == 0)   // K_s(X + u_step)
+        CUDA_TRY(c, ens::launch_reassemble(p.n_stored, c->n_s, p.d_rcp, p.d_rcc, p.d_ral, p.d_retri, p.d_rxyz,
+                                           (step & 1) ? p.d_u1 : p.d_u0, c->nu, c->k_shear, p.d_Kval, st));
+    return ENS_OK;
+}
+
+// P2P halo step (ENS_HALO_P2P): per part, wait for the neighbours' u_n ghost
+// rows (their flags >= step), boundary rows with u_{n+1} forwarded into the neighbours'
+// ghost rows of buffer (step + 1) & 1, publish step + 1; then every part's interior rows.
+// Neighbours only ever write ghost rows of the buffer this part is not reading, and only
+// after it published the step before, so two buffers suffice (no acknowledgement needed).
+int enqueue_step_p2p(ens_ctx* c, int64_t k, cudaStream_t st) {
+    const int64_t step = c->step + k;
+    for (Part& p : c->parts) {
+        CUDA_TRY(c, ens::launch_halo_wait(p.n_in, p.d_in_q, p.d_hflags, c->d_step, k, c->d_herr, st));
+        RC_TRY(reassemble_if_due(c, p, step, st));
+        ens::StepArgs a = part_args(c, p);
+        a.step_off = k;
+        a.fwd_ptr = p.d_fwd_ptr;
+        a.fwd_dst = p.d_fwd_dst;
+        a.peer_buf = p.d_peer_buf;
+        CUDA_TRY(c, launch_rows(c, a, 0, p.plan.b_lo, st));
+        CUDA_TRY(c, launch_rows(c, a, p.n_own - p.plan.b_hi, p.plan.b_hi, st));
+        CUDA_TRY(c, ens::launch_halo_signal(p.n_out, p.d_out_flag, c->d_step, k, st));
+    }
+    for (Part& p : c->parts) {
+        ens::StepArgs a = part_args(c, p);
+        a.step_off = k;
+        CUDA_TRY(c, launch_rows(c, a, p.plan.b_lo, p.n_own - p.plan.b_lo - p.plan.b_hi, st));
+    }
+    return ENS_OK;
+}
+
 int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
     const int64_t step = c->step + k;            // host mirror of *d_step + k
-    if (c->reassemble_every > 0 && step > 0 && step % c->reassemble_every == 0)
-        for (Part& p : c->parts)                 // K_s(X + u_step) for every realisation
-            CUDA_TRY(c, ens::launch_reassemble(p.n_stored, c->n_s, p.d_rcp, p.d_rcc, p.d_ral, p.d_retri, p.d_rxyz,
-                                               (step & 1) ? p.d_u1 : p.d_u0, c->nu, c->k_shear, p.d_Kval, st));
+    if (c->p2p()) return enqueue_step_p2p(c, k, st);
+    for (Part& p : c->parts) RC_TRY(reassemble_if_due(c, p, step, st));
     if (!c->has_halo()) {
         ens::StepArgs a = part_args(c, c->parts[0]);
         a.step_off = k;
@@ -444,7 +518,7 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
     RC_TRY(upload(c, &P.d_col, cl.data(), cl.size()));
     RC_TRY(upload(c, &P.d_map_own, map_all.data(), size_t(P.n_own)));
     RC_TRY(upload(c, &P.d_map_all, map_all.data(), map_all.size()));
-    if (c->nccl_comm) {        // one part per process: owned rows in local order (ens_get_owned)
+    if (c->multi) {            // one part per process: owned rows in local order (ens_get_owned)
         std::vector<int32_t> ident(size_t(P.n_own));
         for (int64_t i = 0; i < P.n_own; ++i) ident[size_t(i)] = int32_t(i);
         RC_TRY(upload(c, &P.d_map_abi, ident.data(), ident.size()));
@@ -457,7 +531,7 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
         RC_TRY(upload(c, &P.d_c2a, c2a.data(), c2a.size()));
         RC_TRY(upload(c, &P.d_c3a, c3a.data(), c3a.size()));
     }
-    if (!pl.send_rows.empty()) {
+    if (!pl.send_rows.empty() && !c->p2p()) {
         RC_TRY(upload(c, &P.d_send_rows, pl.send_rows.data(), pl.send_rows.size()));
         RC_TRY(dalloc(c, &P.d_sendbuf, pl.send_rows.size() * 3 * size_t(n_s)));
     }
@@ -602,18 +676,89 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
         RC_TRY(upload(c, &P.d_alpha, al.data(), al.size()));
     }
     const size_t ns = size_t(n_loc) * 3 * size_t(n_s);
-    RC_TRY(dalloc(c, &P.d_u0, ns));
-    RC_TRY(dalloc(c, &P.d_u1, ns));
+    if (c->multi && c->p2p()) {      // exported to the neighbours: plain cudaMalloc (IPC)
+        RC_TRY(rawalloc(c, &P.d_u0, ns));
+        RC_TRY(rawalloc(c, &P.d_u1, ns));
+    } else {
+        RC_TRY(dalloc(c, &P.d_u0, ns));
+        RC_TRY(dalloc(c, &P.d_u1, ns));
+    }
     CUDA_TRY(c, cudaMemsetAsync(P.d_u0, 0, ns * sizeof(double), c->stream));
     CUDA_TRY(c, cudaMemsetAsync(P.d_u1, 0, ns * sizeof(double), c->stream));
+    return ENS_OK;
+}
+
+// P2P halo tables of part P (rank p) from every part's plan: send row send_rows[off + j]
+// to neighbour q lands in q's local row recv_row(q <- p) + j (q's ghosts are sorted, and
+// those owned by p are contiguous there); q's flags[p] is where p publishes its steps.
+int build_p2p(ens_ctx* c, Part& P, const std::vector<ens::PartPlan>& plans) {
+    const auto& pl = P.plan;
+    const int32_t p = pl.p;
+    std::vector<std::vector<int2>> dst(static_cast<size_t>(P.n_own));
+    std::vector<int32_t> in_q;
+    for (const auto& pe : pl.peers) {
+        if (pe.recv_n) in_q.push_back(pe.q);
+        if (!pe.send_n) continue;
+        const ens::PartPlan& Q = plans[size_t(pe.q)];
+        const auto it = std::find_if(Q.peers.begin(), Q.peers.end(), [&](const ens::PartPlan::Peer& x) { return x.q == p; });
+        if (it == Q.peers.end() || it->recv_n != pe.send_n)
+            return fail(c, ENS_E_ARG, "P2P halo: inconsistent plans of parts " + std::to_string(p) + " and " +
+                                          std::to_string(pe.q));
+        const int32_t slot = int32_t(P.out_q.size());
+        P.out_q.push_back(pe.q);
+        P.out_rows.push_back(Q.n_own() + int64_t(Q.ghosts.size()));
+        for (int64_t j = 0; j < pe.send_n; ++j)
+            dst[size_t(pl.send_rows[size_t(pe.send_off + j)])].push_back(make_int2(slot, int32_t(it->recv_row + j)));
+    }
+    std::vector<int32_t> fptr(size_t(P.n_own) + 1, 0);
+    std::vector<int2> fdst;
+    for (int64_t i = 0; i < P.n_own; ++i) {
+        for (const int2& d : dst[size_t(i)]) fdst.push_back(d);
+        fptr[size_t(i) + 1] = int32_t(fdst.size());
+    }
+    P.n_out = int32_t(P.out_q.size());
+    P.n_in = int32_t(in_q.size());
+    RC_TRY(upload(c, &P.d_fwd_ptr, fptr.data(), fptr.size()));
+    RC_TRY(upload(c, &P.d_fwd_dst, fdst.data(), fdst.size()));
+    RC_TRY(upload(c, &P.d_in_q, in_q.data(), in_q.size()));
+    RC_TRY(dalloc(c, &P.d_peer_buf, size_t(2 * P.n_out)));
+    RC_TRY(dalloc(c, &P.d_out_flag, size_t(P.n_out)));
+    const size_t nf = size_t(c->world);
+    if (c->multi) RC_TRY(rawalloc(c, &P.d_hflags, nf));
+    else RC_TRY(dalloc(c, &P.d_hflags, nf));
+    CUDA_TRY(c, cudaMemsetAsync(P.d_hflags, 0, nf * sizeof(unsigned long long), c->stream));
+    return ENS_OK;
+}
+
+// emulation (all parts here): the neighbours' tables are this context's own parts
+int link_p2p_local(ens_ctx* c) {
+    for (Part& P : c->parts) {
+        std::vector<double*> pb;
+        std::vector<unsigned long long*> of;
+        for (int32_t q : P.out_q) {
+            Part& Q = c->parts[size_t(q)];
+            pb.push_back(Q.d_u0);
+            pb.push_back(Q.d_u1);
+            of.push_back(Q.d_hflags + P.plan.p);
+        }
+        if (!pb.empty()) {
+            CUDA_TRY(c, cudaMemcpyAsync(P.d_peer_buf, pb.data(), pb.size() * sizeof(double*), cudaMemcpyHostToDevice,
+                                        c->stream));
+            CUDA_TRY(c, cudaMemcpyAsync(P.d_out_flag, of.data(), of.size() * sizeof(void*), cudaMemcpyHostToDevice,
+                                        c->stream));
+        }
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return ENS_OK;
 }
 
 int finish_create(ens_ctx* c) {
     RC_TRY(dalloc(c, &c->d_stage, size_t(c->V) * 3 * size_t(c->n_s)));
     RC_TRY(dalloc(c, &c->d_flag, 1));
+    RC_TRY(dalloc(c, &c->d_herr, 1));
     RC_TRY(dalloc(c, &c->d_step, 1));
     CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0xff, sizeof(unsigned long long), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->d_herr, 0xff, sizeof(unsigned long long), c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->d_step, 0, sizeof(int64_t), c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->step = 0;
@@ -688,7 +833,7 @@ int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, cons
         plans[0].hi = V;
     }
     Global G{&m, &pat, &Khat, &alpha, &mass, mesh->fixed, &fans, &cptr, &contrib};
-    if (c->nccl_comm && P > 1) {
+    if (c->multi && P > 1) {
         c->parts.resize(1);
         c->parts[0].plan = plans[size_t(c->rank)];
     } else {
@@ -696,6 +841,10 @@ int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, cons
         for (size_t k = 0; k < plans.size(); ++k) c->parts[k].plan = plans[k];
     }
     for (Part& p : c->parts) RC_TRY(build_part(c, p, G));
+    if (c->p2p()) {
+        for (Part& p : c->parts) RC_TRY(build_p2p(c, p, plans));
+        if (!c->multi) RC_TRY(link_p2p_local(c));
+    }
     // element means of E per realisation (stress recovery, ens_stress)
     c->h_xyz.assign(mesh->xyz, mesh->xyz + 3 * V);
     c->h_tris.assign(mesh->tris, mesh->tris + 3 * F);
@@ -882,6 +1031,7 @@ int ens_step(ens_ctx* c, int64_t n) {
     if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
     if (n < 0) return fail(c, ENS_E_ARG, "n must be >= 0");
     if (c->latched) return fail(c, ENS_E_STATE, "context diverged: call ens_set_state before stepping again");
+    if (!c->p2p_connected) return fail(c, ENS_E_STATE, "P2P halo: call ens_p2p_connect before ens_step");
     int64_t left = n;
     if (c->use_graphs() && n >= c->graph_steps) {
         if (c->graph_dirty) RC_TRY(build_graph(c));
@@ -900,7 +1050,13 @@ int ens_sync(ens_ctx* c) {
     if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (c->comm_stream) CUDA_TRY(c, cudaStreamSynchronize(c->comm_stream));
-    unsigned long long flag = 0;
+    unsigned long long flag = 0, herr = ~0ull;
+    CUDA_TRY(c, cudaMemcpy(&herr, c->d_herr, sizeof(herr), cudaMemcpyDeviceToHost));
+    if (herr != ~0ull) {
+        c->latched = true;
+        return fail(c, ENS_E_CUDA, "P2P halo: step " + std::to_string(herr >> 16) + " waited > 10 s for rank " +
+                                       std::to_string(herr & 0xffff));
+    }
     CUDA_TRY(c, cudaMemcpy(&flag, c->d_flag, sizeof(flag), cudaMemcpyDeviceToHost));
     if (flag != ~0ull) {
         c->latched = true;
@@ -910,7 +1066,7 @@ int ens_sync(ens_ctx* c) {
     return ENS_OK;
 }
 
-static int64_t abi_rows(const ens_ctx* c) { return c->nccl_comm ? c->parts[0].n_own : c->V; }
+static int64_t abi_rows(const ens_ctx* c) { return c->multi ? c->parts[0].n_own : c->V; }
 
 int ens_get_state(ens_ctx* c, double* u_n, double* u_nm1, double* t, int64_t* step) {
     if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
@@ -937,7 +1093,7 @@ int ens_get_owned(const ens_ctx* c, int32_t* node_ids, int64_t* n) {
     if (!c || !n) return fail(nullptr, ENS_E_ARG, "NULL argument");
     *n = abi_rows(c);
     if (node_ids) {
-        if (c->nccl_comm) std::copy(c->parts[0].map_own.begin(), c->parts[0].map_own.end(), node_ids);
+        if (c->multi) std::copy(c->parts[0].map_own.begin(), c->parts[0].map_own.end(), node_ids);
         else
             for (int64_t i = 0; i < c->V; ++i) node_ids[i] = int32_t(i);
     }
@@ -966,6 +1122,13 @@ int ens_set_state(ens_ctx* c, const double* u_n, const double* u_nm1, double t, 
     h_step = step;
     CUDA_TRY(c, cudaMemcpyAsync(c->d_step, &h_step, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0xff, sizeof(unsigned long long), c->stream));
+    if (c->p2p()) {      // every ghost row now holds u_step: the neighbours' flags restart at step
+        static thread_local std::vector<unsigned long long> h_flags;
+        h_flags.assign(size_t(c->world), (unsigned long long)step);
+        for (Part& p : c->parts)
+            CUDA_TRY(c, cudaMemcpyAsync(p.d_hflags, h_flags.data(), h_flags.size() * sizeof(unsigned long long),
+                                        cudaMemcpyHostToDevice, c->stream));
+    }
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->step = step;
     c->latched = false;
@@ -1000,7 +1163,7 @@ int ens_apply_stiffness(ens_ctx* c, const double* u, double* y) {
 }
 
 static int observe_check(ens_ctx* c) {
-    if (c->parts.size() != 1 || c->nccl_comm || c->h_tris.empty())
+    if (c->parts.size() != 1 || c->multi || c->h_tris.empty())
         return fail(c, ENS_E_UNSUPPORTED, "stresses / statistics need a single-part context created by ens_create");
     return ENS_OK;
 }
@@ -1168,6 +1331,71 @@ int ens_matern_fields(const ens_mesh* mesh, double rho_corr, int32_t n, const do
     return rc;
 }
 
+// ---- P2P halo across processes (CUDA IPC) -------------------------------------------------
+namespace {
+struct P2PBlob {
+    uint32_t magic;
+    int32_t rank, world, n_s;
+    int64_t n_loc;
+    cudaIpcMemHandle_t u0, u1, flags;
+};
+static_assert(sizeof(P2PBlob) <= ENS_P2P_BLOB_BYTES, "blob");
+constexpr uint32_t kBlobMagic = 0x32503245u;
+}  // namespace
+
+int ens_p2p_export(const ens_ctx* c, void* blob) {
+    if (!c || !blob) return fail(nullptr, ENS_E_ARG, "NULL argument");
+    ens_ctx* m = const_cast<ens_ctx*>(c);
+    if (!(c->multi && c->p2p())) return fail(m, ENS_E_STATE, "not a one-part-per-process P2P context");
+    const Part& p = c->parts[0];
+    P2PBlob b{};
+    b.magic = kBlobMagic;
+    b.rank = c->rank;
+    b.world = c->world;
+    b.n_s = c->n_s;
+    b.n_loc = p.n_own + p.n_gh;
+    CUDA_TRY(m, cudaIpcGetMemHandle(&b.u0, p.d_u0));
+    CUDA_TRY(m, cudaIpcGetMemHandle(&b.u1, p.d_u1));
+    CUDA_TRY(m, cudaIpcGetMemHandle(&b.flags, p.d_hflags));
+    std::memset(blob, 0, ENS_P2P_BLOB_BYTES);
+    std::memcpy(blob, &b, sizeof(b));
+    return ENS_OK;
+}
+
+int ens_p2p_connect(ens_ctx* c, const void* blobs) {
+    if (!c || !blobs) return fail(nullptr, ENS_E_ARG, "NULL argument");
+    if (!(c->multi && c->p2p())) return fail(c, ENS_E_STATE, "not a one-part-per-process P2P context");
+    if (c->p2p_connected) return fail(c, ENS_E_STATE, "already connected");
+    Part& P = c->parts[0];
+    std::vector<double*> pb;
+    std::vector<unsigned long long*> of;
+    for (size_t k = 0; k < P.out_q.size(); ++k) {
+        const int32_t q = P.out_q[k];
+        P2PBlob b;
+        std::memcpy(&b, static_cast<const char*>(blobs) + size_t(q) * ENS_P2P_BLOB_BYTES, sizeof(b));
+        if (b.magic != kBlobMagic || b.rank != q || b.world != c->world || b.n_s != c->n_s || b.n_loc != P.out_rows[k])
+            return fail(c, ENS_E_ARG, "P2P blob of rank " + std::to_string(q) + " does not match this context");
+        void* ptr[3] = {nullptr, nullptr, nullptr};
+        const cudaIpcMemHandle_t* h[3] = {&b.u0, &b.u1, &b.flags};
+        for (int j = 0; j < 3; ++j) {
+            CUDA_TRY(c, cudaIpcOpenMemHandle(&ptr[j], *h[j], cudaIpcMemLazyEnablePeerAccess));
+            c->ipc_opened.push_back(ptr[j]);
+        }
+        pb.push_back(static_cast<double*>(ptr[0]));
+        pb.push_back(static_cast<double*>(ptr[1]));
+        of.push_back(static_cast<unsigned long long*>(ptr[2]) + P.plan.p);
+    }
+    if (!pb.empty()) {
+        CUDA_TRY(c, cudaMemcpyAsync(P.d_peer_buf, pb.data(), pb.size() * sizeof(double*), cudaMemcpyHostToDevice,
+                                    c->stream));
+        CUDA_TRY(c, cudaMemcpyAsync(P.d_out_flag, of.data(), of.size() * sizeof(void*), cudaMemcpyHostToDevice,
+                                    c->stream));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    c->p2p_connected = true;
+    return ENS_OK;
+}
+
 int ens_query(const ens_ctx* c, ens_info* info) {
     if (!c || !info) return fail(nullptr, ENS_E_ARG, "NULL argument");
     std::memset(info, 0, sizeof(*info));
@@ -1185,6 +1413,7 @@ int ens_query(const ens_ctx* c, ens_info* info) {
     info->rcm_bandwidth = c->bandwidth;
     info->graph_steps = c->use_graphs() ? c->graph_steps : 0;
     info->reassemble_every = c->reassemble_every;
+    info->halo = c->halo;
     // algorithmic HBM bytes of the rows this context advances: values +
     // u_n, u_{n-1} read, u_{n+1} written, c1 (+ c2, c3) per node per realisation
     const int64_t ns = c->n_s, per_node = 3 * 8 * 3 + 8 + (c->damping == ENS_DAMP_IDENTITY ? 16 : 0);
@@ -1193,7 +1422,9 @@ int ens_query(const ens_ctx* c, ens_info* info) {
         own += p.n_own;
         halo += int64_t(p.plan.send_rows.size());
         for (const auto& pe : p.plan.peers) halo += pe.recv_n;
-        launches += c->has_halo() ? (1 + (p.plan.b_lo > 0) + (p.plan.b_hi > 0) + !p.plan.send_rows.empty()) : 1;
+        if (!c->has_halo()) launches += 1;
+        else if (c->p2p()) launches += 1 + (p.n_in > 0) + (p.plan.b_lo > 0) + (p.plan.b_hi > 0) + (p.n_out > 0);
+        else launches += 1 + (p.plan.b_lo > 0) + (p.plan.b_hi > 0) + !p.plan.send_rows.empty();
     }
     info->n_owned = own;
     info->halo_bytes_per_step = halo * 3 * 8 * ns;

@@ -57,7 +57,23 @@ struct StepArgs {
     int32_t s_global0 = 0;
     // diagnostic mode: y = K u_n written to y_out ([V][3][n_s]), no update
     double* y_out = nullptr;
+    // P2P halo (ENS_HALO_P2P): u_{n+1} of local row i also goes to the neighbours' ghost rows
+    // fwd_dst[fwd_ptr[i] .. fwd_ptr[i+1]) = {peer slot, row in the peer's local numbering};
+    // peer_buf[2 slot + b] = the peer's state buffer b.  Null => no forwarding.
+    const int32_t* fwd_ptr = nullptr;   // [rows + 1]
+    const int2* fwd_dst = nullptr;
+    double* const* peer_buf = nullptr;
 };
+
+// P2P halo: publish "ghost data of u_{step+1} stored" to every neighbour
+// (out_flag[k] = the slot of this part in neighbour k's flag array; st.release.sys after a
+// system fence), and wait until every neighbour q in in_q has published >= step
+// (ld.acquire.sys on this part's own flags[q]).  step = *step_base + step_off.  A wait
+// longer than ~10 s stores the step and neighbour into *herr and gives up.
+cudaError_t launch_halo_signal(int32_t n_out, unsigned long long* const* out_flag, const int64_t* step_base,
+                               int64_t step_off, cudaStream_t st);
+cudaError_t launch_halo_wait(int32_t n_in, const int32_t* in_q, const unsigned long long* flags,
+                             const int64_t* step_base, int64_t step_off, unsigned long long* herr, cudaStream_t st);
 
 // Fused step (S2 load + S3 ensemble SpMM + S4 central-difference update) on the
 // assembled values: one launch advances rows [row0, row0+V) by one step.

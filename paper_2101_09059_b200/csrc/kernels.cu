@@ -274,7 +274,17 @@ __device__ __forceinline__ void upd_store(const StepArgs& a, const StepCtx& sc, 
             out.v[v] = w;
         }
         st_vec<VEC>(sc.uo + (i * 3 + c) * n_s + s0, out);
+        if (a.fwd_ptr) {      // P2P halo: the same values into the neighbours' ghost rows
+            const int32_t f1 = __ldg(a.fwd_ptr + i + 1);
+            for (int32_t f = __ldg(a.fwd_ptr + i); f < f1; ++f) {
+                const int2 d = a.fwd_dst[f];
+                double* dst = a.peer_buf[2 * d.x + int((sc.step + 1) & 1)];
+                st_vec<VEC>(dst + (int64_t(d.y) * 3 + c) * n_s + s0, out);
+            }
+        }
     }
+    if (a.fwd_ptr && __ldg(a.fwd_ptr + i) < __ldg(a.fwd_ptr + i + 1))
+        __threadfence_system();   // remote stores ordered before the signal kernel's release
     if (bad) {
         for (int v = 0; v < VEC; ++v)
             if ((bad >> v) & 1) {
@@ -574,6 +584,36 @@ k_step_matrix_free(const StepArgs a) {
 
 __global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
 
+// ---- P2P halo flags (ENS_HALO_P2P) ----------------------------------------------------
+__global__ void k_halo_signal(int32_t n_out, unsigned long long* const* out_flag, const int64_t* step_base,
+                              int64_t step_off) {
+    const int k = int(threadIdx.x);
+    if (k >= n_out) return;
+    const unsigned long long v = (unsigned long long)(*step_base + step_off + 1);
+    asm volatile("fence.sc.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(out_flag[k]), "l"(v) : "memory");
+}
+
+__global__ void k_halo_wait(int32_t n_in, const int32_t* in_q, const unsigned long long* flags,
+                            const int64_t* step_base, int64_t step_off, unsigned long long* herr) {
+    const int k = int(threadIdx.x);
+    if (k >= n_in) return;
+    const long long step = *step_base + step_off;
+    const unsigned long long* f = flags + in_q[k];
+    unsigned long long t0, now, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+        if ((long long)v >= step) break;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (now - t0 > 10000000000ull) {           // 10 s: the neighbour is gone
+            atomicMin(herr, (unsigned long long)step << 16 | (unsigned long long)in_q[k]);
+            break;
+        }
+        __nanosleep(64);
+    }
+}
+
 // ---- F0: device assembly of the per-realisation block values ---------------------------
 __global__ void __launch_bounds__(kThreads)
 k_assemble(int64_t nnzb, int32_t n_s, const int32_t* __restrict__ cptr, const int32_t* __restrict__ contrib,
@@ -682,6 +722,20 @@ static cudaError_t launch_a2(const StepArgs& a, cudaStream_t st) {
         if (a.n_s == 128) return launch_a2_ns<VEC, APPLY, BATCH, MINB, 128>(a, st);
     }
     return launch_a2_ns<VEC, APPLY, BATCH, MINB, 0>(a, st);
+}
+
+cudaError_t launch_halo_signal(int32_t n_out, unsigned long long* const* out_flag, const int64_t* step_base,
+                               int64_t step_off, cudaStream_t st) {
+    if (n_out <= 0) return cudaSuccess;
+    k_halo_signal<<<1, 32 * ((n_out + 31) / 32), 0, st>>>(n_out, out_flag, step_base, step_off);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_wait(int32_t n_in, const int32_t* in_q, const unsigned long long* flags,
+                             const int64_t* step_base, int64_t step_off, unsigned long long* herr, cudaStream_t st) {
+    if (n_in <= 0) return cudaSuccess;
+    k_halo_wait<<<1, 32 * ((n_in + 31) / 32), 0, st>>>(n_in, in_q, flags, step_base, step_off, herr);
+    return cudaGetLastError();
 }
 
 int pick_vec(int32_t n_s) {

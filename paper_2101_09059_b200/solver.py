@@ -16,6 +16,7 @@ from ._ffi import EnsError, check, lib
 DAMPING = {"none": 0, "mass": 1, "identity": 2, 0: 0, 1: 1, 2: 2}
 KERNEL = {"assembled": 0, "matrix_free": 1, "assembled_sym": 2, 0: 0, 1: 1, 2: 2}
 DIST = {"single": 0, "node": 1, "ensemble": 2, 0: 0, 1: 1, 2: 2}
+HALO = {"nccl": 0, "p2p": 1, 0: 0, 1: 1}
 
 
 def _c(a, dtype):
@@ -59,9 +60,16 @@ class Ensemble:
     def __init__(self, xyz, tris, fixed, E, h, *, rho, nu, k_shear=5.0 / 6.0, dt=0.0,
                  cfl_safety=0.9, c_d=0.0, damping="none", kernel="assembled", dist="single",
                  s_begin=0, rank=0, world=1, nccl_comm=None, device=None, stream=None,
-                 torch_alloc=True, reassemble_every=0, _ctx=None):
+                 torch_alloc=True, reassemble_every=0, halo="nccl", p2p_procs=False, group=None,
+                 _ctx=None):
+        """dist="node" splits the RCM rows into `world` parts.  halo="nccl": NCCL
+        send/recv with nccl_comm (one part per process) or, without it, device copies
+        between all parts held here.  halo="p2p": device-initiated stores into the
+        neighbours' ghost rows; p2p_procs=True => one part per process, connected to the
+        other ranks of `group` (torch.distributed, default group) through CUDA IPC."""
         self._ctx = None
         self._alloc = None
+        self._p2p_group, self._p2p_multi = None, False
         if _ctx is not None:                      # from_csr
             self._ctx, self._alloc, self.n_s, self.V = _ctx
             return
@@ -76,9 +84,26 @@ class Ensemble:
         if nccl_comm is not None:
             opt.nccl_comm = C.c_void_p(int(nccl_comm))
         opt.reassemble_every = int(reassemble_every)
+        opt.halo = HALO[halo]
+        opt.p2p_procs = int(bool(p2p_procs))
         ctx = C.c_void_p()
         check(lib().ens_create(C.byref(mesh), C.byref(mat), C.byref(opt), C.byref(ctx)))
         self._ctx = ctx
+        self._p2p_multi = bool(p2p_procs) and int(world) > 1
+        if self._p2p_multi:
+            self._p2p_group = group
+            self._p2p_connect(group)
+
+    def _p2p_connect(self, group):
+        """All-gather the CUDA IPC blobs of every rank (ens_p2p_export) and connect."""
+        import torch.distributed as dist
+        blob = (C.c_char * _ffi.P2P_BLOB_BYTES)()
+        check(lib().ens_p2p_export(self._ctx, blob), self._ctx)
+        world = dist.get_world_size(group)
+        objs = [None] * world
+        dist.all_gather_object(objs, bytes(blob), group=group)
+        allb = b"".join(objs)
+        check(lib().ens_p2p_connect(self._ctx, allb), self._ctx)
 
     @classmethod
     def from_csr(cls, row_ptr, col, Kval, c1, c2, c3, fixed=None, dt=1.0, *, device=None,
@@ -154,6 +179,9 @@ class Ensemble:
         u_n = None if u_n is None else _c(u_n, np.float64)
         u_nm1 = None if u_nm1 is None else _c(u_nm1, np.float64)
         check(lib().ens_set_state(self._ctx, _p(u_n), _p(u_nm1), 0.0, int(step)), self._ctx)
+        if getattr(self, "_p2p_multi", False):
+            import torch.distributed as dist      # neighbours must not step before every reset
+            dist.barrier(group=self._p2p_group)
 
     def apply_stiffness(self, u):
         u = _c(u, np.float64)

@@ -247,20 +247,24 @@ def test_c2_laplace_law_on_gpu():
     ens.close()
 
 
+@pytest.mark.parametrize("halo", ["nccl", "p2p"])
 @pytest.mark.parametrize("kernel", ["assembled", "assembled_sym", "matrix_free"])
 @pytest.mark.parametrize("P", [2, 3, 4])
-def test_node_partition_bitexact(kernel, P):
-    """ENS_DIST_NODE (all P parts in one context, halo by device copies): boundary rows
-    first, pack, exchange, interior rows — bit-identical to the unpartitioned run, since
-    each row keeps its global summation order."""
+def test_node_partition_bitexact(kernel, P, halo):
+    """ENS_DIST_NODE (all P parts in one context): halo "nccl" = boundary rows, pack,
+    device copies, interior rows; halo "p2p" = boundary rows storing u_{n+1} straight into
+    the neighbours' ghost rows + release/acquire step flags, in CUDA graphs.  Both are
+    bit-identical to the unpartitioned run, since each row keeps its global summation
+    order."""
     m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(24, 60), 0.01, 3), 2)
     E, h = _mats(m, 6, 61)
     tr = loads.pulsatile(m.xyz, m.tris, period=0.01, systole=0.004, ramp_T=0.003)
     kw = dict(rho=RHO, nu=NU, k_shear=KS, kernel=kernel, dt=5e-5, damping="identity", c_d=0.3)
     ref = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, **kw)
-    par = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, dist="node", world=P, **kw)
+    par = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, dist="node", world=P, halo=halo, **kw)
     inf = par.info()
     assert inf["n_owned"] == m.n_nodes and inf["halo_bytes_per_step"] > 0
+    assert inf["halo"] == solver.HALO[halo] and (inf["graph_steps"] > 0) == (halo == "p2p")
     for e in (ref, par):
         e.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
         e.step(257)
@@ -471,6 +475,25 @@ def test_geometry_reassembly_parity(kernel):
     lin.set_traction(tr.F, tr.tab_t, tr.tab_g, 0.0, 0.0)
     lin.run(n)
     assert np.linalg.norm(om.u_n - lin.u_n) > 1e-6 * np.linalg.norm(lin.u_n)    # the update matters
+
+
+@pytest.mark.parametrize("halo", ["nccl", "p2p"])
+def test_geometry_reassembly_node_partition_bitexact(halo):
+    """Re-assembly reads the ghost rows' u as well: partitioned runs (P = 3) stay
+    bit-identical to the single-part run."""
+    m = meshmod.shuffle_nodes(meshmod.cylinder(16, 25), 6)
+    E, h = _mats(m, 4, 92)
+    tr = loads.steady(m.xyz, m.tris, p=5 * loads.P_SUPERPOSED)
+    kw = dict(rho=RHO, nu=NU, k_shear=KS, kernel="assembled", dt=1e-4, damping="mass", c_d=100.0,
+              reassemble_every=20)
+    out = []
+    for extra in ({}, dict(dist="node", world=3, halo=halo)):
+        ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, **kw, **extra)
+        ens.set_traction(tr.F)
+        ens.step(150)
+        out.append(ens.get_state()[0])
+        ens.close()
+    assert np.array_equal(out[0], out[1])
 
 
 def test_reassembly_rejected_for_matrix_free():

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_library_exports_every_declared_symbol():
     header = open(os.path.join(ROOT, "include", "ens.h")).read()
-    declared = set(re.findall(r"\b(ens_[a-z_]+)\s*\(", header))
+    declared = set(re.findall(r"\b(ens_[a-z0-9_]+)\s*\(", header))
     declared -= {"ens_ctx"}
     L = _ffi.lib()
     for name in sorted(declared):
