@@ -185,16 +185,18 @@ def run_reference(args):
     return 0
 
 
-def _node_partition_run(args, cfg, base, m, tr, rank, world, local, stream, barrier, n_s):
+def _node_partition_run(args, cfg, base, m, tr, rank, world, local, stream, barrier, n_s, halo):
     """Node partition (strong scaling of the full config): every rank holds the same N_s
-    realisations, the RCM rows are split across ranks, NCCL halo of the interface rows."""
+    realisations, the RCM rows are split across ranks; halo "nccl" = NCCL send/recv of the
+    packed interface rows, "p2p" = device-initiated stores into the neighbours' ghost rows
+    over NVLink (CUDA IPC) with step flags, graph-captured."""
     import torch
     from paper_2101_09059_b200 import solver
-    comm = solver.nccl_comm_of()
+    extra = dict(nccl_comm=solver.nccl_comm_of()) if halo == "nccl" else dict(halo="p2p", p2p_procs=True)
     npar = solver.Ensemble(m.xyz, m.tris, m.fixed, base.E, base.h, rho=cfg.rho, nu=cfg.nu,
                            k_shear=cfg.k_shear, damping=cfg.damping, c_d=cfg.c_d,
                            kernel=args.kernel, dist="node", rank=rank, world=world,
-                           nccl_comm=comm, device=local)
+                           device=local, **extra)
     npar.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
     npar.step(max(3, args.warmup))
     npar.sync()
@@ -212,7 +214,8 @@ def _node_partition_run(args, cfg, base, m, tr, rank, world, local, stream, barr
             "ms_per_step": 1e3 * tmax / args.steps, "scaling": "strong",
             "n_s_total": n_s, "rows_rank0": ninf["n_owned"],
             "halo_bytes_per_step_rank0": ninf["halo_bytes_per_step"],
-            "launches_per_step": ninf["launches_per_step"]}
+            "launches_per_step": ninf["launches_per_step"], "halo": halo,
+            "graph_steps": ninf["graph_steps"]}
     npar.close()
 
     return node
@@ -279,7 +282,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-alternatives", action="store_true", help="do not time the other kernels")
     ap.add_argument("--node-partition", action="store_true",
-                    help="at N > 1 also time ENS_DIST_NODE (RCM rows split, NCCL halo; strong scaling)")
+                    help="at N > 1 also time ENS_DIST_NODE (RCM rows split; NCCL and P2P halos; strong scaling)")
     ap.add_argument("--e2e-windows", type=int, default=10)
     ap.add_argument("--obs-every", type=int, default=100)
     args = ap.parse_args(argv)
@@ -372,10 +375,13 @@ def main(argv=None):
     # every rank, RCM rows split across ranks, NCCL halo of the interface rows per step
     node = None
     if world > 1 and args.node_partition:
-        try:
-            node = _node_partition_run(args, cfg, base, m, tr, rank, world, local, stream, barrier, n_s)
-        except Exception as e:          # reported, never fatal for the primary (sharded) line
-            node = {"error": repr(e)[:300]}
+        node = {}
+        for halo in ("nccl", "p2p"):
+            try:
+                node[halo] = _node_partition_run(args, cfg, base, m, tr, rank, world, local, stream, barrier,
+                                                 n_s, halo)
+            except Exception as e:      # reported, never fatal for the primary (sharded) line
+                node[halo] = {"error": repr(e)[:300]}
 
     # the other kernels of the same step, same inputs, same launch protocol (reported
     # alongside; the headline is --kernel)
