@@ -365,6 +365,11 @@ k_step_assembled(const StepArgs a) {
 // bandwidth, so still in L2).  Lower references (j ascending) then the row's own upper
 // blocks (j ascending) visit the columns in exactly the order of the full CSR row, and
 // K^_e is exactly symmetric, so the result is bit-identical to F1 with ~half the bytes.
+// Both reads of a stored block happen within about half a warp lifetime (~10 us, ~65 MB of
+// streamed values at full bandwidth): row i's transposed read of (j, i) comes FIRST (it is
+// among row i's first blocks, while row j reads its own blocks last), so that read takes
+// an L2 evict_last policy and row j's later own read an evict_first one (HINT 3, default).
+// Without the policies the second reads mostly miss L2.
 template <int VEC, bool APPLY, bool PREF, int HINT>
 __global__ void __launch_bounds__(kThreads)
 k_step_assembled_sym(const StepArgs a) {
@@ -380,12 +385,22 @@ k_step_assembled_sym(const StepArgs a) {
     const int s0 = int(tid % P) * VEC;
     const int n_s = a.n_s;
 
-    // HINT 1: first (own-row) read evict_last, second (transposed) read evict_first;
-    // HINT 2: first read normal, second read evict_first; HINT 0: no policy
-    uint64_t pol_keep = 0, pol_drop = 0;
-    if constexpr (HINT == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
-    if constexpr (HINT == 2) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
-    if constexpr (HINT != 0) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_drop));
+    // L2 policies of the two reads of a stored block: pol_own for row j's own read of
+    // (j, i), pol_tr for row i's transposed read.  HINT 1: own evict_last, tr evict_first;
+    // HINT 2: own normal, tr evict_first; HINT 3: tr evict_last, own evict_first;
+    // HINT 4: tr evict_last, own normal; HINT 0: no policy.
+    uint64_t pol_own = 0, pol_tr = 0;
+    if constexpr (HINT == 1 || HINT == 3 || HINT == 4) {
+        uint64_t keep, drop, norm;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(drop));
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(norm));
+        pol_own = HINT == 1 ? keep : (HINT == 3 ? drop : norm);
+        pol_tr = HINT == 1 ? drop : keep;
+    } else if constexpr (HINT == 2) {
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_own));
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_tr));
+    }
     Upd<VEC> upd;
     if constexpr (!APPLY && PREF) upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
 
@@ -406,7 +421,7 @@ k_step_assembled_sym(const StepArgs a) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) u[d] = ld_ro<VEC>(up + d * n_s);
 #pragma unroll
-        for (int e = 0; e < 9; ++e) kk[e] = HINT ? ld_pol_l1<VEC>(kp + e * n_s, pol_drop) : ld_once_l1<VEC>(kp + e * n_s);
+        for (int e = 0; e < 9; ++e) kk[e] = HINT ? ld_pol_l1<VEC>(kp + e * n_s, pol_tr) : ld_once_l1<VEC>(kp + e * n_s);
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -424,7 +439,7 @@ k_step_assembled_sym(const StepArgs a) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) u[d] = ld_ro<VEC>(up + d * n_s);
 #pragma unroll
-        for (int e = 0; e < 9; ++e) kk[e] = HINT ? ld_pol_l1<VEC>(kp + e * n_s, pol_keep) : ld_once_l1<VEC>(kp + e * n_s);
+        for (int e = 0; e < 9; ++e) kk[e] = HINT ? ld_pol_l1<VEC>(kp + e * n_s, pol_own) : ld_once_l1<VEC>(kp + e * n_s);
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -754,12 +769,15 @@ static cudaError_t launch_a1s(const StepArgs& a, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     static int hint = [] {
         const char* e = std::getenv("ENS_A1S_HINTS");
-        return e ? std::atoi(e) : 0;
+        return e ? std::atoi(e) : 3;
     }();
-    if (hint == 1) k_step_assembled_sym<VEC, APPLY, false, 1><<<grid_for(n), kThreads, 0, st>>>(a);
-    else if (hint == 2) k_step_assembled_sym<VEC, APPLY, false, 2><<<grid_for(n), kThreads, 0, st>>>(a);
-    else if (a1_prefetch()) k_step_assembled_sym<VEC, APPLY, true, 0><<<grid_for(n), kThreads, 0, st>>>(a);
-    else k_step_assembled_sym<VEC, APPLY, false, 0><<<grid_for(n), kThreads, 0, st>>>(a);
+    const unsigned g = grid_for(n);
+    if (hint == 1) k_step_assembled_sym<VEC, APPLY, false, 1><<<g, kThreads, 0, st>>>(a);
+    else if (hint == 2) k_step_assembled_sym<VEC, APPLY, false, 2><<<g, kThreads, 0, st>>>(a);
+    else if (hint == 3) k_step_assembled_sym<VEC, APPLY, false, 3><<<g, kThreads, 0, st>>>(a);
+    else if (hint == 4) k_step_assembled_sym<VEC, APPLY, false, 4><<<g, kThreads, 0, st>>>(a);
+    else if (a1_prefetch()) k_step_assembled_sym<VEC, APPLY, true, 0><<<g, kThreads, 0, st>>>(a);
+    else k_step_assembled_sym<VEC, APPLY, false, 0><<<g, kThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 
