@@ -1,11 +1,13 @@
 #!/usr/bin/env python
 """Benchmark of the fused ensemble step (arXiv 2101.09059 hot path) on B200.
 
-    python bench.py [--gpus N --steps K --warmup W --config c2 --kernel assembled|matrix_free]
+    python bench.py [--gpus N --steps K --warmup W --config c2 --kernel assembled_sym|assembled|matrix_free]
     python bench.py --impl reference ...        # the CPU oracle, timed on the host cores
 
 One "step" = one explicit central-difference step of all N_s realisations (S2 load +
-S3 ensemble SpMM + S4 update, one fused kernel launch).  Metric (BASELINE.json):
+S3 ensemble SpMM + S4 update, one fused kernel launch).  Default kernel: the assembled
+per-realisation block-CSR values in symmetric half storage (a1s, the fastest assembled
+path); the full-storage a1 and the matrix-free a2 are timed alongside ("alternatives").  Metric (BASELINE.json):
 ensemble DOF-updates/s = N_s * 3V * steps / time, plus the fused step's HBM GB/s against
 the measured peak.  Multi-GPU (torchrun): ensemble sharding, N_s per GPU fixed (weak
 scaling), no collective on the data path; timing = max over ranks (CUDA events).
@@ -278,7 +280,7 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--n-s", type=int, default=None, help="realisations per GPU (default: the config's)")
-    ap.add_argument("--kernel", default="assembled", choices=["assembled", "assembled_sym", "matrix_free"])
+    ap.add_argument("--kernel", default="assembled_sym", choices=["assembled", "assembled_sym", "matrix_free"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-alternatives", action="store_true", help="do not time the other kernels")
     ap.add_argument("--node-partition", action="store_true",
