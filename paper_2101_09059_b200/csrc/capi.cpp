@@ -45,6 +45,7 @@ struct Part {
     int4* d_fan = nullptr;
     double *d_Krow = nullptr, *d_alpha = nullptr;
     int32_t mf_rows = 1, mf_groups = 1, mf_smem_inc = 0;
+    int32_t pipe_rows = 0, pipe_cap = 0;                  // pipelined matrix-free kernel
     int32_t *d_sym_lptr = nullptr, *d_sym_lidx = nullptr, *d_sym_lcol = nullptr, *d_sym_scol = nullptr;
     int2* d_sym_urange = nullptr;
     int64_t n_stored = 0;                                  // value blocks held (assembled kernels)
@@ -99,6 +100,8 @@ struct ens_ctx {
 
     double* d_stage = nullptr;              // [n_s][V][3] ABI staging
     unsigned long long* d_flag = nullptr;
+    double* d_coef = nullptr;               // [2][kMaxFields] load coefficients (StepArgs.coef_buf)
+    bool coef_dirty = true;                 // seed d_coef before the next step
     int64_t* d_step = nullptr;
     int32_t n_fields = 0, n_tab = 0;
     double *d_tab_t = nullptr, *d_tab_g = nullptr;
@@ -303,6 +306,8 @@ ens::StepArgs part_args(const ens_ctx* c, const Part& p) {
     a.mf_rows = p.mf_rows;
     a.mf_groups = p.mf_groups;
     a.mf_smem_inc = p.mf_smem_inc;
+    a.pipe_rows = p.pipe_rows;
+    a.pipe_cap = p.pipe_cap;
     a.sym_lptr = p.d_sym_lptr;
     a.sym_lidx = p.d_sym_lidx;
     a.sym_lcol = p.d_sym_lcol;
@@ -326,6 +331,7 @@ ens::StepArgs part_args(const ens_ctx* c, const Part& p) {
     a.ubuf0 = p.d_u0;
     a.ubuf1 = p.d_u1;
     a.flag = c->d_flag;
+    a.coef_buf = c->d_coef;
     a.s_global0 = c->s_begin;
     return a;
 }
@@ -669,6 +675,23 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
         }
         if (int64_t(P.mf_smem_inc) * 240 > 200 * 1024)
             return fail(c, ENS_E_UNSUPPORTED, "a node has too many incident elements for the matrix-free kernel");
+        // pipelined variant (N_s % 64 == 0): rows per warp such that any window of that many
+        // consecutive rows (launches start at any row) has <= 96 incidences
+        P.pipe_rows = P.pipe_cap = 0;
+        if (c->n_s % 64 == 0 && ens::mf_pipe_enabled()) {
+            for (int32_t rw = ens::mf_pipe_rows(); rw >= 1; rw /= 2) {
+                int32_t mx = 0;
+                for (int64_t r = 0; r < P.n_own; ++r) {
+                    const int64_t r1 = std::min<int64_t>(r + rw, P.n_own);
+                    mx = std::max(mx, ip[size_t(r1)] - ip[size_t(r)]);
+                }
+                if (mx <= 96) {
+                    P.pipe_rows = rw;
+                    P.pipe_cap = (mx + 7) / 8 * 8;
+                    break;
+                }
+            }
+        }
         static_assert(sizeof(ens::FanRec) == sizeof(int4), "FanRec layout");
         RC_TRY(upload(c, &P.d_inc_ptr, ip.data(), ip.size()));
         RC_TRY(upload(c, &P.d_fan, reinterpret_cast<const int4*>(rec.data()), rec.size()));
@@ -756,6 +779,8 @@ int finish_create(ens_ctx* c) {
     RC_TRY(dalloc(c, &c->d_stage, size_t(c->V) * 3 * size_t(c->n_s)));
     RC_TRY(dalloc(c, &c->d_flag, 1));
     RC_TRY(dalloc(c, &c->d_herr, 1));
+    RC_TRY(dalloc(c, &c->d_coef, 2 * ens::kMaxFields));
+    c->coef_dirty = true;
     RC_TRY(dalloc(c, &c->d_step, 1));
     CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0xff, sizeof(unsigned long long), c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->d_herr, 0xff, sizeof(unsigned long long), c->stream));
@@ -1009,11 +1034,11 @@ int ens_set_traction(ens_ctx* c, int32_t n_fields, const double* F, int32_t n_ta
     dfree(c, c->d_tab_g);
     for (Part& p : c->parts) {
         dfree(c, p.d_Fk);
-        std::vector<double> Fd(size_t(n_fields * p.n_own * 3));
+        std::vector<double> Fd(size_t(n_fields * p.n_own * 4), 0.0);     // [k][row][4]
         for (int32_t k = 0; k < n_fields; ++k)
             for (int64_t i = 0; i < p.n_own; ++i)
                 for (int d = 0; d < 3; ++d)
-                    Fd[size_t((k * p.n_own + i) * 3 + d)] = F[(k * c->V + p.map_own[size_t(i)]) * 3 + d];
+                    Fd[size_t((k * p.n_own + i) * 4 + d)] = F[(k * c->V + p.map_own[size_t(i)]) * 3 + d];
         RC_TRY(upload(c, &p.d_Fk, Fd.data(), Fd.size()));
     }
     if (n_tab > 0) {
@@ -1024,6 +1049,7 @@ int ens_set_traction(ens_ctx* c, int32_t n_fields, const double* F, int32_t n_ta
     c->n_tab = n_tab;
     c->period = period;
     c->ramp_T = ramp_T;
+    c->coef_dirty = true;
     return ENS_OK;
 }
 
@@ -1032,6 +1058,10 @@ int ens_step(ens_ctx* c, int64_t n) {
     if (n < 0) return fail(c, ENS_E_ARG, "n must be >= 0");
     if (c->latched) return fail(c, ENS_E_STATE, "context diverged: call ens_set_state before stepping again");
     if (!c->p2p_connected) return fail(c, ENS_E_STATE, "P2P halo: call ens_p2p_connect before ens_step");
+    if (n > 0 && c->coef_dirty) {
+        CUDA_TRY(c, ens::launch_seed_coeffs(part_args(c, c->parts[0]), c->stream));
+        c->coef_dirty = false;
+    }
     int64_t left = n;
     if (c->use_graphs() && n >= c->graph_steps) {
         if (c->graph_dirty) RC_TRY(build_graph(c));
@@ -1132,6 +1162,7 @@ int ens_set_state(ens_ctx* c, const double* u_n, const double* u_nm1, double t, 
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->step = step;
     c->latched = false;
+    c->coef_dirty = true;
     return ENS_OK;
 }
 

@@ -35,6 +35,8 @@ struct StepArgs {
     int32_t mf_rows = 1;                // rows per CTA
     int32_t mf_groups = 1;              // realisation groups (threads) per row per CTA
     int32_t mf_smem_inc = 0;            // max incidences staged by one CTA
+    int32_t pipe_rows = 0;              // pipelined a2: consecutive rows per warp (0 = not built)
+    int32_t pipe_cap = 0;               // max incidences of any pipe_rows consecutive rows
     // update coefficients
     const double* c1 = nullptr;
     const double* c2a = nullptr;        // null => scalars c2, c3
@@ -43,7 +45,7 @@ struct StepArgs {
     const uint8_t* fixed = nullptr;     // [rows]
     // load f(t) = ramp(t) sum_k g_k(t) F_k
     int32_t n_fields = 0;
-    const double* Fk = nullptr;         // [n_fields][fk_rows][3]
+    const double* Fk = nullptr;         // [n_fields][fk_rows][4] (x, y, z, 0: 32 B rows for TMA)
     int32_t n_tab = 0;
     const double* tab_t = nullptr;      // device [n_tab]
     const double* tab_g = nullptr;      // device [n_fields][n_tab]
@@ -54,6 +56,7 @@ struct StepArgs {
     double* ubuf0 = nullptr;
     double* ubuf1 = nullptr;
     unsigned long long* flag = nullptr; // min over (step << 24 | s) of non-finite results
+    double* coef_buf = nullptr;         // [2][kMaxFields] load coefficients of steps of each parity
     int32_t s_global0 = 0;
     // diagnostic mode: y = K u_n written to y_out ([V][3][n_s]), no update
     double* y_out = nullptr;
@@ -85,6 +88,10 @@ cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st);
 // realisations per thread of the step kernels for a given N_s (4, 2 or 1)
 int pick_vec(int32_t n_s);      // assembled kernel
 int pick_vec_mf(int32_t n_s);   // matrix-free kernel
+bool mf_pipe_enabled();         // pipelined matrix-free variant (ENS_MF_PIPE=1; default off)
+int mf_pipe_rows();             // its rows per warp (ENS_MF_PIPE_ROWS, default 4)
+// coef_buf[(step & 1)] = the load coefficients of step *step_base (after host changes)
+cudaError_t launch_seed_coeffs(const StepArgs& a, cudaStream_t st);
 // *step_base += n (after n steps were enqueued)
 cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st);
 

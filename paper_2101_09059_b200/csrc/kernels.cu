@@ -158,6 +158,7 @@ __device__ void load_coeffs(const StepArgs& a, double t, double* coef) {
     }
 }
 
+// (step_coef below, after step_ctx)
 struct StepCtx {
     int64_t step;
     const double* un;
@@ -170,6 +171,16 @@ __device__ __forceinline__ StepCtx step_ctx(const StepArgs& a) {
     c.un = (c.step & 1) ? a.ubuf1 : a.ubuf0;
     c.uo = (c.step & 1) ? a.ubuf0 : a.ubuf1;
     return c;
+}
+
+// Load coefficients of the step: coef_buf[(step & 1) * kMaxFields + k] = ramp(t_step) g_k(t_step).
+// One thread of every step launch evaluates the NEXT step's (table search, sine) into the
+// other half, so no CTA has it on its critical path; ens_step seeds the current step's
+// after any host-side change (launch_seed_coeffs).  The halves never alias within a launch.
+__device__ __forceinline__ const double* step_coef(const StepArgs& a, const StepCtx& sc) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+        load_coeffs(a, double(sc.step + 1) * a.dt, a.coef_buf + ((sc.step + 1) & 1) * kMaxFields);
+    return a.coef_buf + (sc.step & 1) * kMaxFields;
 }
 
 // S2 + S4: r = f - y; u_{n+1} = c1 r + c2 u_n - c3 u_{n-1}; Dirichlet; non-finite flag.
@@ -201,7 +212,7 @@ __device__ __forceinline__ void upd_load(const StepArgs& a, const StepCtx& sc, c
         if (load_un) u.un[c] = ld_ro<VEC>(sc.un + off);
         u.uo[c] = ld_rw<VEC>(sc.uo + off);
         double f = 0.0;
-        for (int k = 0; k < a.n_fields; ++k) f = fma(coef[k], __ldg(a.Fk + (int64_t(k) * a.fk_rows + i) * 3 + c), f);
+        for (int k = 0; k < a.n_fields; ++k) f = fma(coef[k], __ldg(a.Fk + (int64_t(k) * a.fk_rows + i) * 4 + c), f);
         u.f[c] = f;
     }
 }
@@ -235,9 +246,10 @@ __device__ __forceinline__ void upd_load_async(const StepArgs& a, const StepCtx&
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+// fk: the row's F_k staged in shared memory (field k at fk[k * fk_stride + c])
 template <int VEC>
 __device__ __forceinline__ void upd_collect(const StepArgs& a, const double* coef, int64_t i, const double* slot,
-                                            Upd<VEC>& u) {
+                                            const double* fk, int fk_stride, Upd<VEC>& u) {
     asm volatile("cp.async.wait_all;" ::: "memory");
     u.fx = a.fixed ? __ldg(a.fixed + i) : uint8_t(0);
 #pragma unroll
@@ -251,7 +263,7 @@ __device__ __forceinline__ void upd_collect(const StepArgs& a, const double* coe
 #pragma unroll
         for (int v = 0; v < VEC; ++v) u.uo[c].v[v] = slot[(3 + c) * VEC + v];
         double f = 0.0;
-        for (int k = 0; k < a.n_fields; ++k) f = fma(coef[k], __ldg(a.Fk + (int64_t(k) * a.fk_rows + i) * 3 + c), f);
+        for (int k = 0; k < a.n_fields; ++k) f = fma(coef[k], fk[k * fk_stride + c], f);
         u.f[c] = f;
     }
 }
@@ -309,10 +321,8 @@ __device__ __forceinline__ void store_y(const StepArgs& a, int64_t i, int s0, co
 template <int VEC, bool APPLY, bool PREF>
 __global__ void __launch_bounds__(kThreads)
 k_step_assembled(const StepArgs a) {
-    __shared__ double s_coef[kMaxFields];
     const StepCtx sc = step_ctx(a);
-    if (!APPLY && threadIdx.x == 0) load_coeffs(a, double(sc.step) * a.dt, s_coef);
-    if (!APPLY) __syncthreads();
+    const double* s_coef = APPLY ? nullptr : step_coef(a, sc);
 
     const int P = a.n_s / VEC;                       // realisation groups per row
     const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -373,10 +383,8 @@ k_step_assembled(const StepArgs a) {
 template <int VEC, bool APPLY, bool PREF, int HINT>
 __global__ void __launch_bounds__(kThreads)
 k_step_assembled_sym(const StepArgs a) {
-    __shared__ double s_coef[kMaxFields];
     const StepCtx sc = step_ctx(a);
-    if (!APPLY && threadIdx.x == 0) load_coeffs(a, double(sc.step) * a.dt, s_coef);
-    if (!APPLY) __syncthreads();
+    const double* s_coef = APPLY ? nullptr : step_coef(a, sc);
 
     const int P = a.n_s / VEC;
     const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -499,14 +507,25 @@ k_step_matrix_free(const StepArgs a) {
     double* sK = reinterpret_cast<double*>(smem);
     const int4* sRec = reinterpret_cast<const int4*>(smem + size_t(a.mf_smem_inc) * 224);
     const uint32_t bar = uint32_t(__cvta_generic_to_shared(&s_bar));
+    // F_k of the CTA's rows ([k][rows][4], 32 B per row) staged with the same barrier
+    double* sF = reinterpret_cast<double*>(smem + size_t(a.mf_smem_inc) * 240);
+    const uint32_t nF = APPLY ? 0u : uint32_t(a.n_fields), fbytes = uint32_t(r1 - r0) * 32u;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
-        if (n_inc) {
-            mbar_expect_tx(bar, n_inc * 240u);
-            tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sK)), a.Krow + size_t(k0) * 28, n_inc * 224u, bar);
-            tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sRec)), a.fan + k0, n_inc * 16u, bar);
+        if (n_inc || nF) {
+            mbar_expect_tx(bar, n_inc * 240u + nF * fbytes);
+            if (n_inc) {
+                tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sK)), a.Krow + size_t(k0) * 28, n_inc * 224u, bar);
+                tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sRec)), a.fan + k0, n_inc * 16u, bar);
+            }
+            for (int k = 0; k < int(nF); ++k)
+                tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sF + size_t(k) * R * 4)),
+                             a.Fk + (size_t(k) * size_t(a.fk_rows) + size_t(r0)) * 4, fbytes, bar);
         }
-        if (!APPLY) load_coeffs(a, double(sc.step) * a.dt, s_coef);
+        if (!APPLY) {
+            const double* cb = step_coef(a, sc);
+            for (int k = 0; k < a.n_fields; ++k) s_coef[k] = cb[k];
+        }
     }
     __syncthreads();
 
@@ -529,9 +548,10 @@ k_step_matrix_free(const StepArgs a) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) uo[d] = ld_ro<VEC>(un_base + (i * 3 + d) * n_s);
     }
-    double* slot = reinterpret_cast<double*>(smem + size_t(a.mf_smem_inc) * 240) + size_t(threadIdx.x) * 6 * VEC;
+    double* slot = reinterpret_cast<double*>(smem + size_t(a.mf_smem_inc) * 240 + size_t(a.n_fields) * R * 32) +
+                   size_t(threadIdx.x) * 6 * VEC;
     if (!APPLY && valid) upd_load_async<VEC>(a, sc, i, s0, slot);
-    if (n_inc) mbar_wait(bar, 0);
+    if (n_inc || nF) mbar_wait(bar, 0);
     if (!valid) return;
 
     // 32-bit element offsets (V * 3 * N_s and F * N_s stay below 2^31 up to config c5)
@@ -590,14 +610,225 @@ k_step_matrix_free(const StepArgs a) {
         store_y<VEC>(a, i, s0, y);
     } else {
         Upd<VEC> upd;
-        upd_collect<VEC>(a, s_coef, i, slot, upd);
+        upd_collect<VEC>(a, s_coef, i, slot, sF + lr * 4, R * 4, upd);
 #pragma unroll
         for (int d = 0; d < 3; ++d) upd.un[d] = uo[d];
         upd_store<VEC>(a, sc, i, s0, y, upd);
     }
 }
 
+// ---- F2p: the same step with a per-warp cp.async pipeline -------------------------------
+// One warp advances pipe_rows consecutive rows for 64 realisations (lane l: s0 + 2l, +1).
+// Everything a row needs is a sequence of "items", each one ring stage of 64 B per lane
+// (4 x 16 B chunks, copied by the lane that reads them, cp.async.cg) plus, for incidences,
+// the shared K^ row and fan record (224 + 16 B, copied by lanes 0..14):
+//   R0 {u_n[i] d0..2, c1[i]}   R2 {u_n[first chain's n_prev] d0..2, c3[i]}
+//   I_k {u_n[n_next] d0..2, alpha[e]} + K^ row k      R1 {u_{n-1}[i] d0..2, c2[i]}
+// The warp keeps D items in flight (cp.async.commit_group per item, wait_group D-1 before
+// consuming one) with no register cost for the loads in flight, across row boundaries.
+// The arithmetic (order included) is exactly k_step_matrix_free's, so results are
+// bit-identical to it.
+constexpr int kPipeWarps = 4;
+constexpr int kPipeStageLane = 4 * 512;      // 4 chunks x 32 lanes x 16 B
+constexpr int kPipeStageK = 256;             // K^ row 224 B + fan record 16 B (+ pad)
+
+__host__ __device__ constexpr int pipe_warp_bytes(int D, int cap) {
+    return D * (kPipeStageLane + kPipeStageK) + cap * 16;
+}
+
+__device__ __forceinline__ void cp16(void* dst_smem, const void* src) {
+    const uint32_t d = uint32_t(__cvta_generic_to_shared(dst_smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
+struct PipeCursor {      // producer position: row i, item pos (0 R0, 1 R2, 2.. incidences, last R1)
+    int64_t i;
+    int32_t pos, kb, ke;
+};
+
+template <int D>
+__device__ __forceinline__ void pipe_issue(const StepArgs& a, const StepCtx& sc, PipeCursor& pc, int64_t r1,
+                                           int32_t k0, const int4* srec, unsigned char* wbase, int stage, int lane,
+                                           int s0) {
+    if (pc.i < r1) {
+        const int n_s = a.n_s;
+        double* L = reinterpret_cast<double*>(wbase + stage * kPipeStageLane) + lane * 2;   // chunk c: + c * 64 doubles
+        unsigned char* Ks = wbase + D * kPipeStageLane + stage * kPipeStageK;
+        const int32_t n_inc = pc.ke - pc.kb;
+        const int64_t i = pc.i;
+        if (pc.pos == 0) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) cp16(L + d * 64, sc.un + (i * 3 + d) * n_s + s0);
+            cp16(L + 3 * 64, a.c1 + i * n_s + s0);
+        } else if (pc.pos == 1) {
+            const int64_t q = srec[pc.kb - k0].y;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) cp16(L + d * 64, sc.un + (q * 3 + d) * n_s + s0);
+            if (a.c3a) cp16(L + 3 * 64, a.c3a + i * n_s + s0);
+        } else if (pc.pos < 2 + n_inc) {
+            const int32_t k = pc.kb + pc.pos - 2;
+            const int4 r = srec[k - k0];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) cp16(L + d * 64, sc.un + (int64_t(r.z) * 3 + d) * n_s + s0);
+            cp16(L + 3 * 64, a.alpha + int64_t(r.x) * n_s + s0);
+            if (lane < 14) cp16(Ks + lane * 16, a.Krow + int64_t(k) * 28 + lane * 2);
+            else if (lane == 14) cp16(Ks + 224, a.fan + k);
+        } else {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) cp16(L + d * 64, sc.uo + (i * 3 + d) * n_s + s0);
+            if (a.c2a) cp16(L + 3 * 64, a.c2a + i * n_s + s0);
+        }
+        // advance (R2 only when the row has incidences)
+        if (pc.pos == 0) pc.pos = n_inc > 0 ? 1 : 2;
+        else if (pc.pos < 2 + n_inc) ++pc.pos;
+        else {
+            ++pc.i;
+            if (pc.i < r1) {
+                pc.kb = pc.ke;
+                pc.ke = __ldg(a.inc_ptr + pc.i + 1);
+            }
+            pc.pos = 0;
+        }
+    }
+    cp_commit();          // one group per item, empty past the end: the wait count stays D - 1
+}
+
+template <int D, int NS>
+#ifndef PIPE_MINB
+#define PIPE_MINB 1
+#endif
+__global__ void __launch_bounds__(kPipeWarps * 32, PIPE_MINB)
+k_step_mf_pipe(const StepArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double s_coef[kMaxFields];
+    const StepCtx sc = step_ctx(a);
+    if (threadIdx.x == 0) {
+        const double* cb = step_coef(a, sc);
+        for (int k = 0; k < a.n_fields; ++k) s_coef[k] = cb[k];
+    }
+    __syncthreads();
+
+    const int lane = int(threadIdx.x) & 31, wib = int(threadIdx.x) >> 5;
+    const int64_t r0 = a.row0 + (int64_t(blockIdx.x) * kPipeWarps + wib) * a.pipe_rows;
+    const int64_t r1 = min(r0 + a.pipe_rows, a.row0 + a.V);
+    if (r0 >= r1) return;
+    const int n_s = NS ? NS : a.n_s;
+    const int s0 = int(blockIdx.y) * 64 + lane * 2;
+    unsigned char* wbase = smem + size_t(wib) * pipe_warp_bytes(D, a.pipe_cap);
+    int4* srec = reinterpret_cast<int4*>(wbase + D * (kPipeStageLane + kPipeStageK));
+
+    // fan records of the warp's rows (contiguous incidences) -> shared memory
+    const int32_t k0 = __ldg(a.inc_ptr + r0), k1 = __ldg(a.inc_ptr + r1);
+    for (int32_t q = lane; q < k1 - k0; q += 32) cp16(srec + q, a.fan + k0 + q);
+    cp_commit();
+    cp_wait<0>();
+    __syncwarp();
+
+    PipeCursor pc{r0, 0, k0, __ldg(a.inc_ptr + r0 + 1)};
+#pragma unroll
+    for (int t = 0; t < D; ++t) pipe_issue<D>(a, sc, pc, r1, k0, srec, wbase, t, lane, s0);
+
+    int stage = 0;
+    auto take = [&]() -> const double* {          // wait for the oldest item; its lane chunks
+        cp_wait<D - 1>();
+        __syncwarp();
+        return reinterpret_cast<const double*>(wbase + stage * kPipeStageLane) + lane * 2;
+    };
+    auto next = [&]() {                           // release it, refill the stage D items ahead
+        __syncwarp();
+        pipe_issue<D>(a, sc, pc, r1, k0, srec, wbase, stage, lane, s0);
+        stage = stage + 1 == D ? 0 : stage + 1;
+    };
+
+    int32_t kb = k0;
+    for (int64_t i = r0; i < r1; ++i) {
+        const int32_t ke = __ldg(a.inc_ptr + i + 1);
+        Upd<2> upd;
+        upd.fx = a.fixed ? __ldg(a.fixed + i) : uint8_t(0);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double f = 0.0;
+            for (int k = 0; k < a.n_fields; ++k) f = fma(s_coef[k], __ldg(a.Fk + (int64_t(k) * a.fk_rows + i) * 4 + c), f);
+            upd.f[c] = f;
+        }
+        Vec<2> uo[3], up[3];
+        {   // R0
+            const double* L = take();
+#pragma unroll
+            for (int d = 0; d < 3; ++d) { uo[d].v[0] = L[d * 64]; uo[d].v[1] = L[d * 64 + 1]; }
+            upd.c1.v[0] = L[3 * 64];
+            upd.c1.v[1] = L[3 * 64 + 1];
+            next();
+        }
+        upd.c2.v[0] = upd.c2.v[1] = a.c2;
+        upd.c3.v[0] = upd.c3.v[1] = a.c3;
+        if (kb < ke) {   // R2
+            const double* L = take();
+#pragma unroll
+            for (int d = 0; d < 3; ++d) { up[d].v[0] = L[d * 64]; up[d].v[1] = L[d * 64 + 1]; }
+            if (a.c3a) { upd.c3.v[0] = L[3 * 64]; upd.c3.v[1] = L[3 * 64 + 1]; }
+            next();
+        }
+        double y[3][2];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) y[c][0] = y[c][1] = 0.0;
+        for (int32_t k = kb; k < ke; ++k) {
+            const double* L = take();
+            const double* K = reinterpret_cast<const double*>(wbase + D * kPipeStageLane + stage * kPipeStageK);
+            const int4 rec = srec[k - k0];
+            if (rec.w && k != kb) {               // a further chain (non-manifold vertex): rare
+#pragma unroll
+                for (int d = 0; d < 3; ++d) up[d] = ld_ro<2>(sc.un + (int64_t(rec.y) * 3 + d) * n_s + s0);
+            }
+            Vec<2> un[3], al;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) { un[d].v[0] = L[d * 64]; un[d].v[1] = L[d * 64 + 1]; }
+            al.v[0] = L[3 * 64];
+            al.v[1] = L[3 * 64 + 1];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double t[2] = {0.0, 0.0};
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const double k_own = K[9 * c + d], k_prev = K[9 * c + 3 + d], k_next = K[9 * c + 6 + d];
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) {
+                        t[v] = fma(k_own, uo[d].v[v], t[v]);
+                        t[v] = fma(k_prev, up[d].v[v], t[v]);
+                        t[v] = fma(k_next, un[d].v[v], t[v]);
+                    }
+                }
+#pragma unroll
+                for (int v = 0; v < 2; ++v) y[c][v] = fma(al.v[v], t[v], y[c][v]);
+            }
+#pragma unroll
+            for (int d = 0; d < 3; ++d) up[d] = un[d];
+            next();
+        }
+        {   // R1: u_{n-1}, then the update of row i
+            const double* L = take();
+#pragma unroll
+            for (int d = 0; d < 3; ++d) { upd.uo[d].v[0] = L[d * 64]; upd.uo[d].v[1] = L[d * 64 + 1]; }
+            if (a.c2a) { upd.c2.v[0] = L[3 * 64]; upd.c2.v[1] = L[3 * 64 + 1]; }
+            next();
+        }
+#pragma unroll
+        for (int d = 0; d < 3; ++d) upd.un[d] = uo[d];
+        upd_store<2>(a, sc, i, s0, y, upd);
+        kb = ke;
+    }
+    cp_wait<0>();
+}
+
 __global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
+
+__global__ void k_seed_coeffs(const StepArgs a) {
+    const int64_t step = *a.step_base;
+    load_coeffs(a, double(step) * a.dt, a.coef_buf + (step & 1) * kMaxFields);
+}
 
 // ---- P2P halo flags (ENS_HALO_P2P) ----------------------------------------------------
 __global__ void k_halo_signal(int32_t n_out, unsigned long long* const* out_flag, const int64_t* step_base,
@@ -717,7 +948,8 @@ template <int VEC, bool APPLY, int BATCH, int MINB, int NS>
 static cudaError_t launch_a2_ns(const StepArgs& a, cudaStream_t st) {
     if (a.V == 0) return cudaSuccess;
     const int P = a.n_s / VEC;
-    const size_t smem = size_t(a.mf_smem_inc) * 240 + size_t(a.mf_rows * a.mf_groups) * 6 * VEC * sizeof(double);
+    const size_t smem = size_t(a.mf_smem_inc) * 240 + size_t(a.n_fields) * a.mf_rows * 32 +
+                        size_t(a.mf_rows * a.mf_groups) * 6 * VEC * sizeof(double);
     static bool attr_set = false;      // per template instance
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS>,
@@ -819,8 +1051,64 @@ int pick_vec_mf(int32_t n_s) {
     return 2;
 }
 
+template <int D, int NS>
+static cudaError_t launch_pipe_ns(const StepArgs& a, cudaStream_t st) {
+    const size_t smem = size_t(kPipeWarps) * size_t(pipe_warp_bytes(D, a.pipe_cap));
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_step_mf_pipe<D, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int64_t warps = (a.V + a.pipe_rows - 1) / a.pipe_rows;
+    dim3 grid(unsigned((warps + kPipeWarps - 1) / kPipeWarps), unsigned(a.n_s / 64));
+    k_step_mf_pipe<D, NS><<<grid, kPipeWarps * 32, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+bool mf_pipe_enabled() {          // read at context creation (tests switch it per context)
+    const char* e = std::getenv("ENS_MF_PIPE");      // measured slower on c2 (80-112 vs 77 us): off
+    return e ? std::atoi(e) != 0 : false;
+}
+
+int mf_pipe_rows() {
+    const char* e = std::getenv("ENS_MF_PIPE_ROWS");
+    return e ? std::max(1, std::atoi(e)) : 4;
+}
+
+int pipe_depth() {
+    static int v = [] {
+        const char* e = std::getenv("ENS_MF_PIPE_D");
+        return e ? std::atoi(e) : 4;
+    }();
+    return v;
+}
+
+static cudaError_t launch_pipe(const StepArgs& a, cudaStream_t st) {
+    if (a.V == 0) return cudaSuccess;
+    const int D = pipe_depth();
+    if (a.n_s == 64) {
+        if (D == 2) return launch_pipe_ns<2, 64>(a, st);
+        if (D == 3) return launch_pipe_ns<3, 64>(a, st);
+        if (D == 6) return launch_pipe_ns<6, 64>(a, st);
+        return launch_pipe_ns<4, 64>(a, st);
+    }
+    if (a.n_s == 128) {
+        if (D == 2) return launch_pipe_ns<2, 128>(a, st);
+        if (D == 3) return launch_pipe_ns<3, 128>(a, st);
+        if (D == 6) return launch_pipe_ns<6, 128>(a, st);
+        return launch_pipe_ns<4, 128>(a, st);
+    }
+    if (D == 2) return launch_pipe_ns<2, 0>(a, st);
+    if (D == 3) return launch_pipe_ns<3, 0>(a, st);
+    if (D == 6) return launch_pipe_ns<6, 0>(a, st);
+    return launch_pipe_ns<4, 0>(a, st);
+}
+
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
     const bool ap = a.y_out != nullptr;
+    if (!ap && a.pipe_rows > 0 && a.n_s % 64 == 0) return launch_pipe(a, st);
     const int vec = pick_vec_mf(a.n_s);
     const int var = mf_variant();
     if (vec == 4) return ap ? launch_a2<4, true, 1, 1>(a, st) : launch_a2<4, false, 1, 1>(a, st);
@@ -832,6 +1120,11 @@ cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
     }
     if (var == 3) return ap ? launch_a2<1, true, 1, 4>(a, st) : launch_a2<1, false, 1, 4>(a, st);
     return ap ? launch_a2<1, true, 2, 3>(a, st) : launch_a2<1, false, 2, 3>(a, st);
+}
+
+cudaError_t launch_seed_coeffs(const StepArgs& a, cudaStream_t st) {
+    k_seed_coeffs<<<1, 1, 0, st>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st) {
