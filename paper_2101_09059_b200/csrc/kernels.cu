@@ -263,7 +263,9 @@ __device__ __forceinline__ void upd_collect(const StepArgs& a, const double* coe
 #pragma unroll
         for (int v = 0; v < VEC; ++v) u.uo[c].v[v] = slot[(3 + c) * VEC + v];
         double f = 0.0;
-        for (int k = 0; k < a.n_fields; ++k) f = fma(coef[k], fk[k * fk_stride + c], f);
+#pragma unroll
+        for (int k = 0; k < kMaxFields; ++k)
+            if (k < a.n_fields) f = fma(coef[k], fk[k * fk_stride + c], f);
         u.f[c] = f;
     }
 }
@@ -499,7 +501,10 @@ k_step_matrix_free(const StepArgs a) {
     __shared__ __align__(8) uint64_t s_bar;
 
     const StepCtx sc = step_ctx(a);
-    const int G = a.mf_groups, R = a.mf_rows;
+    // realisation groups per row: compile-time for the templated N_s (the host sets
+    // mf_groups = min(N_s / VEC, 256)), so the thread -> (row, group) split is a shift
+    const int G = NS ? (NS / VEC < 256 ? NS / VEC : 256) : a.mf_groups;
+    const int R = a.mf_rows;
     const int64_t r0 = a.row0 + int64_t(blockIdx.x) * R;
     const int64_t r1 = min(r0 + R, a.row0 + a.V);
     const int32_t k0 = __ldg(a.inc_ptr + r0), k1 = __ldg(a.inc_ptr + r1);
@@ -576,14 +581,9 @@ k_step_matrix_free(const StepArgs a) {
                 al[j] = ld_ro<VEC>(al_base + rec[j].x * n_s);
             }
         }
-#pragma unroll
-        for (int j = 0; j < BATCH; ++j) {
-            if (k + j >= ke) break;
-            if (rec[j].w && k + j != kb) {       // a further chain (non-manifold vertex): rare
-#pragma unroll
-                for (int d = 0; d < 3; ++d) up[d] = ld_ro<VEC>(un_base + (rec[j].y * W3 + d * n_s));
-            }
-            const double* K = sK + (k + j) * 28;
+        // incidence (e, i, prev, next): y += alpha_e (K_own u_i + K_prev u_prev + K_next u_next)
+        auto incidence = [&](const Vec<VEC> (&prev)[3], const Vec<VEC> (&next)[3], const Vec<VEC>& alj,
+                             const double* K) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 double t[VEC];
@@ -595,15 +595,36 @@ k_step_matrix_free(const StepArgs a) {
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) {
                         t[v] = fma(k_own, uo[d].v[v], t[v]);
-                        t[v] = fma(k_prev, up[d].v[v], t[v]);
-                        t[v] = fma(k_next, un[j][d].v[v], t[v]);
+                        t[v] = fma(k_prev, prev[d].v[v], t[v]);
+                        t[v] = fma(k_next, next[d].v[v], t[v]);
                     }
                 }
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) y[c][v] = fma(al[j].v[v], t[v], y[c][v]);
+                for (int v = 0; v < VEC; ++v) y[c][v] = fma(alj.v[v], t[v], y[c][v]);
             }
+        };
+        // the previous neighbour of incidence j is next(j - 1) (carried in registers, no
+        // copies), except at the start of a further chain (non-manifold vertex: rare)
 #pragma unroll
-            for (int d = 0; d < 3; ++d) up[d] = un[j][d];
+        for (int j = 0; j < BATCH; ++j) {
+            if (k + j >= ke) break;
+            const double* K = sK + (k + j) * 28;
+            const bool restart = rec[j].w && k + j != kb;
+            if (restart) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d) up[d] = ld_ro<VEC>(un_base + (rec[j].y * W3 + d * n_s));
+            }
+            if (j == 0 || restart) incidence(up, un[j], al[j], K);
+            else incidence(un[j > 0 ? j - 1 : 0], un[j], al[j], K);
+        }
+        {
+            const int last = min(BATCH, ke - k) - 1;      // carry next(last) into the next batch
+#pragma unroll
+            for (int j = 0; j < BATCH; ++j)
+                if (j == last) {
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) up[d] = un[j][d];
+                }
         }
     }
     if constexpr (APPLY) {
