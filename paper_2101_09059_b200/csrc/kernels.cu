@@ -493,46 +493,43 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     }
 }
 
-template <int VEC, bool APPLY, int BATCH, int MINB, int NS>
-__global__ void __launch_bounds__(kThreads, MINB)
-k_step_matrix_free(const StepArgs a) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ double s_coef[kMaxFields];
-    __shared__ __align__(8) uint64_t s_bar;
+// Tile = the mf_rows consecutive rows [r0, r1) of one CTA pass.  Its shared-memory image:
+// K^ rows (224 B per incidence), fan records (16 B), F_k rows ([k][R][4]); issued by one
+// thread as 1-D TMA bulk copies completing on `bar`.
+__device__ __forceinline__ size_t mf_tile_bytes(const StepArgs& a) {
+    return size_t(a.mf_smem_inc) * 240 + size_t(a.n_fields) * a.mf_rows * 32;
+}
 
-    const StepCtx sc = step_ctx(a);
+template <bool APPLY>
+__device__ __forceinline__ void mf_issue_tile(const StepArgs& a, int64_t r0, int64_t r1, unsigned char* tile,
+                                              uint32_t bar) {
+    const int32_t k0 = __ldg(a.inc_ptr + r0), k1 = __ldg(a.inc_ptr + r1);
+    const uint32_t n_inc = uint32_t(k1 - k0);
+    const uint32_t nF = APPLY ? 0u : uint32_t(a.n_fields), fbytes = uint32_t(r1 - r0) * 32u;
+    double* sF = reinterpret_cast<double*>(tile + size_t(a.mf_smem_inc) * 240);
+    mbar_expect_tx(bar, n_inc * 240u + nF * fbytes);      // arrives even when nothing is copied
+    if (n_inc) {
+        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(tile)), a.Krow + size_t(k0) * 28, n_inc * 224u, bar);
+        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(tile + size_t(a.mf_smem_inc) * 224)), a.fan + k0,
+                     n_inc * 16u, bar);
+    }
+    for (int k = 0; k < int(nF); ++k)
+        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sF + size_t(k) * a.mf_rows * 4)),
+                     a.Fk + (size_t(k) * size_t(a.fk_rows) + size_t(r0)) * 4, fbytes, bar);
+}
+
+// One thread's share of a tile: row r0 + threadIdx.x / G, realisations of group g.
+template <int VEC, bool APPLY, int BATCH, int NS>
+__device__ __forceinline__ void mf_tile_rows(const StepArgs& a, const StepCtx& sc, const double* s_coef, int64_t r0,
+                                             int64_t r1, const unsigned char* tile, double* slot, uint32_t bar,
+                                             uint32_t phase) {
     // realisation groups per row: compile-time for the templated N_s (the host sets
     // mf_groups = min(N_s / VEC, 256)), so the thread -> (row, group) split is a shift
     const int G = NS ? (NS / VEC < 256 ? NS / VEC : 256) : a.mf_groups;
     const int R = a.mf_rows;
-    const int64_t r0 = a.row0 + int64_t(blockIdx.x) * R;
-    const int64_t r1 = min(r0 + R, a.row0 + a.V);
-    const int32_t k0 = __ldg(a.inc_ptr + r0), k1 = __ldg(a.inc_ptr + r1);
-    const uint32_t n_inc = uint32_t(k1 - k0);
-    double* sK = reinterpret_cast<double*>(smem);
-    const int4* sRec = reinterpret_cast<const int4*>(smem + size_t(a.mf_smem_inc) * 224);
-    const uint32_t bar = uint32_t(__cvta_generic_to_shared(&s_bar));
-    // F_k of the CTA's rows ([k][rows][4], 32 B per row) staged with the same barrier
-    double* sF = reinterpret_cast<double*>(smem + size_t(a.mf_smem_inc) * 240);
-    const uint32_t nF = APPLY ? 0u : uint32_t(a.n_fields), fbytes = uint32_t(r1 - r0) * 32u;
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        if (n_inc || nF) {
-            mbar_expect_tx(bar, n_inc * 240u + nF * fbytes);
-            if (n_inc) {
-                tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sK)), a.Krow + size_t(k0) * 28, n_inc * 224u, bar);
-                tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sRec)), a.fan + k0, n_inc * 16u, bar);
-            }
-            for (int k = 0; k < int(nF); ++k)
-                tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(sF + size_t(k) * R * 4)),
-                             a.Fk + (size_t(k) * size_t(a.fk_rows) + size_t(r0)) * 4, fbytes, bar);
-        }
-        if (!APPLY) {
-            const double* cb = step_coef(a, sc);
-            for (int k = 0; k < a.n_fields; ++k) s_coef[k] = cb[k];
-        }
-    }
-    __syncthreads();
+    const double* sK = reinterpret_cast<const double*>(tile);
+    const int4* sRec = reinterpret_cast<const int4*>(tile + size_t(a.mf_smem_inc) * 224);
+    const double* sF = reinterpret_cast<const double*>(tile + size_t(a.mf_smem_inc) * 240);
 
     const int P = a.n_s / VEC;
     const int lr = int(threadIdx.x) / G;
@@ -553,15 +550,14 @@ k_step_matrix_free(const StepArgs a) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) uo[d] = ld_ro<VEC>(un_base + (i * 3 + d) * n_s);
     }
-    double* slot = reinterpret_cast<double*>(smem + size_t(a.mf_smem_inc) * 240 + size_t(a.n_fields) * R * 32) +
-                   size_t(threadIdx.x) * 6 * VEC;
     if (!APPLY && valid) upd_load_async<VEC>(a, sc, i, s0, slot);
-    if (n_inc || nF) mbar_wait(bar, 0);
+    mbar_wait(bar, phase);
     if (!valid) return;
 
     // 32-bit element offsets (V * 3 * N_s and F * N_s stay below 2^31 up to config c5)
     const int W3 = 3 * n_s;
     const double* al_base = a.alpha + s0;
+    const int32_t k0 = __ldg(a.inc_ptr + r0);
     const int32_t kb = __ldg(a.inc_ptr + i) - k0, ke = __ldg(a.inc_ptr + i + 1) - k0;
     if (kb < ke) {                               // the row's first chain starts at kb
         const int4 r = sRec[kb];
@@ -636,6 +632,30 @@ k_step_matrix_free(const StepArgs a) {
         for (int d = 0; d < 3; ++d) upd.un[d] = uo[d];
         upd_store<VEC>(a, sc, i, s0, y, upd);
     }
+}
+
+template <int VEC, bool APPLY, int BATCH, int MINB, int NS>
+__global__ void __launch_bounds__(kThreads, MINB)
+k_step_matrix_free(const StepArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double s_coef[kMaxFields];
+    __shared__ __align__(8) uint64_t s_bar;
+
+    const StepCtx sc = step_ctx(a);
+    const int64_t r0 = a.row0 + int64_t(blockIdx.x) * a.mf_rows;
+    const int64_t r1 = min(r0 + a.mf_rows, a.row0 + a.V);
+    const uint32_t bar = uint32_t(__cvta_generic_to_shared(&s_bar));
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mf_issue_tile<APPLY>(a, r0, r1, smem, bar);
+        if (!APPLY) {
+            const double* cb = step_coef(a, sc);
+            for (int k = 0; k < a.n_fields; ++k) s_coef[k] = cb[k];
+        }
+    }
+    __syncthreads();
+    double* slot = reinterpret_cast<double*>(smem + mf_tile_bytes(a)) + size_t(threadIdx.x) * 6 * VEC;
+    mf_tile_rows<VEC, APPLY, BATCH, NS>(a, sc, s_coef, r0, r1, smem, slot, bar, 0);
 }
 
 // ---- F2p: the same step with a per-warp cp.async pipeline -------------------------------
