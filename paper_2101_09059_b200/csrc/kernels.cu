@@ -645,15 +645,19 @@ k_step_matrix_free(const StepArgs a) {
     const int64_t r0 = a.row0 + int64_t(blockIdx.x) * a.mf_rows;
     const int64_t r1 = min(r0 + a.mf_rows, a.row0 + a.V);
     const uint32_t bar = uint32_t(__cvta_generic_to_shared(&s_bar));
+    if (threadIdx.x == 0) mbar_init(bar, 1);
+    __syncthreads();
+    // Only the barrier's initialisation is waited for here: thread 0's global loads (the
+    // incidence range, the load coefficients) and the TMA issue overlap the other threads'
+    // own loads.  s_coef is written before the expect_tx arrive (release), and read after
+    // the mbarrier wait (acquire).
     if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        mf_issue_tile<APPLY>(a, r0, r1, smem, bar);
         if (!APPLY) {
             const double* cb = step_coef(a, sc);
             for (int k = 0; k < a.n_fields; ++k) s_coef[k] = cb[k];
         }
+        mf_issue_tile<APPLY>(a, r0, r1, smem, bar);
     }
-    __syncthreads();
     double* slot = reinterpret_cast<double*>(smem + mf_tile_bytes(a)) + size_t(threadIdx.x) * 6 * VEC;
     mf_tile_rows<VEC, APPLY, BATCH, NS>(a, sc, s_coef, r0, r1, smem, slot, bar, 0);
 }
