@@ -45,7 +45,6 @@ struct Part {
     int4* d_fan = nullptr;
     double *d_Krow = nullptr, *d_alpha = nullptr;
     int32_t mf_rows = 1, mf_groups = 1, mf_smem_inc = 0;
-    int32_t pipe_rows = 0, pipe_cap = 0;                  // pipelined matrix-free kernel
     int32_t *d_sym_lptr = nullptr, *d_sym_lidx = nullptr, *d_sym_lcol = nullptr, *d_sym_scol = nullptr;
     int2* d_sym_urange = nullptr;
     int64_t n_stored = 0;                                  // value blocks held (assembled kernels)
@@ -306,8 +305,6 @@ ens::StepArgs part_args(const ens_ctx* c, const Part& p) {
     a.mf_rows = p.mf_rows;
     a.mf_groups = p.mf_groups;
     a.mf_smem_inc = p.mf_smem_inc;
-    a.pipe_rows = p.pipe_rows;
-    a.pipe_cap = p.pipe_cap;
     a.sym_lptr = p.d_sym_lptr;
     a.sym_lidx = p.d_sym_lidx;
     a.sym_lcol = p.d_sym_lcol;
@@ -675,23 +672,6 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
         }
         if (int64_t(P.mf_smem_inc) * 240 > 200 * 1024)
             return fail(c, ENS_E_UNSUPPORTED, "a node has too many incident elements for the matrix-free kernel");
-        // pipelined variant (N_s % 64 == 0): rows per warp such that any window of that many
-        // consecutive rows (launches start at any row) has <= 96 incidences
-        P.pipe_rows = P.pipe_cap = 0;
-        if (c->n_s % 64 == 0 && ens::mf_pipe_enabled()) {
-            for (int32_t rw = ens::mf_pipe_rows(); rw >= 1; rw /= 2) {
-                int32_t mx = 0;
-                for (int64_t r = 0; r < P.n_own; ++r) {
-                    const int64_t r1 = std::min<int64_t>(r + rw, P.n_own);
-                    mx = std::max(mx, ip[size_t(r1)] - ip[size_t(r)]);
-                }
-                if (mx <= 96) {
-                    P.pipe_rows = rw;
-                    P.pipe_cap = (mx + 7) / 8 * 8;
-                    break;
-                }
-            }
-        }
         static_assert(sizeof(ens::FanRec) == sizeof(int4), "FanRec layout");
         RC_TRY(upload(c, &P.d_inc_ptr, ip.data(), ip.size()));
         RC_TRY(upload(c, &P.d_fan, reinterpret_cast<const int4*>(rec.data()), rec.size()));

@@ -35,8 +35,6 @@ struct StepArgs {
     int32_t mf_rows = 1;                // rows per CTA
     int32_t mf_groups = 1;              // realisation groups (threads) per row per CTA
     int32_t mf_smem_inc = 0;            // max incidences staged by one CTA
-    int32_t pipe_rows = 0;              // pipelined a2: consecutive rows per warp (0 = not built)
-    int32_t pipe_cap = 0;               // max incidences of any pipe_rows consecutive rows
     // update coefficients
     const double* c1 = nullptr;
     const double* c2a = nullptr;        // null => scalars c2, c3
@@ -88,8 +86,6 @@ cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st);
 // realisations per thread of the step kernels for a given N_s (4, 2 or 1)
 int pick_vec(int32_t n_s);      // assembled kernel
 int pick_vec_mf(int32_t n_s);   // matrix-free kernel
-bool mf_pipe_enabled();         // pipelined matrix-free variant (ENS_MF_PIPE=1; default off)
-int mf_pipe_rows();             // its rows per warp (ENS_MF_PIPE_ROWS, default 4)
 // coef_buf[(step & 1)] = the load coefficients of step *step_base (after host changes)
 cudaError_t launch_seed_coeffs(const StepArgs& a, cudaStream_t st);
 // *step_base += n (after n steps were enqueued)

@@ -7,7 +7,7 @@
 // Thread mapping (assembled kernel): thread = (row i, realisation group g), VEC
 // consecutive realisations per thread, groups of one row on consecutive lanes, so that
 // every (block, entry) segment Kval[b][k][0..n_s) — n_s*8 contiguous bytes — is read by
-// consecutive lanes with 16 B (VEC = 2) or 32 B (VEC = 4) vector loads.  Each thread
+// consecutive lanes with 16 B (VEC = 2) vector loads (8 B for odd N_s, VEC = 1).  Each thread
 // accumulates its realisations sequentially in CSR block order then d = 0,1,2 with explicit
 // fma(): the per-realisation arithmetic is identical whatever N_s, VEC or the launch
 // geometry, which makes ensemble runs bit-identical to single-realisation runs.
@@ -28,8 +28,8 @@ template <> struct Vec<2> { double v[2]; };
 template <> struct Vec<4> { double v[4]; };
 
 // ---- loads -----------------------------------------------------------------------------
-// Kval is streamed exactly once per step: no L1 allocation, L2 evict-first (createpolicy /
-// the 256-bit EFL2 form), so the u_n gather working set stays resident in the 126 MB L2.
+// Kval is streamed exactly once per step: no L1 allocation, L2 evict-first (createpolicy),
+// so the u_n gather working set stays resident in the 126 MB L2.
 template <int VEC>
 __device__ __forceinline__ Vec<VEC> ld_stream(const double* p, uint64_t pol);
 
@@ -45,13 +45,6 @@ __device__ __forceinline__ Vec<2> ld_stream<2>(const double* p, uint64_t pol) {
     Vec<2> r;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
                  : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p), "l"(pol));
-    return r;
-}
-template <>
-__device__ __forceinline__ Vec<4> ld_stream<4>(const double* p, uint64_t) {
-    Vec<4> r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
-                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
     return r;
 }
 
@@ -320,7 +313,7 @@ __device__ __forceinline__ void store_y(const StepArgs& a, int64_t i, int s0, co
 }
 
 // ---- F1: fused step on the assembled per-realisation block values ----------------------
-template <int VEC, bool APPLY, bool PREF>
+template <int VEC, bool APPLY>
 __global__ void __launch_bounds__(kThreads)
 k_step_assembled(const StepArgs a) {
     const StepCtx sc = step_ctx(a);
@@ -337,7 +330,6 @@ k_step_assembled(const StepArgs a) {
     if constexpr (VEC < 4) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
 
     Upd<VEC> upd;
-    if constexpr (!APPLY && PREF) upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
 
     double y[3][VEC];
 #pragma unroll
@@ -366,7 +358,7 @@ k_step_assembled(const StepArgs a) {
     if constexpr (APPLY) {
         store_y<VEC>(a, i, s0, y);
     } else {
-        if constexpr (!PREF) upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
+        upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
         upd_store<VEC>(a, sc, i, s0, y, upd);
     }
 }
@@ -382,7 +374,7 @@ k_step_assembled(const StepArgs a) {
 // among row i's first blocks, while row j reads its own blocks last), so that read takes
 // an L2 evict_last policy and row j's later own read an evict_first one (HINT 3, default).
 // Without the policies the second reads mostly miss L2.
-template <int VEC, bool APPLY, bool PREF, int HINT>
+template <int VEC, bool APPLY, int HINT>
 __global__ void __launch_bounds__(kThreads)
 k_step_assembled_sym(const StepArgs a) {
     const StepCtx sc = step_ctx(a);
@@ -396,23 +388,18 @@ k_step_assembled_sym(const StepArgs a) {
     const int n_s = a.n_s;
 
     // L2 policies of the two reads of a stored block: pol_own for row j's own read of
-    // (j, i), pol_tr for row i's transposed read.  HINT 1: own evict_last, tr evict_first;
-    // HINT 2: own normal, tr evict_first; HINT 3: tr evict_last, own evict_first;
-    // HINT 4: tr evict_last, own normal; HINT 0: no policy.
+    // (j, i), pol_tr for row i's transposed read.  HINT 3 (default): tr evict_last, own
+    // evict_first; HINT 1 (the first guess, measured): own evict_last, tr evict_first;
+    // HINT 0: no policy.
     uint64_t pol_own = 0, pol_tr = 0;
-    if constexpr (HINT == 1 || HINT == 3 || HINT == 4) {
-        uint64_t keep, drop, norm;
+    if constexpr (HINT != 0) {
+        uint64_t keep, drop;
         asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(drop));
-        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(norm));
-        pol_own = HINT == 1 ? keep : (HINT == 3 ? drop : norm);
+        pol_own = HINT == 1 ? keep : drop;
         pol_tr = HINT == 1 ? drop : keep;
-    } else if constexpr (HINT == 2) {
-        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_own));
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_tr));
     }
     Upd<VEC> upd;
-    if constexpr (!APPLY && PREF) upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
 
     double y[3][VEC];
 #pragma unroll
@@ -460,7 +447,7 @@ k_step_assembled_sym(const StepArgs a) {
     if constexpr (APPLY) {
         store_y<VEC>(a, i, s0, y);
     } else {
-        if constexpr (!PREF) upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
+        upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
         upd_store<VEC>(a, sc, i, s0, y, upd);
     }
 }
@@ -662,212 +649,6 @@ k_step_matrix_free(const StepArgs a) {
     mf_tile_rows<VEC, APPLY, BATCH, NS>(a, sc, s_coef, r0, r1, smem, slot, bar, 0);
 }
 
-// ---- F2p: the same step with a per-warp cp.async pipeline -------------------------------
-// One warp advances pipe_rows consecutive rows for 64 realisations (lane l: s0 + 2l, +1).
-// Everything a row needs is a sequence of "items", each one ring stage of 64 B per lane
-// (4 x 16 B chunks, copied by the lane that reads them, cp.async.cg) plus, for incidences,
-// the shared K^ row and fan record (224 + 16 B, copied by lanes 0..14):
-//   R0 {u_n[i] d0..2, c1[i]}   R2 {u_n[first chain's n_prev] d0..2, c3[i]}
-//   I_k {u_n[n_next] d0..2, alpha[e]} + K^ row k      R1 {u_{n-1}[i] d0..2, c2[i]}
-// The warp keeps D items in flight (cp.async.commit_group per item, wait_group D-1 before
-// consuming one) with no register cost for the loads in flight, across row boundaries.
-// The arithmetic (order included) is exactly k_step_matrix_free's, so results are
-// bit-identical to it.
-constexpr int kPipeWarps = 4;
-constexpr int kPipeStageLane = 4 * 512;      // 4 chunks x 32 lanes x 16 B
-constexpr int kPipeStageK = 256;             // K^ row 224 B + fan record 16 B (+ pad)
-
-__host__ __device__ constexpr int pipe_warp_bytes(int D, int cap) {
-    return D * (kPipeStageLane + kPipeStageK) + cap * 16;
-}
-
-__device__ __forceinline__ void cp16(void* dst_smem, const void* src) {
-    const uint32_t d = uint32_t(__cvta_generic_to_shared(dst_smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
-
-struct PipeCursor {      // producer position: row i, item pos (0 R0, 1 R2, 2.. incidences, last R1)
-    int64_t i;
-    int32_t pos, kb, ke;
-};
-
-template <int D>
-__device__ __forceinline__ void pipe_issue(const StepArgs& a, const StepCtx& sc, PipeCursor& pc, int64_t r1,
-                                           int32_t k0, const int4* srec, unsigned char* wbase, int stage, int lane,
-                                           int s0) {
-    if (pc.i < r1) {
-        const int n_s = a.n_s;
-        double* L = reinterpret_cast<double*>(wbase + stage * kPipeStageLane) + lane * 2;   // chunk c: + c * 64 doubles
-        unsigned char* Ks = wbase + D * kPipeStageLane + stage * kPipeStageK;
-        const int32_t n_inc = pc.ke - pc.kb;
-        const int64_t i = pc.i;
-        if (pc.pos == 0) {
-#pragma unroll
-            for (int d = 0; d < 3; ++d) cp16(L + d * 64, sc.un + (i * 3 + d) * n_s + s0);
-            cp16(L + 3 * 64, a.c1 + i * n_s + s0);
-        } else if (pc.pos == 1) {
-            const int64_t q = srec[pc.kb - k0].y;
-#pragma unroll
-            for (int d = 0; d < 3; ++d) cp16(L + d * 64, sc.un + (q * 3 + d) * n_s + s0);
-            if (a.c3a) cp16(L + 3 * 64, a.c3a + i * n_s + s0);
-        } else if (pc.pos < 2 + n_inc) {
-            const int32_t k = pc.kb + pc.pos - 2;
-            const int4 r = srec[k - k0];
-#pragma unroll
-            for (int d = 0; d < 3; ++d) cp16(L + d * 64, sc.un + (int64_t(r.z) * 3 + d) * n_s + s0);
-            cp16(L + 3 * 64, a.alpha + int64_t(r.x) * n_s + s0);
-            if (lane < 14) cp16(Ks + lane * 16, a.Krow + int64_t(k) * 28 + lane * 2);
-            else if (lane == 14) cp16(Ks + 224, a.fan + k);
-        } else {
-#pragma unroll
-            for (int d = 0; d < 3; ++d) cp16(L + d * 64, sc.uo + (i * 3 + d) * n_s + s0);
-            if (a.c2a) cp16(L + 3 * 64, a.c2a + i * n_s + s0);
-        }
-        // advance (R2 only when the row has incidences)
-        if (pc.pos == 0) pc.pos = n_inc > 0 ? 1 : 2;
-        else if (pc.pos < 2 + n_inc) ++pc.pos;
-        else {
-            ++pc.i;
-            if (pc.i < r1) {
-                pc.kb = pc.ke;
-                pc.ke = __ldg(a.inc_ptr + pc.i + 1);
-            }
-            pc.pos = 0;
-        }
-    }
-    cp_commit();          // one group per item, empty past the end: the wait count stays D - 1
-}
-
-template <int D, int NS>
-#ifndef PIPE_MINB
-#define PIPE_MINB 1
-#endif
-__global__ void __launch_bounds__(kPipeWarps * 32, PIPE_MINB)
-k_step_mf_pipe(const StepArgs a) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ double s_coef[kMaxFields];
-    const StepCtx sc = step_ctx(a);
-    if (threadIdx.x == 0) {
-        const double* cb = step_coef(a, sc);
-        for (int k = 0; k < a.n_fields; ++k) s_coef[k] = cb[k];
-    }
-    __syncthreads();
-
-    const int lane = int(threadIdx.x) & 31, wib = int(threadIdx.x) >> 5;
-    const int64_t r0 = a.row0 + (int64_t(blockIdx.x) * kPipeWarps + wib) * a.pipe_rows;
-    const int64_t r1 = min(r0 + a.pipe_rows, a.row0 + a.V);
-    if (r0 >= r1) return;
-    const int n_s = NS ? NS : a.n_s;
-    const int s0 = int(blockIdx.y) * 64 + lane * 2;
-    unsigned char* wbase = smem + size_t(wib) * pipe_warp_bytes(D, a.pipe_cap);
-    int4* srec = reinterpret_cast<int4*>(wbase + D * (kPipeStageLane + kPipeStageK));
-
-    // fan records of the warp's rows (contiguous incidences) -> shared memory
-    const int32_t k0 = __ldg(a.inc_ptr + r0), k1 = __ldg(a.inc_ptr + r1);
-    for (int32_t q = lane; q < k1 - k0; q += 32) cp16(srec + q, a.fan + k0 + q);
-    cp_commit();
-    cp_wait<0>();
-    __syncwarp();
-
-    PipeCursor pc{r0, 0, k0, __ldg(a.inc_ptr + r0 + 1)};
-#pragma unroll
-    for (int t = 0; t < D; ++t) pipe_issue<D>(a, sc, pc, r1, k0, srec, wbase, t, lane, s0);
-
-    int stage = 0;
-    auto take = [&]() -> const double* {          // wait for the oldest item; its lane chunks
-        cp_wait<D - 1>();
-        __syncwarp();
-        return reinterpret_cast<const double*>(wbase + stage * kPipeStageLane) + lane * 2;
-    };
-    auto next = [&]() {                           // release it, refill the stage D items ahead
-        __syncwarp();
-        pipe_issue<D>(a, sc, pc, r1, k0, srec, wbase, stage, lane, s0);
-        stage = stage + 1 == D ? 0 : stage + 1;
-    };
-
-    int32_t kb = k0;
-    for (int64_t i = r0; i < r1; ++i) {
-        const int32_t ke = __ldg(a.inc_ptr + i + 1);
-        Upd<2> upd;
-        upd.fx = a.fixed ? __ldg(a.fixed + i) : uint8_t(0);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            double f = 0.0;
-            for (int k = 0; k < a.n_fields; ++k) f = fma(s_coef[k], __ldg(a.Fk + (int64_t(k) * a.fk_rows + i) * 4 + c), f);
-            upd.f[c] = f;
-        }
-        Vec<2> uo[3], up[3];
-        {   // R0
-            const double* L = take();
-#pragma unroll
-            for (int d = 0; d < 3; ++d) { uo[d].v[0] = L[d * 64]; uo[d].v[1] = L[d * 64 + 1]; }
-            upd.c1.v[0] = L[3 * 64];
-            upd.c1.v[1] = L[3 * 64 + 1];
-            next();
-        }
-        upd.c2.v[0] = upd.c2.v[1] = a.c2;
-        upd.c3.v[0] = upd.c3.v[1] = a.c3;
-        if (kb < ke) {   // R2
-            const double* L = take();
-#pragma unroll
-            for (int d = 0; d < 3; ++d) { up[d].v[0] = L[d * 64]; up[d].v[1] = L[d * 64 + 1]; }
-            if (a.c3a) { upd.c3.v[0] = L[3 * 64]; upd.c3.v[1] = L[3 * 64 + 1]; }
-            next();
-        }
-        double y[3][2];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) y[c][0] = y[c][1] = 0.0;
-        for (int32_t k = kb; k < ke; ++k) {
-            const double* L = take();
-            const double* K = reinterpret_cast<const double*>(wbase + D * kPipeStageLane + stage * kPipeStageK);
-            const int4 rec = srec[k - k0];
-            if (rec.w && k != kb) {               // a further chain (non-manifold vertex): rare
-#pragma unroll
-                for (int d = 0; d < 3; ++d) up[d] = ld_ro<2>(sc.un + (int64_t(rec.y) * 3 + d) * n_s + s0);
-            }
-            Vec<2> un[3], al;
-#pragma unroll
-            for (int d = 0; d < 3; ++d) { un[d].v[0] = L[d * 64]; un[d].v[1] = L[d * 64 + 1]; }
-            al.v[0] = L[3 * 64];
-            al.v[1] = L[3 * 64 + 1];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                double t[2] = {0.0, 0.0};
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const double k_own = K[9 * c + d], k_prev = K[9 * c + 3 + d], k_next = K[9 * c + 6 + d];
-#pragma unroll
-                    for (int v = 0; v < 2; ++v) {
-                        t[v] = fma(k_own, uo[d].v[v], t[v]);
-                        t[v] = fma(k_prev, up[d].v[v], t[v]);
-                        t[v] = fma(k_next, un[d].v[v], t[v]);
-                    }
-                }
-#pragma unroll
-                for (int v = 0; v < 2; ++v) y[c][v] = fma(al.v[v], t[v], y[c][v]);
-            }
-#pragma unroll
-            for (int d = 0; d < 3; ++d) up[d] = un[d];
-            next();
-        }
-        {   // R1: u_{n-1}, then the update of row i
-            const double* L = take();
-#pragma unroll
-            for (int d = 0; d < 3; ++d) { upd.uo[d].v[0] = L[d * 64]; upd.uo[d].v[1] = L[d * 64 + 1]; }
-            if (a.c2a) { upd.c2.v[0] = L[3 * 64]; upd.c2.v[1] = L[3 * 64 + 1]; }
-            next();
-        }
-#pragma unroll
-        for (int d = 0; d < 3; ++d) upd.un[d] = uo[d];
-        upd_store<2>(a, sc, i, s0, y, upd);
-        kb = ke;
-    }
-    cp_wait<0>();
-}
-
 __global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
 
 __global__ void k_seed_coeffs(const StepArgs a) {
@@ -972,20 +753,11 @@ inline unsigned grid_for(int64_t n) { return unsigned((n + kThreads - 1) / kThre
 }  // namespace
 
 
-static bool a1_prefetch() {
-    static int v = [] {
-        const char* e = std::getenv("ENS_A1_PREFETCH");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v != 0;
-}
-
 template <int VEC, bool APPLY>
 static cudaError_t launch_a1(const StepArgs& a, cudaStream_t st) {
     const int64_t n = a.V * (a.n_s / VEC);
     if (n == 0) return cudaSuccess;
-    if (a1_prefetch()) k_step_assembled<VEC, APPLY, true><<<grid_for(n), kThreads, 0, st>>>(a);
-    else k_step_assembled<VEC, APPLY, false><<<grid_for(n), kThreads, 0, st>>>(a);
+    k_step_assembled<VEC, APPLY><<<grid_for(n), kThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -1030,140 +802,42 @@ cudaError_t launch_halo_wait(int32_t n_in, const int32_t* in_q, const unsigned l
     return cudaGetLastError();
 }
 
-int pick_vec(int32_t n_s) {
-    static int vec4 = [] {
-        const char* e = std::getenv("ENS_A1_VEC4");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (vec4 && n_s % 4 == 0) return 4;
-    return n_s % 2 == 0 ? 2 : 1;
-}
-
+int pick_vec(int32_t n_s) { return n_s % 2 == 0 ? 2 : 1; }
 
 template <int VEC, bool APPLY>
 static cudaError_t launch_a1s(const StepArgs& a, cudaStream_t st) {
     const int64_t n = a.V * (a.n_s / VEC);
     if (n == 0) return cudaSuccess;
-    static int hint = [] {
+    static int hint = [] {           // L2 policies of the two reads: 3 default
         const char* e = std::getenv("ENS_A1S_HINTS");
         return e ? std::atoi(e) : 3;
     }();
     const unsigned g = grid_for(n);
-    if (hint == 1) k_step_assembled_sym<VEC, APPLY, false, 1><<<g, kThreads, 0, st>>>(a);
-    else if (hint == 2) k_step_assembled_sym<VEC, APPLY, false, 2><<<g, kThreads, 0, st>>>(a);
-    else if (hint == 3) k_step_assembled_sym<VEC, APPLY, false, 3><<<g, kThreads, 0, st>>>(a);
-    else if (hint == 4) k_step_assembled_sym<VEC, APPLY, false, 4><<<g, kThreads, 0, st>>>(a);
-    else if (a1_prefetch()) k_step_assembled_sym<VEC, APPLY, true, 0><<<g, kThreads, 0, st>>>(a);
-    else k_step_assembled_sym<VEC, APPLY, false, 0><<<g, kThreads, 0, st>>>(a);
+    if (hint == 3) k_step_assembled_sym<VEC, APPLY, 3><<<g, kThreads, 0, st>>>(a);
+    else if (hint == 1) k_step_assembled_sym<VEC, APPLY, 1><<<g, kThreads, 0, st>>>(a);
+    else k_step_assembled_sym<VEC, APPLY, 0><<<g, kThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_step_assembled_sym(const StepArgs& a, cudaStream_t st) {
     const bool apply = a.y_out != nullptr;
-    switch (pick_vec(a.n_s)) {
-        case 4: return apply ? launch_a1s<4, true>(a, st) : launch_a1s<4, false>(a, st);
-        case 2: return apply ? launch_a1s<2, true>(a, st) : launch_a1s<2, false>(a, st);
-        default: return apply ? launch_a1s<1, true>(a, st) : launch_a1s<1, false>(a, st);
-    }
+    if (pick_vec(a.n_s) == 2) return apply ? launch_a1s<2, true>(a, st) : launch_a1s<2, false>(a, st);
+    return apply ? launch_a1s<1, true>(a, st) : launch_a1s<1, false>(a, st);
 }
 
 cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st) {
     const bool apply = a.y_out != nullptr;
-    switch (pick_vec(a.n_s)) {
-        case 4: return apply ? launch_a1<4, true>(a, st) : launch_a1<4, false>(a, st);
-        case 2: return apply ? launch_a1<2, true>(a, st) : launch_a1<2, false>(a, st);
-        default: return apply ? launch_a1<1, true>(a, st) : launch_a1<1, false>(a, st);
-    }
+    if (pick_vec(a.n_s) == 2) return apply ? launch_a1<2, true>(a, st) : launch_a1<2, false>(a, st);
+    return apply ? launch_a1<1, true>(a, st) : launch_a1<1, false>(a, st);
 }
 
-// Matrix-free variants (tuning knob ENS_MF_VARIANT = 0..3):
-//   0: VEC 2, batch 1, >= 2 CTAs/SM   1: VEC 2, batch 2, >= 2 CTAs/SM
-//   2: VEC 1, batch 2, >= 3 CTAs/SM   3: VEC 1, batch 1, >= 4 CTAs/SM
-//   4: VEC 2, batch 1, >= 3 CTAs/SM   5: VEC 2, batch 2, >= 3 CTAs/SM
-//   6: VEC 4 (256-bit loads, half a warp per row), batch 1
-int mf_variant() {
-    static int v = [] {
-        const char* e = std::getenv("ENS_MF_VARIANT");
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
-}
-
-int pick_vec_mf(int32_t n_s) {
-    const int v = mf_variant();
-    if (v == 6 && n_s % 4 == 0) return 4;
-    if (v == 2 || v == 3 || n_s % 2) return 1;
-    return 2;
-}
-
-template <int D, int NS>
-static cudaError_t launch_pipe_ns(const StepArgs& a, cudaStream_t st) {
-    const size_t smem = size_t(kPipeWarps) * size_t(pipe_warp_bytes(D, a.pipe_cap));
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_step_mf_pipe<D, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             200 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
-    const int64_t warps = (a.V + a.pipe_rows - 1) / a.pipe_rows;
-    dim3 grid(unsigned((warps + kPipeWarps - 1) / kPipeWarps), unsigned(a.n_s / 64));
-    k_step_mf_pipe<D, NS><<<grid, kPipeWarps * 32, smem, st>>>(a);
-    return cudaGetLastError();
-}
-
-bool mf_pipe_enabled() {          // read at context creation (tests switch it per context)
-    const char* e = std::getenv("ENS_MF_PIPE");      // measured slower on c2 (80-112 vs 77 us): off
-    return e ? std::atoi(e) != 0 : false;
-}
-
-int mf_pipe_rows() {
-    const char* e = std::getenv("ENS_MF_PIPE_ROWS");
-    return e ? std::max(1, std::atoi(e)) : 4;
-}
-
-int pipe_depth() {
-    static int v = [] {
-        const char* e = std::getenv("ENS_MF_PIPE_D");
-        return e ? std::atoi(e) : 4;
-    }();
-    return v;
-}
-
-static cudaError_t launch_pipe(const StepArgs& a, cudaStream_t st) {
-    if (a.V == 0) return cudaSuccess;
-    const int D = pipe_depth();
-    if (a.n_s == 64) {
-        if (D == 2) return launch_pipe_ns<2, 64>(a, st);
-        if (D == 3) return launch_pipe_ns<3, 64>(a, st);
-        if (D == 6) return launch_pipe_ns<6, 64>(a, st);
-        return launch_pipe_ns<4, 64>(a, st);
-    }
-    if (a.n_s == 128) {
-        if (D == 2) return launch_pipe_ns<2, 128>(a, st);
-        if (D == 3) return launch_pipe_ns<3, 128>(a, st);
-        if (D == 6) return launch_pipe_ns<6, 128>(a, st);
-        return launch_pipe_ns<4, 128>(a, st);
-    }
-    if (D == 2) return launch_pipe_ns<2, 0>(a, st);
-    if (D == 3) return launch_pipe_ns<3, 0>(a, st);
-    if (D == 6) return launch_pipe_ns<6, 0>(a, st);
-    return launch_pipe_ns<4, 0>(a, st);
-}
+// Matrix-free: VEC 2 (even N_s), batches of 2 incidences, >= 2 CTAs/SM; VEC 1 for odd N_s
+// (batch 2, >= 3 CTAs/SM).  The variants measured and dropped are listed in DESIGN.md §5.
+int pick_vec_mf(int32_t n_s) { return n_s % 2 == 0 ? 2 : 1; }
 
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
     const bool ap = a.y_out != nullptr;
-    if (!ap && a.pipe_rows > 0 && a.n_s % 64 == 0) return launch_pipe(a, st);
-    const int vec = pick_vec_mf(a.n_s);
-    const int var = mf_variant();
-    if (vec == 4) return ap ? launch_a2<4, true, 1, 1>(a, st) : launch_a2<4, false, 1, 1>(a, st);
-    if (vec == 2) {
-        if (var == 1) return ap ? launch_a2<2, true, 2, 2>(a, st) : launch_a2<2, false, 2, 2>(a, st);
-        if (var == 4) return ap ? launch_a2<2, true, 1, 3>(a, st) : launch_a2<2, false, 1, 3>(a, st);
-        if (var == 5) return ap ? launch_a2<2, true, 2, 3>(a, st) : launch_a2<2, false, 2, 3>(a, st);
-        return ap ? launch_a2<2, true, 1, 2>(a, st) : launch_a2<2, false, 1, 2>(a, st);
-    }
-    if (var == 3) return ap ? launch_a2<1, true, 1, 4>(a, st) : launch_a2<1, false, 1, 4>(a, st);
+    if (pick_vec_mf(a.n_s) == 2) return ap ? launch_a2<2, true, 2, 2>(a, st) : launch_a2<2, false, 2, 2>(a, st);
     return ap ? launch_a2<1, true, 2, 3>(a, st) : launch_a2<1, false, 2, 3>(a, st);
 }
 

@@ -124,7 +124,7 @@ def test_ensemble_equivalence_bitexact(kernel):
         u1, up1, _, _ = one.get_state()
         assert np.array_equal(u1[0], u_all[s]) and np.array_equal(up1[0], up_all[s])
         one.close()
-    # and an N_s = 128 run (VEC = 4) whose first 8 realisations are the same fields
+    # and an N_s = 128 run (two warps per row) whose first 8 realisations are the same fields
     E2 = np.concatenate([E] * 16)
     h2 = np.concatenate([h] * 16)
     big = solver.Ensemble(m.xyz, m.tris, m.fixed, E2, h2, **kw)
@@ -502,25 +502,3 @@ def test_reassembly_rejected_for_matrix_free():
     with pytest.raises(EnsError):
         solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, kernel="matrix_free",
                         reassemble_every=10)
-
-
-@pytest.mark.parametrize("n_s", [64, 128, 192])
-@pytest.mark.parametrize("damping", ["mass", "identity"])
-def test_matrix_free_pipelined_bitexact(n_s, damping, monkeypatch):
-    """The cp.async-pipelined matrix-free kernel (k_step_mf_pipe, N_s % 64 == 0) does the
-    arithmetic of k_step_matrix_free in the same order: bit-identical states, also with
-    a jagged incidence structure (shuffled, perturbed mesh) and node partitioning."""
-    m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(24, 37), 0.02, 4), 3)
-    E, h = _mats(m, n_s, 97)
-    tr = loads.pulsatile(m.xyz, m.tris, period=0.01, systole=0.004, ramp_T=0.003)
-    kw = dict(rho=RHO, nu=NU, k_shear=KS, kernel="matrix_free", dt=5e-5, damping=damping, c_d=0.3)
-    out = []
-    for pipe, extra in (("0", {}), ("1", {}), ("1", dict(dist="node", world=3, halo="p2p"))):
-        monkeypatch.setenv("ENS_MF_PIPE", pipe)
-        ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, **kw, **extra)
-        ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
-        ens.step(133)
-        out.append(ens.get_state())
-        ens.close()
-    for o in out[1:]:
-        assert np.array_equal(out[0][0], o[0]) and np.array_equal(out[0][1], o[1])
