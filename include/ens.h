@@ -163,7 +163,11 @@ int ens_create(const ens_mesh* mesh, const ens_materials* mat, const ens_options
  *   (PAPER.md:512, 571), g_k = linear interpolation of tab_g[k][:] at tau = t mod period
  *   (period <= 0: no wrap), clamped to the end values; n_tab = 0 => g_k = 1.
  * F: [n_fields][V][3] nodal forces (dyn) in the caller's numbering, 1 <= n_fields <= 4.
- * tab_t: [n_tab] strictly increasing (s); tab_g: [n_fields][n_tab].  Copied. */
+ * tab_t: [n_tab] strictly increasing (s); tab_g: [n_fields][n_tab].  Copied before return.
+ * The first call (or one changing n_fields or n_tab) allocates and synchronises; a later
+ * call with the same shape packs the values into pinned staging and enqueues their copy on
+ * the context stream after the steps already enqueued (asynchronous, no graph rebuild):
+ * the per-window input update of a running simulation. */
 int ens_set_traction(ens_ctx* ctx, int32_t n_fields, const double* F, int32_t n_tab,
                      const double* tab_t, const double* tab_g, double period, double ramp_T);
 
@@ -176,6 +180,18 @@ int ens_step(ens_ctx* ctx, int64_t n);
 
 /* Wait for the enqueued work; report a pending divergence. */
 int ens_sync(ens_ctx* ctx);
+
+/* Snapshot of u_n without stopping the step loop (output every k steps):
+ * enqueue, after the steps enqueued so far, the layout transpose of u_n on the context
+ * stream and its device->host copy on a separate copy stream, then return.  u_n: caller
+ * HOST buffer [n_s][R][3] as ens_get_state (pinned memory recommended: pageable memory makes
+ * the copy synchronous); it must stay valid and untouched until ens_observe_wait returns.
+ * One snapshot in flight: a second ens_observe orders its transpose after the previous
+ * copy.  ens_observe_wait blocks until the copy is done, returns the snapshot's step, and
+ * reports ENS_E_DIVERGED if a non-finite value had appeared by then (ENS_E_STATE if no
+ * snapshot is in flight). */
+int ens_observe(ens_ctx* ctx, double* u_n);
+int ens_observe_wait(ens_ctx* ctx, int64_t* step);
 
 /* Copy the state to caller-owned HOST buffers (either may be NULL):
  * u_n, u_nm1: [n_s][R][3] with R = V in the caller's node numbering, except for a NODE

@@ -56,7 +56,8 @@ EXPORTS = [
     "ens_apply_stiffness", "ens_query", "ens_destroy", "ens_last_error", "ens_host_validate",
     "ens_host_pattern", "ens_host_partition", "ens_host_ghosts", "ens_host_element_stiffness",
     "ens_host_materials", "ens_create_csr", "ens_get_owned", "ens_host_halo_plan", "ens_stress",
-    "ens_displacement_stats", "ens_matern_fields", "ens_p2p_export", "ens_p2p_connect",
+    "ens_displacement_stats", "ens_matern_fields", "ens_p2p_export", "ens_p2p_connect", "ens_observe",
+    "ens_observe_wait",
 ]
 P2P_BLOB_BYTES = 256
 
@@ -107,6 +108,8 @@ def lib():
         "ens_host_halo_plan": (C.c_int, [i64, vp, vp, i32, i32, vp, vp, vp, vp, i64, P(i64), P(i64)]),
         "ens_p2p_export": (C.c_int, [vp, vp]),
         "ens_p2p_connect": (C.c_int, [vp, vp]),
+        "ens_observe": (C.c_int, [vp, vp]),
+        "ens_observe_wait": (C.c_int, [vp, P(i64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -100,6 +100,17 @@ struct ens_ctx {
     double* d_stage = nullptr;              // [n_s][V][3] ABI staging
     unsigned long long* d_flag = nullptr;
     double* d_coef = nullptr;               // [2][kMaxFields] load coefficients (StepArgs.coef_buf)
+    // asynchronous traction updates (same shape): host staging in pinned memory
+    double* h_trac = nullptr;
+    size_t h_trac_n = 0;
+    cudaEvent_t ev_trac = nullptr;          // the last traction H2D copy has consumed h_trac
+    // asynchronous observation (ens_observe): transpose on the stream, D2H on obs_stream
+    cudaStream_t obs_stream = nullptr;
+    cudaEvent_t ev_obs_ready = nullptr, ev_obs_done = nullptr;
+    double* d_obs = nullptr;
+    unsigned long long* h_obs_flag = nullptr;   // pinned copy of d_flag taken with the snapshot
+    bool obs_pending = false;
+    int64_t obs_step = 0;
     bool coef_dirty = true;                 // seed d_coef before the next step
     int64_t* d_step = nullptr;
     int32_t n_fields = 0, n_tab = 0;
@@ -213,7 +224,18 @@ void drop_graph(ens_ctx* c) {
 
 void free_all(ens_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->obs_stream) cudaStreamSynchronize(c->obs_stream);
     drop_graph(c);
+    if (c->h_trac) cudaFreeHost(c->h_trac);
+    if (c->h_obs_flag) cudaFreeHost(c->h_obs_flag);
+    if (c->ev_trac) cudaEventDestroy(c->ev_trac);
+    if (c->obs_stream) cudaStreamDestroy(c->obs_stream);
+    if (c->ev_obs_ready) cudaEventDestroy(c->ev_obs_ready);
+    if (c->ev_obs_done) cudaEventDestroy(c->ev_obs_done);
+    c->h_trac = nullptr;
+    c->h_obs_flag = nullptr;
+    c->ev_trac = c->ev_obs_ready = c->ev_obs_done = nullptr;
+    c->obs_stream = nullptr;
     for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
     c->ipc_opened.clear();
     for (void* p : c->raw_bufs) cudaFree(p);
@@ -1006,6 +1028,44 @@ int ens_set_traction(ens_ctx* c, int32_t n_fields, const double* F, int32_t n_ta
     for (int32_t k = 0; k + 1 < n_tab; ++k)
         if (!(tab_t[k] < tab_t[k + 1])) return fail(c, ENS_E_ARG, "tab_t must be strictly increasing");
     if (!std::isfinite(period) || !std::isfinite(ramp_T)) return fail(c, ENS_E_ARG, "period / ramp_T not finite");
+    // Same shape as the current traction: pack into the pinned staging and enqueue the
+    // copies on the stream (they run after the steps already enqueued), no synchronisation
+    // and no graph rebuild — the per-window input update of a running simulation.
+    size_t need = size_t(n_tab) * size_t(1 + n_fields);
+    for (const Part& p : c->parts) need += size_t(n_fields) * size_t(p.n_own) * 4;
+    if (n_fields > 0 && n_fields == c->n_fields && n_tab == c->n_tab && c->h_trac && c->h_trac_n == need) {
+        CUDA_TRY(c, cudaEventSynchronize(c->ev_trac));  // the previous update has left the staging
+        double* h = c->h_trac;
+        for (Part& p : c->parts) {
+            double* Fd = h;
+            for (int32_t k = 0; k < n_fields; ++k)
+                for (int64_t i = 0; i < p.n_own; ++i) {
+                    double* dst = Fd + (k * p.n_own + i) * 4;
+                    const double* src = F + (k * c->V + p.map_own[size_t(i)]) * 3;
+                    dst[0] = src[0];
+                    dst[1] = src[1];
+                    dst[2] = src[2];
+                    dst[3] = 0.0;
+                }
+            const size_t nb = size_t(n_fields) * size_t(p.n_own) * 4;
+            CUDA_TRY(c, cudaMemcpyAsync(p.d_Fk, Fd, nb * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            h += nb;
+        }
+        if (n_tab > 0) {
+            std::copy(tab_t, tab_t + n_tab, h);
+            std::copy(tab_g, tab_g + size_t(n_tab) * size_t(n_fields), h + n_tab);
+            CUDA_TRY(c, cudaMemcpyAsync(c->d_tab_t, h, size_t(n_tab) * sizeof(double), cudaMemcpyHostToDevice,
+                                        c->stream));
+            CUDA_TRY(c, cudaMemcpyAsync(c->d_tab_g, h + n_tab, size_t(n_tab) * size_t(n_fields) * sizeof(double),
+                                        cudaMemcpyHostToDevice, c->stream));
+        }
+        CUDA_TRY(c, cudaEventRecord(c->ev_trac, c->stream));
+        if (period != c->period || ramp_T != c->ramp_T) drop_graph(c);   // scalars of the captured steps
+        c->period = period;
+        c->ramp_T = ramp_T;
+        c->coef_dirty = true;
+        return ENS_OK;
+    }
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));       // old buffers may still be in use
     drop_graph(c);
     c->n_fields = 0;
@@ -1030,6 +1090,60 @@ int ens_set_traction(ens_ctx* c, int32_t n_fields, const double* F, int32_t n_ta
     c->period = period;
     c->ramp_T = ramp_T;
     c->coef_dirty = true;
+    // pinned staging for later same-shape updates
+    if (c->h_trac) cudaFreeHost(c->h_trac);
+    c->h_trac = nullptr;
+    c->h_trac_n = 0;
+    if (need > 0) {
+        CUDA_TRY(c, cudaHostAlloc(reinterpret_cast<void**>(&c->h_trac), need * sizeof(double), cudaHostAllocDefault));
+        c->h_trac_n = need;
+        if (!c->ev_trac) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_trac, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventRecord(c->ev_trac, c->stream));
+    }
+    return ENS_OK;
+}
+
+int ens_observe(ens_ctx* c, double* u_n) {
+    if (!c || !u_n) return fail(c, ENS_E_ARG, "NULL argument");
+    if (!c->obs_stream) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->obs_stream, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_obs_ready, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_obs_done, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaHostAlloc(reinterpret_cast<void**>(&c->h_obs_flag), sizeof(unsigned long long),
+                                  cudaHostAllocDefault));
+        const int64_t rows = c->multi ? c->parts[0].n_own : c->V;
+        RC_TRY(dalloc(c, &c->d_obs, size_t(rows) * 3 * size_t(c->n_s)));
+    }
+    const int64_t Vabi = c->multi ? c->parts[0].n_own : c->V;
+    if (c->obs_pending) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_obs_done, 0));   // d_obs is free
+    for (Part& p : c->parts) {
+        const double* src = (c->step & 1) ? p.d_u1 : p.d_u0;     // u_n = buf[step & 1]
+        CUDA_TRY(c, ens::launch_dev_to_abi(p.n_own, c->n_s, p.d_map_abi, Vabi, src, c->d_obs, c->stream));
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev_obs_ready, c->stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->obs_stream, c->ev_obs_ready, 0));
+    CUDA_TRY(c, cudaMemcpyAsync(u_n, c->d_obs, size_t(Vabi) * 3 * size_t(c->n_s) * sizeof(double),
+                                cudaMemcpyDeviceToHost, c->obs_stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_obs_flag, c->d_flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                c->obs_stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev_obs_done, c->obs_stream));
+    c->obs_pending = true;
+    c->obs_step = c->step;
+    return ENS_OK;
+}
+
+int ens_observe_wait(ens_ctx* c, int64_t* step) {
+    if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
+    if (!c->obs_pending) return fail(c, ENS_E_STATE, "no snapshot in flight (call ens_observe first)");
+    CUDA_TRY(c, cudaEventSynchronize(c->ev_obs_done));
+    c->obs_pending = false;
+    if (step) *step = c->obs_step;
+    const unsigned long long flag = *c->h_obs_flag;
+    if (flag != ~0ull) {
+        c->latched = true;
+        return fail(c, ENS_E_DIVERGED, "non-finite displacement at step " + std::to_string(flag >> 24) +
+                                           " in realisation " + std::to_string(flag & 0xffffff));
+    }
     return ENS_OK;
 }
 

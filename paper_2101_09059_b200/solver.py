@@ -175,6 +175,24 @@ class Ensemble:
         check(lib().ens_get_state(self._ctx, _ptr(u_n), _ptr(u_nm1), C.byref(t), C.byref(st)), self._ctx)
         return u_n, u_nm1, t.value, st.value
 
+    def observe(self, out=None):
+        """Enqueue a snapshot of u_n into `out` ([n_s][R][3] float64, a pinned CPU torch
+        tensor or a numpy array) and return it at once; the copy overlaps later steps.
+        observe_wait() completes it (ens_observe / ens_observe_wait)."""
+        if out is None:
+            n = C.c_int64()
+            check(lib().ens_get_owned(self._ctx, None, C.byref(n)), self._ctx)
+            out = np.empty((self.n_s, n.value, 3))
+        self._obs_out = out                      # keep the buffer alive while in flight
+        check(lib().ens_observe(self._ctx, _ptr(out)), self._ctx)
+        return out
+
+    def observe_wait(self) -> int:
+        """Block until the last observe() copy is done; returns its step."""
+        st = C.c_int64()
+        check(lib().ens_observe_wait(self._ctx, C.byref(st)), self._ctx)
+        return st.value
+
     def set_state(self, u_n=None, u_nm1=None, step=0):
         u_n = None if u_n is None else _c(u_n, np.float64)
         u_nm1 = None if u_nm1 is None else _c(u_nm1, np.float64)

@@ -502,3 +502,40 @@ def test_reassembly_rejected_for_matrix_free():
     with pytest.raises(EnsError):
         solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, kernel="matrix_free",
                         reassemble_every=10)
+
+
+def test_async_traction_update_and_observe():
+    """Same-shape ens_set_traction is enqueued after the running steps (no sync, no graph
+    rebuild) and ens_observe snapshots u_n while later steps run: the results equal the
+    oracle run with the traction switched at the same step, and the snapshot equals the
+    state at its step."""
+    import torch
+    m = meshmod.shuffle_nodes(meshmod.cylinder(16, 25), 8)
+    E, h = _mats(m, 4, 93)
+    tr1 = loads.pulsatile(m.xyz, m.tris, period=0.01, systole=0.004, ramp_T=0.003)
+    tr2 = loads.pulsatile(m.xyz, m.tris, p_base=1.5 * loads.P_SUPERPOSED, period=0.012, systole=0.005,
+                          ramp_T=0.003)
+    ens, om = _pair(m, E, h, kernel="assembled_sym", damping="mass", c_d=80.0, dt=5e-5)
+    ens.set_traction(tr1.F, tr1.tab_t, tr1.tab_g, tr1.period, tr1.ramp_T)
+    ens.step(150)                                    # graph replays + direct steps
+    snap = torch.empty((4, m.n_nodes, 3), dtype=torch.float64).pin_memory()
+    ens.observe(snap)
+    ens.set_traction(2 * tr1.F, tr1.tab_t, 0.5 * tr1.tab_g, tr1.period, tr1.ramp_T)    # same shape: async
+    ens.step(130)
+    assert ens.observe_wait() == 150
+    ens.set_traction(tr2.F, tr2.tab_t, tr2.tab_g, tr2.period, tr2.ramp_T)              # period changes
+    ens.step(70)
+    u, up, _, st = ens.get_state()
+    om.set_traction(tr1.F, tr1.tab_t, tr1.tab_g, tr1.period, tr1.ramp_T)
+    om.run(150)
+    assert np.linalg.norm(snap.numpy() - om.u_n) <= 1e-12 * np.linalg.norm(om.u_n)
+    om.set_traction(2 * tr1.F, tr1.tab_t, 0.5 * tr1.tab_g, tr1.period, tr1.ramp_T)
+    om.run(130)
+    om.set_traction(tr2.F, tr2.tab_t, tr2.tab_g, tr2.period, tr2.ramp_T)
+    om.run(70)
+    assert st == 350
+    assert np.linalg.norm(u - om.u_n) <= 1e-11 * np.linalg.norm(om.u_n)
+    assert np.linalg.norm(up - om.u_nm1) <= 1e-11 * np.linalg.norm(om.u_nm1)
+    with pytest.raises(EnsError):
+        ens.observe_wait()                           # nothing in flight
+    ens.close()
