@@ -267,9 +267,11 @@ def _time_kernel(kernel, args, cfg, m, tr, world, rank, local, stream, barrier, 
     el = _max_over_ranks(el)
     ens.close()
     ach = info["bytes_per_step"] / (el / args.steps) / 1e9
+    tf = info["flops_per_step"] / (el / args.steps) / 1e12
     return {"value": world * cfg.n_s * 3 * m.n_nodes * args.steps / el, "unit": "DOF-updates/s",
             "ms_per_step": 1e3 * el / args.steps, "achieved_GBs": ach, "frac": ach / peak,
-            "algorithmic_bytes_per_launch": info["bytes_per_step"]}
+            "algorithmic_bytes_per_launch": info["bytes_per_step"], "achieved_fp64_TFLOPs": tf,
+            "algorithmic_flops_per_launch": info["flops_per_step"]}
 
 
 def main(argv=None):
@@ -405,6 +407,16 @@ def main(argv=None):
                 alts[k] = {"error": repr(e)[:200]}
 
     read_gbs = _read_stream_gbs() if rank == 0 else None
+    try:                         # FP64 FMA probe: the ALU roofline
+        from paper_2101_09059_b200 import solver as _solver
+        fp64_peak = _solver.measure_fp64_tflops(local) if rank == 0 else None
+    except Exception:
+        fp64_peak = None
+    if fp64_peak:
+        for a in alts.values():
+            if "achieved_fp64_TFLOPs" in a:
+                a["fp64_frac"] = a["achieved_fp64_TFLOPs"] / fp64_peak
+    tf_head = info["flops_per_step"] / (el_max / args.steps) / 1e12
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -425,7 +437,10 @@ def main(argv=None):
                          "kernel": {"assembled": "k_step_assembled", "assembled_sym": "k_step_assembled_sym",
                                     "matrix_free": "k_step_matrix_free"}[args.kernel],
                          "algorithmic_bytes_per_launch": info["bytes_per_step"],
-                         "read_stream_GBs": read_gbs, "frac_of_read_stream": achieved / read_gbs if read_gbs else None},
+                         "read_stream_GBs": read_gbs, "frac_of_read_stream": achieved / read_gbs if read_gbs else None,
+                         "fp64": {"achieved_TFLOPs": tf_head, "peak_TFLOPs": fp64_peak,
+                                  "peak_source": "measured (ens_measure_fp64: DFMA probe, this run)",
+                                  "frac": tf_head / fp64_peak if fp64_peak else None}},
             "cpu_baseline": cpu,
             "alternatives": alts,
             "node_partition": node,

@@ -260,6 +260,12 @@ int ens_matern_fields(const ens_mesh* mesh, double rho_corr, int32_t n, const do
 int ens_p2p_export(const ens_ctx* ctx, void* blob);
 int ens_p2p_connect(ens_ctx* ctx, const void* blobs);
 
+/* Measured FP64 FMA throughput of `device` (< 0: current), TFLOP/s: the ALU roofline the
+ * matrix-free step is compared with (not in MEASURED_PEAKS.json).  A
+ * DFMA loop with 8 independent chains per thread on 8 CTAs x 256 threads per SM, best of
+ * 5 timed launches.  Synchronous; ENS_E_CUDA without a device. */
+int ens_measure_fp64(int32_t device, double* tflops);
+
 /* Sizes, dt and algorithmic traffic of the context. */
 int ens_query(const ens_ctx* ctx, ens_info* info);
 

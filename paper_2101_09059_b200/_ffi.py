@@ -57,7 +57,7 @@ EXPORTS = [
     "ens_host_pattern", "ens_host_partition", "ens_host_ghosts", "ens_host_element_stiffness",
     "ens_host_materials", "ens_create_csr", "ens_get_owned", "ens_host_halo_plan", "ens_stress",
     "ens_displacement_stats", "ens_matern_fields", "ens_p2p_export", "ens_p2p_connect", "ens_observe",
-    "ens_observe_wait",
+    "ens_observe_wait", "ens_measure_fp64",
 ]
 P2P_BLOB_BYTES = 256
 
@@ -110,6 +110,7 @@ def lib():
         "ens_p2p_connect": (C.c_int, [vp, vp]),
         "ens_observe": (C.c_int, [vp, vp]),
         "ens_observe_wait": (C.c_int, [vp, P(i64)]),
+        "ens_measure_fp64": (C.c_int, [i32, P(f64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -1521,6 +1521,17 @@ int ens_p2p_connect(ens_ctx* c, const void* blobs) {
     return ENS_OK;
 }
 
+int ens_measure_fp64(int32_t device, double* tflops) {
+    if (!tflops) return fail(nullptr, ENS_E_ARG, "tflops is NULL");
+    if (device >= 0) {
+        cudaError_t e = cudaSetDevice(device);
+        if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+    }
+    cudaError_t e = ens::measure_fp64_fma(tflops);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "fp64 FMA probe");
+    return ENS_OK;
+}
+
 int ens_query(const ens_ctx* c, ens_info* info) {
     if (!c || !info) return fail(nullptr, ENS_E_ARG, "NULL argument");
     std::memset(info, 0, sizeof(*info));

@@ -88,6 +88,8 @@ int pick_vec(int32_t n_s);      // assembled kernel
 int pick_vec_mf(int32_t n_s);   // matrix-free kernel
 // coef_buf[(step & 1)] = the load coefficients of step *step_base (after host changes)
 cudaError_t launch_seed_coeffs(const StepArgs& a, cudaStream_t st);
+// FP64 FMA throughput of this device (TFLOP/s, best of 5 timed launches)
+cudaError_t measure_fp64_fma(double* tflops);
 // *step_base += n (after n steps were enqueued)
 cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st);
 

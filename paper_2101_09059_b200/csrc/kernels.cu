@@ -11,6 +11,7 @@
 // accumulates its realisations sequentially in CSR block order then d = 0,1,2 with explicit
 // fma(): the per-realisation arithmetic is identical whatever N_s, VEC or the launch
 // geometry, which makes ensemble runs bit-identical to single-realisation runs.
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
@@ -651,6 +652,23 @@ k_step_matrix_free(const StepArgs a) {
 
 __global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
 
+// FP64 FMA throughput probe (the ALU roofline of the matrix-free step):
+// 8 independent dependency chains per thread, so the DFMA pipe, not latency, is the limit.
+__global__ void __launch_bounds__(256) k_fp64_fma(int iters, double seed, double* out) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = seed + 1e-3 * (threadIdx.x + k);
+    const double a = 0.999999999, b = 1e-9;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 12345.678) out[threadIdx.x] = s;      // never true: keeps the chains alive
+}
+
 __global__ void k_seed_coeffs(const StepArgs a) {
     const int64_t step = *a.step_base;
     load_coeffs(a, double(step) * a.dt, a.coef_buf + (step & 1) * kMaxFields);
@@ -839,6 +857,36 @@ cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
     const bool ap = a.y_out != nullptr;
     if (pick_vec_mf(a.n_s) == 2) return ap ? launch_a2<2, true, 2, 2>(a, st) : launch_a2<2, false, 2, 2>(a, st);
     return ap ? launch_a2<1, true, 2, 3>(a, st) : launch_a2<1, false, 2, 3>(a, st);
+}
+
+cudaError_t measure_fp64_fma(double* tflops) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double* d_out = nullptr;
+    cudaError_t e = cudaMalloc(&d_out, 256 * sizeof(double));
+    if (e != cudaSuccess) return e;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 4096, blocks = sms * 8;
+    float best = 1e30f;
+    for (int rep = 0; rep < 6; ++rep) {          // first launch warms up
+        cudaEventRecord(e0);
+        k_fp64_fma<<<blocks, 256>>>(iters, 1.0, d_out);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0) best = std::min(best, ms);
+    }
+    e = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d_out);
+    if (e != cudaSuccess) return e;
+    *tflops = 2.0 * 8.0 * iters * double(blocks) * 256.0 / (double(best) * 1e-3) / 1e12;
+    return cudaSuccess;
 }
 
 cudaError_t launch_seed_coeffs(const StepArgs& a, cudaStream_t st) {

@@ -360,6 +360,13 @@ def nccl_comm_of(group=None, device=None) -> int:
     return int(pg._get_backend(dev)._comm_ptr())
 
 
+def measure_fp64_tflops(device=None) -> float:
+    """Measured FP64 FMA throughput of the device (ens_measure_fp64), TFLOP/s."""
+    v = C.c_double()
+    check(lib().ens_measure_fp64(-1 if device is None else int(device), C.byref(v)))
+    return v.value
+
+
 def matern_fields(xyz, tris, rho_corr, z, tol=1e-13, max_iter=5000, device=None):
     """GPU GMRF draws x[k] = A^-1 C~^{1/2} z[k] / sigma (ens_matern_fields); z [n][V]."""
     xyz, tris, z = _c(xyz, np.float64), _c(tris, np.int32), _c(z, np.float64)

@@ -539,3 +539,10 @@ def test_async_traction_update_and_observe():
     with pytest.raises(EnsError):
         ens.observe_wait()                           # nothing in flight
     ens.close()
+
+
+def test_fp64_fma_probe_is_plausible():
+    """ens_measure_fp64 (the ALU roofline of a2): a B200 has ~37 TFLOP/s of FP64 FMA
+    (148 SMs x 64 DFMA/clk x 2 x ~1.9 GHz); the probe must land in a plausible band."""
+    tf = solver.measure_fp64_tflops(0)
+    assert 15.0 < tf < 80.0, tf

@@ -111,6 +111,15 @@ def test_create_without_gpu_fails_loudly():
     assert ei.value.code in (_ffi.ENS_E_CUDA, _ffi.ENS_E_OOM)
 
 
+def test_fp64_probe_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(_ffi.EnsError) as ei:
+        solver.measure_fp64_tflops()
+    assert ei.value.code == _ffi.ENS_E_CUDA
+
+
 @pytest.mark.parametrize("bad", ["E", "h", "nu", "rho", "mesh"])
 def test_create_argument_errors(bad):
     m = meshmod.cylinder(6, 3)
