@@ -12,6 +12,7 @@
 // fma(): the per-realisation arithmetic is identical whatever N_s, VEC or the launch
 // geometry, which makes ensemble runs bit-identical to single-realisation runs.
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
@@ -785,12 +786,17 @@ static cudaError_t launch_a2_ns(const StepArgs& a, cudaStream_t st) {
     const int P = a.n_s / VEC;
     const size_t smem = size_t(a.mf_smem_inc) * 240 + size_t(a.n_fields) * a.mf_rows * 32 +
                         size_t(a.mf_rows * a.mf_groups) * 6 * VEC * sizeof(double);
-    static bool attr_set = false;      // per template instance
-    if (!attr_set) {
+    // the shared-memory opt-in is a per-device function attribute: once per device and
+    // template instance (contexts of one process may live on different devices)
+    static std::atomic<uint64_t> attr_set{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (!(attr_set.load(std::memory_order_acquire) & bit)) {
         cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set.fetch_or(bit, std::memory_order_release);
     }
     dim3 grid(unsigned((a.V + a.mf_rows - 1) / a.mf_rows), unsigned((P + a.mf_groups - 1) / a.mf_groups));
     k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(a);
