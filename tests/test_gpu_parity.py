@@ -546,3 +546,29 @@ def test_fp64_fma_probe_is_plausible():
     (148 SMs x 64 DFMA/clk x 2 x ~1.9 GHz); the probe must land in a plausible band."""
     tf = solver.measure_fp64_tflops(0)
     assert 15.0 < tf < 80.0, tf
+
+
+@pytest.mark.parametrize("name,kernel,steps,samples", [
+    ("c4", "assembled_sym", 100, (0, 77, 127)),        # bench --config c4 (N_s = 128, the default kernel)
+    ("c5", "matrix_free", 30, (0, 311, 511)),          # bench --config c5 (N_s = 512, one GPU)
+])
+def test_full_size_launch_configuration_sampled(name, kernel, steps, samples):
+    """The aorta configs at their full size and in the launch configuration bench.py times
+    (N_s = 128 / 512 on one device): sampled realisations recomputed one by one by the
+    oracle (ensemble equivalence makes the single-realisation run the reference), <= 1e-9."""
+    cfg = configs.make(name)
+    m, tr = cfg.mesh, cfg.traction
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=cfg.rho, nu=cfg.nu, k_shear=cfg.k_shear,
+                          damping=cfg.damping, c_d=cfg.c_d, kernel=kernel)
+    dt = ens.info()["dt"]
+    ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    ens.step(steps)
+    u = ens.get_state(want_prev=False)[0]
+    ens.close()
+    for s in samples:
+        om = oracle.OracleModel(m.xyz, m.tris, m.fixed, cfg.E[s:s + 1], cfg.h[s:s + 1], rho=cfg.rho, nu=cfg.nu,
+                                k_shear=cfg.k_shear, damping=cfg.damping, c_d=cfg.c_d, dt=dt)
+        om.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+        om.run(steps)
+        ref = om.u_n[0]
+        assert np.linalg.norm(u[s] - ref) <= 1e-9 * np.linalg.norm(ref), s
