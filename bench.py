@@ -223,6 +223,34 @@ def _node_partition_run(args, cfg, base, m, tr, rank, world, local, stream, barr
     return node
 
 
+def _emulated_partition_run(args, cfg, m, tr, local, stream, halo, single_value):
+    """ENS_DIST_NODE with all P parts in this one context on this one GPU: the per-step cost
+    of the partitioned schedule (boundary / interior launches, halo by device copies or by
+    the P2P forwarding stores + step flags) against the unpartitioned step.  Not a
+    multi-GPU number: the parts run one after another on the same device."""
+    import torch
+    from paper_2101_09059_b200 import solver
+    P = args.emulate_partition
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=cfg.rho, nu=cfg.nu, k_shear=cfg.k_shear,
+                          damping=cfg.damping, c_d=cfg.c_d, kernel=args.kernel, dist="node", world=P, halo=halo,
+                          device=local)
+    ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    ens.step(max(3, args.warmup))
+    ens.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ens.step(args.steps)
+    e1.record(stream)
+    e1.synchronize()
+    el = e0.elapsed_time(e1) / 1e3
+    inf = ens.info()
+    ens.close()
+    v = cfg.n_s * 3 * m.n_nodes * args.steps / el
+    return {"value": v, "unit": "DOF-updates/s", "ms_per_step": 1e3 * el / args.steps,
+            "of_unpartitioned": v / single_value, "launches_per_step": inf["launches_per_step"],
+            "graph_steps": inf["graph_steps"], "halo_bytes_per_step": inf["halo_bytes_per_step"]}
+
+
 def _read_stream_gbs(gib: float = 4.0, reps: int = 10) -> float:
     """Practical ceiling of a read-dominated kernel on this box: torch.sum over a 4 GiB fp64
     tensor, best of `reps`, CUDA events."""
@@ -287,6 +315,8 @@ def main(argv=None):
     ap.add_argument("--no-alternatives", action="store_true", help="do not time the other kernels")
     ap.add_argument("--node-partition", action="store_true",
                     help="at N > 1 also time ENS_DIST_NODE (RCM rows split; NCCL and P2P halos; strong scaling)")
+    ap.add_argument("--emulate-partition", type=int, default=0,
+                    help="at N = 1 also time ENS_DIST_NODE with this many parts in one context (schedule overhead)")
     ap.add_argument("--e2e-windows", type=int, default=10)
     ap.add_argument("--obs-every", type=int, default=100)
     args = ap.parse_args(argv)
@@ -392,6 +422,13 @@ def main(argv=None):
                 node[halo] = _node_partition_run(args, cfg, base, m, tr, rank, world, local, stream, barrier,
                                                  n_s, halo)
             except Exception as e:      # reported, never fatal for the primary (sharded) line
+                node[halo] = {"error": repr(e)[:300]}
+    elif world == 1 and args.emulate_partition > 1:
+        node = {"emulated_parts": args.emulate_partition}
+        for halo in ("nccl", "p2p"):
+            try:
+                node[halo] = _emulated_partition_run(args, cfg, m, tr, local, stream, halo, value)
+            except Exception as e:
                 node[halo] = {"error": repr(e)[:300]}
 
     # the other kernels of the same step, same inputs, same launch protocol (reported

@@ -374,31 +374,66 @@ int reassemble_if_due(ens_ctx* c, Part& p, int64_t step, cudaStream_t st) {
     return ENS_OK;
 }
 
-// P2P halo step (ENS_HALO_P2P; DESIGN.md §7): per part, wait for the neighbours' u_n ghost
-// rows (their flags >= step), boundary rows with u_{n+1} forwarded into the neighbours'
-// ghost rows of buffer (step + 1) & 1, publish step + 1; then every part's interior rows.
-// Neighbours only ever write ghost rows of the buffer this part is not reading, and only
-// after it published the step before, so two buffers suffice (no acknowledgement needed).
-int enqueue_step_p2p(ens_ctx* c, int64_t k, cudaStream_t st) {
-    const int64_t step = c->step + k;
-    for (Part& p : c->parts) {
-        CUDA_TRY(c, ens::launch_halo_wait(p.n_in, p.d_in_q, p.d_hflags, c->d_step, k, c->d_herr, st));
-        RC_TRY(reassemble_if_due(c, p, step, st));
-        ens::StepArgs a = part_args(c, p);
-        a.step_off = k;
-        a.fwd_ptr = p.d_fwd_ptr;
-        a.fwd_dst = p.d_fwd_dst;
-        a.peer_buf = p.d_peer_buf;
-        CUDA_TRY(c, launch_rows(c, a, 0, p.plan.b_lo, st));
-        CUDA_TRY(c, launch_rows(c, a, p.n_own - p.plan.b_hi, p.plan.b_hi, st));
-        CUDA_TRY(c, ens::launch_halo_signal(p.n_out, p.d_out_flag, c->d_step, k, st));
+// Steps with a halo run on two streams: the halo chain (boundary rows of every part, which
+// read ghosts and which the neighbours need, then the exchange) on comm_stream, the
+// interior rows (no ghost column) on the step stream; both join before the next step,
+// since each half reads the other's u_{n+1} next step.  A step that re-assembles first
+// runs serially on the step stream.
+bool reassembly_due(const ens_ctx* c, int64_t step) {
+    return c->reassemble_every > 0 && step > 0 && step % c->reassemble_every == 0;
+}
+
+int fork_halo(ens_ctx* c, cudaStream_t st, bool fork, cudaStream_t* hs) {
+    *hs = fork ? c->comm_stream : st;
+    if (fork) {
+        CUDA_TRY(c, cudaEventRecord(c->ev_packed, st));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
     }
+    return ENS_OK;
+}
+
+int join_halo(ens_ctx* c, cudaStream_t st, bool fork) {
+    if (fork) {
+        CUDA_TRY(c, cudaEventRecord(c->ev_halo, c->comm_stream));
+        CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
+    }
+    return ENS_OK;
+}
+
+int launch_interior(ens_ctx* c, int64_t k, cudaStream_t st) {
     for (Part& p : c->parts) {
         ens::StepArgs a = part_args(c, p);
         a.step_off = k;
         CUDA_TRY(c, launch_rows(c, a, p.plan.b_lo, p.n_own - p.plan.b_lo - p.plan.b_hi, st));
     }
     return ENS_OK;
+}
+
+// P2P halo step (ENS_HALO_P2P; DESIGN.md §9): per part, wait for the neighbours' u_n ghost
+// rows (their flags >= step), boundary rows with u_{n+1} forwarded into the neighbours'
+// ghost rows of buffer (step + 1) & 1, publish step + 1 — all on the halo stream, while
+// the interior rows run on the step stream.  Neighbours only ever write ghost rows of the
+// buffer this part is not reading, and only after it published the step before, so two
+// buffers suffice (no acknowledgement needed).
+int enqueue_step_p2p(ens_ctx* c, int64_t k, cudaStream_t st) {
+    const int64_t step = c->step + k;
+    const bool fork = !reassembly_due(c, step);
+    cudaStream_t hs;
+    RC_TRY(fork_halo(c, st, fork, &hs));
+    for (Part& p : c->parts) {
+        CUDA_TRY(c, ens::launch_halo_wait(p.n_in, p.d_in_q, p.d_hflags, c->d_step, k, c->d_herr, hs));
+        RC_TRY(reassemble_if_due(c, p, step, hs));
+        ens::StepArgs a = part_args(c, p);
+        a.step_off = k;
+        a.fwd_ptr = p.d_fwd_ptr;
+        a.fwd_dst = p.d_fwd_dst;
+        a.peer_buf = p.d_peer_buf;
+        CUDA_TRY(c, launch_rows(c, a, 0, p.plan.b_lo, hs));
+        CUDA_TRY(c, launch_rows(c, a, p.n_own - p.plan.b_hi, p.plan.b_hi, hs));
+        CUDA_TRY(c, ens::launch_halo_signal(p.n_out, p.d_out_flag, c->d_step, k, hs));
+    }
+    RC_TRY(launch_interior(c, k, st));
+    return join_halo(c, st, fork);
 }
 
 int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
@@ -411,37 +446,36 @@ int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
         CUDA_TRY(c, launch_rows(c, a, 0, c->parts[0].n_own, st));
         return ENS_OK;
     }
+    cudaStream_t hs;
+    RC_TRY(fork_halo(c, st, true, &hs));
     // (1) boundary rows of every part (they read ghosts, and the neighbours need them)
     for (Part& p : c->parts) {
         ens::StepArgs a = part_args(c, p);
         a.step_off = k;
-        CUDA_TRY(c, launch_rows(c, a, 0, p.plan.b_lo, st));
-        CUDA_TRY(c, launch_rows(c, a, p.n_own - p.plan.b_hi, p.plan.b_hi, st));
+        CUDA_TRY(c, launch_rows(c, a, 0, p.plan.b_lo, hs));
+        CUDA_TRY(c, launch_rows(c, a, p.n_own - p.plan.b_hi, p.plan.b_hi, hs));
         CUDA_TRY(c, ens::launch_pack(int64_t(p.plan.send_rows.size()), c->n_s, p.d_send_rows, c->d_step, k, p.d_u0,
-                                     p.d_u1, p.d_sendbuf, st));
+                                     p.d_u1, p.d_sendbuf, hs));
     }
     const size_t w = size_t(3) * size_t(c->n_s);
     auto unew = [&](Part& p) { return ((step + 1) & 1) ? p.d_u1 : p.d_u0; };
     // (2) halo: u_{n+1} of the send rows -> the neighbours' ghost rows
     if (c->nccl_comm) {
         Part& p = c->parts[0];
-        CUDA_TRY(c, cudaEventRecord(c->ev_packed, st));
-        CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_packed, 0));
         const ens::Nccl& N = *c->nccl;
         int r = N.group_start();
         for (const auto& pe : p.plan.peers) {
             if (r == 0 && pe.send_n)
                 r = N.send(p.d_sendbuf + size_t(pe.send_off) * w, size_t(pe.send_n) * w, ens::Nccl::kDouble, pe.q,
-                           c->nccl_comm, c->comm_stream);
+                           c->nccl_comm, hs);
             if (r == 0 && pe.recv_n)
                 r = N.recv(unew(p) + size_t(pe.recv_row) * w, size_t(pe.recv_n) * w, ens::Nccl::kDouble, pe.q,
-                           c->nccl_comm, c->comm_stream);
+                           c->nccl_comm, hs);
         }
         int r2 = N.group_end();
         if (r == 0) r = r2;
         if (r != 0)
             return fail(c, ENS_E_NCCL, std::string("halo exchange: ") + (N.error_string ? N.error_string(r) : "error"));
-        CUDA_TRY(c, cudaEventRecord(c->ev_halo, c->comm_stream));
     } else {
         for (Part& p : c->parts)
             for (const auto& pe : p.plan.peers) {
@@ -450,18 +484,12 @@ int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
                 const auto it = std::find_if(q.plan.peers.begin(), q.plan.peers.end(),
                                              [&](const ens::PartPlan::Peer& x) { return x.q == p.plan.p; });
                 CUDA_TRY(c, cudaMemcpyAsync(unew(p) + size_t(pe.recv_row) * w, q.d_sendbuf + size_t(it->send_off) * w,
-                                            size_t(pe.recv_n) * w * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                                            size_t(pe.recv_n) * w * sizeof(double), cudaMemcpyDeviceToDevice, hs));
             }
     }
-    // (3) interior rows, overlapping the exchange on the comm stream
-    for (Part& p : c->parts) {
-        ens::StepArgs a = part_args(c, p);
-        a.step_off = k;
-        CUDA_TRY(c, launch_rows(c, a, p.plan.b_lo, p.n_own - p.plan.b_lo - p.plan.b_hi, st));
-    }
-    // (4) the next step's boundary rows read the ghosts: join the exchange
-    if (c->nccl_comm) CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
-    return ENS_OK;
+    // (3) interior rows on the step stream, overlapping (1)-(2); (4) join
+    RC_TRY(launch_interior(c, k, st));
+    return join_halo(c, st, true);
 }
 
 // Capture graph_steps steps + the counter advance on a private stream (the caller's stream
@@ -868,6 +896,11 @@ int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, cons
         for (size_t k = 0; k < plans.size(); ++k) c->parts[k].plan = plans[k];
     }
     for (Part& p : c->parts) RC_TRY(build_part(c, p, G));
+    if (c->has_halo() && !c->comm_stream) {      // the halo chain's stream (one-context emulation)
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+    }
     if (c->p2p()) {
         for (Part& p : c->parts) RC_TRY(build_p2p(c, p, plans));
         if (!c->multi) RC_TRY(link_p2p_local(c));
