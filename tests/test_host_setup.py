@@ -175,3 +175,31 @@ def test_halo_plan_vs_oracle(P):
             if np.any((cols < lo) | (cols >= hi)):
                 li = i - lo
                 assert li < pl["b_lo"] or li >= n_own - pl["b_hi"]
+
+
+def test_null_context_is_an_argument_error():
+    """Every context call rejects a NULL context with ENS_E_ARG and a message (no crash);
+    ens_destroy(NULL) is a no-op."""
+    L = _ffi.lib()
+    i64 = C.c_int64()
+    calls = {
+        "ens_step": lambda: L.ens_step(None, 1),
+        "ens_sync": lambda: L.ens_sync(None),
+        "ens_get_state": lambda: L.ens_get_state(None, None, None, None, None),
+        "ens_get_owned": lambda: L.ens_get_owned(None, None, C.byref(i64)),
+        "ens_set_state": lambda: L.ens_set_state(None, None, None, 0.0, 0),
+        "ens_set_traction": lambda: L.ens_set_traction(None, 0, None, 0, None, None, 0.0, 0.0),
+        "ens_apply_stiffness": lambda: L.ens_apply_stiffness(None, None, None),
+        "ens_stress": lambda: L.ens_stress(None, 0, None, 0, None, None, None, None),
+        "ens_displacement_stats": lambda: L.ens_displacement_stats(None, None, None, None),
+        "ens_observe": lambda: L.ens_observe(None, None),
+        "ens_observe_wait": lambda: L.ens_observe_wait(None, C.byref(i64)),
+        "ens_p2p_export": lambda: L.ens_p2p_export(None, None),
+        "ens_p2p_connect": lambda: L.ens_p2p_connect(None, None),
+        "ens_query": lambda: L.ens_query(None, None),
+        "ens_measure_fp64": lambda: L.ens_measure_fp64(-1, None),
+    }
+    for name, call in calls.items():
+        assert call() == _ffi.ENS_E_ARG, name
+        assert L.ens_last_error(None), name
+    L.ens_destroy(None)
