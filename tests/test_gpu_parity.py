@@ -631,3 +631,23 @@ def test_nonmanifold_vertex_and_components(kernel):
     u = ens.get_state()[0]
     assert np.linalg.norm(u - om.u_n) <= 1e-9 * np.linalg.norm(om.u_n)
     ens.close()
+
+
+@pytest.mark.parametrize("halo", ["nccl", "p2p"])
+@pytest.mark.parametrize("kernel", ["assembled_sym", "matrix_free"])
+def test_many_small_parts_bitexact(kernel, halo):
+    """P = 8 parts of a 157-node mesh: parts whose every row is a boundary row, parts with
+    several (not only adjacent) neighbours, a part holding a whole component — still
+    bit-identical to the single-part run."""
+    m = meshmod.shuffle_nodes(_nonmanifold_mesh(), 10)
+    E, h = _mats(m, 4, 42)
+    tr = loads.pulsatile(m.xyz, m.tris, period=0.01, systole=0.004, ramp_T=0.003)
+    kw = dict(rho=RHO, nu=NU, k_shear=KS, kernel=kernel, dt=2e-5, damping="mass", c_d=100.0)
+    out = []
+    for extra in ({}, dict(dist="node", world=8, halo=halo)):
+        ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, **kw, **extra)
+        ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+        ens.step(150)
+        out.append(ens.get_state())
+        ens.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
