@@ -571,21 +571,27 @@ __device__ __forceinline__ void mf_tile_rows(const StepArgs& a, const StepCtx& s
                              const double* K) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                double t[VEC];
+                // three independent 3-term chains (own, prev, next), then their sum: short
+                // dependency chains for the FP64 pipe
+                double to[VEC], tp[VEC], tn[VEC];
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) t[v] = 0.0;
+                for (int v = 0; v < VEC; ++v) {
+                    to[v] = K[9 * c] * uo[0].v[v];
+                    tp[v] = K[9 * c + 3] * prev[0].v[v];
+                    tn[v] = K[9 * c + 6] * next[0].v[v];
+                }
 #pragma unroll
-                for (int d = 0; d < 3; ++d) {
+                for (int d = 1; d < 3; ++d) {
                     const double k_own = K[9 * c + d], k_prev = K[9 * c + 3 + d], k_next = K[9 * c + 6 + d];
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) {
-                        t[v] = fma(k_own, uo[d].v[v], t[v]);
-                        t[v] = fma(k_prev, prev[d].v[v], t[v]);
-                        t[v] = fma(k_next, next[d].v[v], t[v]);
+                        to[v] = fma(k_own, uo[d].v[v], to[v]);
+                        tp[v] = fma(k_prev, prev[d].v[v], tp[v]);
+                        tn[v] = fma(k_next, next[d].v[v], tn[v]);
                     }
                 }
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) y[c][v] = fma(alj.v[v], t[v], y[c][v]);
+                for (int v = 0; v < VEC; ++v) y[c][v] = fma(alj.v[v], (to[v] + tp[v]) + tn[v], y[c][v]);
             }
         };
         // the previous neighbour of incidence j is next(j - 1) (carried in registers, no
