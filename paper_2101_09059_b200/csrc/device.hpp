@@ -35,6 +35,7 @@ struct StepArgs {
     int32_t mf_rows = 1;                // rows per CTA
     int32_t mf_groups = 1;              // realisation groups (threads) per row per CTA
     int32_t mf_smem_inc = 0;            // max incidences staged by one CTA
+    int32_t mf_prefetch = 0;            // L2 prefetch distance in tiles (set by the launcher)
     // update coefficients
     const double* c1 = nullptr;
     const double* c2a = nullptr;        // null => scalars c2, c3

@@ -489,6 +489,9 @@ __device__ __forceinline__ size_t mf_tile_bytes(const StepArgs& a) {
     return size_t(a.mf_smem_inc) * 240 + size_t(a.n_fields) * a.mf_rows * 32;
 }
 
+constexpr int kMfPrefetchWave = 1;
+__device__ __forceinline__ int64_t mf_wave_ctas(const StepArgs& a) { return a.mf_prefetch; }
+
 template <bool APPLY>
 __device__ __forceinline__ void mf_issue_tile(const StepArgs& a, int64_t r0, int64_t r1, unsigned char* tile,
                                               uint32_t bar) {
@@ -652,6 +655,19 @@ k_step_matrix_free(const StepArgs a) {
             for (int k = 0; k < a.n_fields; ++k) s_coef[k] = cb[k];
         }
         mf_issue_tile<APPLY>(a, r0, r1, smem, bar);
+        // warm L2 for the tile that starts about when this one ends (one wave of CTAs
+        // later): its K^ rows and fan records, so that its own TMA does not wait on DRAM
+        const int64_t f0 = r0 + int64_t(gridDim.y > 0 ? kMfPrefetchWave : 0) * a.mf_rows * mf_wave_ctas(a);
+        if (a.mf_prefetch && f0 < a.row0 + a.V) {
+            const int64_t f1 = min(f0 + a.mf_rows, a.row0 + a.V);
+            const int32_t q0 = __ldg(a.inc_ptr + f0), q1 = __ldg(a.inc_ptr + f1);
+            if (q1 > q0) {
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                             :: "l"(a.Krow + size_t(q0) * 28), "r"(uint32_t(q1 - q0) * 224u) : "memory");
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                             :: "l"(a.fan + q0), "r"(uint32_t(q1 - q0) * 16u) : "memory");
+            }
+        }
     }
     double* slot = reinterpret_cast<double*>(smem + mf_tile_bytes(a)) + size_t(threadIdx.x) * 6 * VEC;
     mf_tile_rows<VEC, APPLY, BATCH, NS>(a, sc, s_coef, r0, r1, smem, slot, bar, 0);
@@ -805,7 +821,22 @@ static cudaError_t launch_a2_ns(const StepArgs& a, cudaStream_t st) {
         attr_set.fetch_or(bit, std::memory_order_release);
     }
     dim3 grid(unsigned((a.V + a.mf_rows - 1) / a.mf_rows), unsigned((P + a.mf_groups - 1) / a.mf_groups));
-    k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(a);
+    StepArgs b = a;
+    {   // tiles resident at once (one wave): the L2 prefetch distance, in tiles
+        static int per_sm[64] = {0};
+        static int sms[64] = {0};
+        const int d = dev & 63;
+        if (per_sm[d] == 0) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[d], k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS>,
+                                                          a.mf_rows * a.mf_groups, smem);
+            cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, dev);
+            per_sm[d] = std::max(per_sm[d], 1);
+        }
+        const char* e = std::getenv("ENS_MF_PREFETCH");
+        const bool on = e ? std::atoi(e) != 0 : true;
+        b.mf_prefetch = on ? int32_t(int64_t(per_sm[d]) * sms[d] / std::max<unsigned>(grid.y, 1)) : 0;
+    }
+    k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(b);
     return cudaGetLastError();
 }
 
