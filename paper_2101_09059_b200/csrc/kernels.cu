@@ -493,9 +493,8 @@ constexpr int kMfPrefetchWave = 1;
 __device__ __forceinline__ int64_t mf_wave_ctas(const StepArgs& a) { return a.mf_prefetch; }
 
 template <bool APPLY>
-__device__ __forceinline__ void mf_issue_tile(const StepArgs& a, int64_t r0, int64_t r1, unsigned char* tile,
-                                              uint32_t bar) {
-    const int32_t k0 = __ldg(a.inc_ptr + r0), k1 = __ldg(a.inc_ptr + r1);
+__device__ __forceinline__ void mf_issue_tile(const StepArgs& a, int64_t r0, int64_t r1, int32_t k0, int32_t k1,
+                                              unsigned char* tile, uint32_t bar) {
     const uint32_t n_inc = uint32_t(k1 - k0);
     const uint32_t nF = APPLY ? 0u : uint32_t(a.n_fields), fbytes = uint32_t(r1 - r0) * 32u;
     double* sF = reinterpret_cast<double*>(tile + size_t(a.mf_smem_inc) * 240);
@@ -650,11 +649,18 @@ k_step_matrix_free(const StepArgs a) {
     // own loads.  s_coef is written before the expect_tx arrive (release), and read after
     // the mbarrier wait (acquire).
     if (threadIdx.x == 0) {
+        // the incidence range and the load coefficients are independent loads: both in
+        // flight at once, then s_coef, then the expect_tx arrive that publishes it
+        const int32_t k0 = __ldg(a.inc_ptr + r0), k1 = __ldg(a.inc_ptr + r1);
         if (!APPLY) {
             const double* cb = step_coef(a, sc);
-            for (int k = 0; k < a.n_fields; ++k) s_coef[k] = cb[k];
+            double cv[kMaxFields];
+#pragma unroll
+            for (int k = 0; k < kMaxFields; ++k) cv[k] = k < a.n_fields ? cb[k] : 0.0;
+#pragma unroll
+            for (int k = 0; k < kMaxFields; ++k) s_coef[k] = cv[k];
         }
-        mf_issue_tile<APPLY>(a, r0, r1, smem, bar);
+        mf_issue_tile<APPLY>(a, r0, r1, k0, k1, smem, bar);
         // warm L2 for the tile that starts about when this one ends (one wave of CTAs
         // later): its K^ rows and fan records, so that its own TMA does not wait on DRAM
         const int64_t f0 = r0 + int64_t(gridDim.y > 0 ? kMfPrefetchWave : 0) * a.mf_rows * mf_wave_ctas(a);
