@@ -717,15 +717,26 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
                 mx = std::max(mx, ip[size_t(r1)] - ip[size_t(r0)]);
             }
             P.mf_smem_inc = mx;
-            if (int64_t(mx) * 240 <= 96 * 1024 || P.mf_rows == 1) break;
+            if (int64_t(mx) * ens::mf_inc_bytes() <= 96 * 1024 || P.mf_rows == 1) break;
             P.mf_rows = std::max(1, P.mf_rows / 2);
         }
-        if (int64_t(P.mf_smem_inc) * 240 > 200 * 1024)
+        if (int64_t(P.mf_smem_inc) * ens::mf_inc_bytes() > 200 * 1024)
             return fail(c, ENS_E_UNSUPPORTED, "a node has too many incident elements for the matrix-free kernel");
         static_assert(sizeof(ens::FanRec) == sizeof(int4), "FanRec layout");
         RC_TRY(upload(c, &P.d_inc_ptr, ip.data(), ip.size()));
         RC_TRY(upload(c, &P.d_fan, reinterpret_cast<const int4*>(rec.data()), rec.size()));
-        RC_TRY(upload(c, &P.d_Krow, fans.Krow.data() + size_t(k0) * 28, size_t(k1 - k0) * 28));
+        if (ens::mf_diff()) {      // (prev, next) columns only: K^_e[a,a] u_i cancels (kernels.cu DIFF)
+            std::vector<double> k18(size_t(k1 - k0) * 18);
+            for (int64_t k = 0; k < k1 - k0; ++k)
+                for (int c = 0; c < 3; ++c)
+                    for (int b = 0; b < 2; ++b)
+                        for (int d = 0; d < 3; ++d)
+                            k18[size_t(k) * 18 + size_t(6 * c + 3 * b + d)] =
+                                fans.Krow[size_t(k0 + k) * 28 + size_t(9 * c + 3 * (b + 1) + d)];
+            RC_TRY(upload(c, &P.d_Krow, k18.data(), k18.size()));
+        } else {
+            RC_TRY(upload(c, &P.d_Krow, fans.Krow.data() + size_t(k0) * 28, size_t(k1 - k0) * 28));
+        }
         RC_TRY(upload(c, &P.d_alpha, al.data(), al.size()));
     }
     const size_t ns = size_t(n_loc) * 3 * size_t(n_s);
@@ -1608,8 +1619,13 @@ int ens_query(const ens_ctx* c, ens_info* info) {
         info->bytes_per_step = ns * (72 * stored + int64_t(frac * double(per_node * c->V)));
         info->flops_per_step = int64_t(frac * double(ns * (18 * c->nnzb + 3 * 5 * c->V)));
     } else {
-        info->bytes_per_step = int64_t(frac * double(ns * (8 * c->F + per_node * c->V) + 648 * c->F));
-        info->flops_per_step = int64_t(frac * double(ns * (3 * c->F * 60 + 3 * 5 * c->V)));
+        // K^: the 2 x 9 (prev, next) values of each of an element's 3 rows = 432 B per element
+        // (DIFF), else the full 9 x 9 = 648 B.  Flops per incidence: DIFF 18 FMA + 3 adds + the
+        // alpha FMA on 3 components + the 3-component difference of the new neighbour = 48;
+        // else 27 FMA + 2 x 3 adds + 3 alpha FMA = 66 (counted 60: the adds folded)
+        const bool dif = ens::mf_diff();
+        info->bytes_per_step = int64_t(frac * double(ns * (8 * c->F + per_node * c->V) + (dif ? 432 : 648) * c->F));
+        info->flops_per_step = int64_t(frac * double(ns * (3 * c->F * (dif ? 48 : 60) + 3 * 5 * c->V)));
     }
     return ENS_OK;
 }

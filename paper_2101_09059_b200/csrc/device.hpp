@@ -87,6 +87,8 @@ cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st);
 // realisations per thread of the step kernels for a given N_s (4, 2 or 1)
 int pick_vec(int32_t n_s);      // assembled kernel
 int pick_vec_mf(int32_t n_s);   // matrix-free kernel
+bool mf_diff();            // matrix-free: neighbours relative to u_i, (prev, next) K^ columns only (ENS_MF_DIFF, default 1)
+int mf_inc_bytes();        // matrix-free: shared-memory bytes per incidence (K^ image + fan record)
 // coef_buf[(step & 1)] = the load coefficients of step *step_base (after host changes)
 cudaError_t launch_seed_coeffs(const StepArgs& a, cudaStream_t st);
 // FP64 FMA throughput of this device (TFLOP/s, best of 5 timed launches)

@@ -485,23 +485,33 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
 // Tile = the mf_rows consecutive rows [r0, r1) of one CTA pass.  Its shared-memory image:
 // K^ rows (224 B per incidence), fan records (16 B), F_k rows ([k][R][4]); issued by one
 // thread as 1-D TMA bulk copies completing on `bar`.
+// K^ row image per incidence: DIFF (default) keeps only the (prev, next) columns, [c][2][3]
+// = 18 doubles (144 B); otherwise (own, prev, next), [c][3][3] + pad = 28 doubles (224 B).
+template <bool DIFF> struct MfLayout {
+    static constexpr int kst = DIFF ? 18 : 28;              // doubles per incidence
+    static constexpr uint32_t kbytes = uint32_t(kst) * 8;
+    static constexpr uint32_t inc = kbytes + 16;              // + fan record
+};
+
+template <bool DIFF>
 __device__ __forceinline__ size_t mf_tile_bytes(const StepArgs& a) {
-    return size_t(a.mf_smem_inc) * 240 + size_t(a.n_fields) * a.mf_rows * 32;
+    return size_t(a.mf_smem_inc) * MfLayout<DIFF>::inc + size_t(a.n_fields) * a.mf_rows * 32;
 }
 
 constexpr int kMfPrefetchWave = 1;
 __device__ __forceinline__ int64_t mf_wave_ctas(const StepArgs& a) { return a.mf_prefetch; }
 
-template <bool APPLY>
+template <bool APPLY, bool DIFF>
 __device__ __forceinline__ void mf_issue_tile(const StepArgs& a, int64_t r0, int64_t r1, int32_t k0, int32_t k1,
                                               unsigned char* tile, uint32_t bar) {
     const uint32_t n_inc = uint32_t(k1 - k0);
     const uint32_t nF = APPLY ? 0u : uint32_t(a.n_fields), fbytes = uint32_t(r1 - r0) * 32u;
-    double* sF = reinterpret_cast<double*>(tile + size_t(a.mf_smem_inc) * 240);
-    mbar_expect_tx(bar, n_inc * 240u + nF * fbytes);      // arrives even when nothing is copied
+    using L = MfLayout<DIFF>;
+    double* sF = reinterpret_cast<double*>(tile + size_t(a.mf_smem_inc) * L::inc);
+    mbar_expect_tx(bar, n_inc * L::inc + nF * fbytes);      // arrives even when nothing is copied
     if (n_inc) {
-        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(tile)), a.Krow + size_t(k0) * 28, n_inc * 224u, bar);
-        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(tile + size_t(a.mf_smem_inc) * 224)), a.fan + k0,
+        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(tile)), a.Krow + size_t(k0) * L::kst, n_inc * L::kbytes, bar);
+        tma_bulk_g2s(uint32_t(__cvta_generic_to_shared(tile + size_t(a.mf_smem_inc) * L::kbytes)), a.fan + k0,
                      n_inc * 16u, bar);
     }
     for (int k = 0; k < int(nF); ++k)
@@ -510,7 +520,7 @@ __device__ __forceinline__ void mf_issue_tile(const StepArgs& a, int64_t r0, int
 }
 
 // One thread's share of a tile: row r0 + threadIdx.x / G, realisations of group g.
-template <int VEC, bool APPLY, int BATCH, int NS>
+template <int VEC, bool APPLY, int BATCH, int NS, bool DIFF>
 __device__ __forceinline__ void mf_tile_rows(const StepArgs& a, const StepCtx& sc, const double* s_coef, int64_t r0,
                                              int64_t r1, const unsigned char* tile, double* slot, uint32_t bar,
                                              uint32_t phase) {
@@ -519,8 +529,9 @@ __device__ __forceinline__ void mf_tile_rows(const StepArgs& a, const StepCtx& s
     const int G = NS ? (NS / VEC < 256 ? NS / VEC : 256) : a.mf_groups;
     const int R = a.mf_rows;
     const double* sK = reinterpret_cast<const double*>(tile);
-    const int4* sRec = reinterpret_cast<const int4*>(tile + size_t(a.mf_smem_inc) * 224);
-    const double* sF = reinterpret_cast<const double*>(tile + size_t(a.mf_smem_inc) * 240);
+    using L = MfLayout<DIFF>;
+    const int4* sRec = reinterpret_cast<const int4*>(tile + size_t(a.mf_smem_inc) * L::kbytes);
+    const double* sF = reinterpret_cast<const double*>(tile + size_t(a.mf_smem_inc) * L::inc);
 
     const int P = a.n_s / VEC;
     const int lr = int(threadIdx.x) / G;
@@ -537,6 +548,16 @@ __device__ __forceinline__ void mf_tile_rows(const StepArgs& a, const StepCtx& s
 #pragma unroll
         for (int v = 0; v < VEC; ++v) y[c][v] = 0.0;
     Vec<VEC> uo[3], up[3];
+    // DIFF: neighbour displacements relative to u_i.  K^_e annihilates rigid translations
+    // (the nullspace holds the three translations), so
+    // K^_e[a,:] u_e = K^_e[a,b] (u_b - u_i) + K^_e[a,c] (u_c - u_i): the own 3x3 block drops
+    // out (18 instead of 27 FMA per incidence and realisation; DESIGN.md §5 F2).
+    auto rel_to_own = [&](Vec<VEC> (&w)[3]) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) w[d].v[v] -= uo[d].v[v];
+    };
     if (valid) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) uo[d] = ld_ro<VEC>(un_base + (i * 3 + d) * n_s);
@@ -554,6 +575,7 @@ __device__ __forceinline__ void mf_tile_rows(const StepArgs& a, const StepCtx& s
         const int4 r = sRec[kb];
 #pragma unroll
         for (int d = 0; d < 3; ++d) up[d] = ld_ro<VEC>(un_base + (r.y * W3 + d * n_s));
+        if constexpr (DIFF) rel_to_own(up);
     }
     for (int32_t k = kb; k < ke; k += BATCH) {
         // gather phase: every load of the batch in flight before any arithmetic
@@ -573,27 +595,47 @@ __device__ __forceinline__ void mf_tile_rows(const StepArgs& a, const StepCtx& s
                              const double* K) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                // three independent 3-term chains (own, prev, next), then their sum: short
-                // dependency chains for the FP64 pipe
-                double to[VEC], tp[VEC], tn[VEC];
-#pragma unroll
-                for (int v = 0; v < VEC; ++v) {
-                    to[v] = K[9 * c] * uo[0].v[v];
-                    tp[v] = K[9 * c + 3] * prev[0].v[v];
-                    tn[v] = K[9 * c + 6] * next[0].v[v];
-                }
-#pragma unroll
-                for (int d = 1; d < 3; ++d) {
-                    const double k_own = K[9 * c + d], k_prev = K[9 * c + 3 + d], k_next = K[9 * c + 6 + d];
+                if constexpr (DIFF) {        // prev / next already relative to u_i
+                    double tp[VEC], tn[VEC];
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) {
-                        to[v] = fma(k_own, uo[d].v[v], to[v]);
-                        tp[v] = fma(k_prev, prev[d].v[v], tp[v]);
-                        tn[v] = fma(k_next, next[d].v[v], tn[v]);
+                        tp[v] = K[6 * c] * prev[0].v[v];
+                        tn[v] = K[6 * c + 3] * next[0].v[v];
                     }
-                }
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) y[c][v] = fma(alj.v[v], (to[v] + tp[v]) + tn[v], y[c][v]);
+                    for (int d = 1; d < 3; ++d) {
+                        const double k_prev = K[6 * c + d], k_next = K[6 * c + 3 + d];
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) {
+                            tp[v] = fma(k_prev, prev[d].v[v], tp[v]);
+                            tn[v] = fma(k_next, next[d].v[v], tn[v]);
+                        }
+                    }
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) y[c][v] = fma(alj.v[v], tp[v] + tn[v], y[c][v]);
+                } else {
+                    // three independent 3-term chains (own, prev, next), then their sum: short
+                    // dependency chains for the FP64 pipe
+                    double to[VEC], tp[VEC], tn[VEC];
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) {
+                        to[v] = K[9 * c] * uo[0].v[v];
+                        tp[v] = K[9 * c + 3] * prev[0].v[v];
+                        tn[v] = K[9 * c + 6] * next[0].v[v];
+                    }
+#pragma unroll
+                    for (int d = 1; d < 3; ++d) {
+                        const double k_own = K[9 * c + d], k_prev = K[9 * c + 3 + d], k_next = K[9 * c + 6 + d];
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) {
+                            to[v] = fma(k_own, uo[d].v[v], to[v]);
+                            tp[v] = fma(k_prev, prev[d].v[v], tp[v]);
+                            tn[v] = fma(k_next, next[d].v[v], tn[v]);
+                        }
+                    }
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) y[c][v] = fma(alj.v[v], (to[v] + tp[v]) + tn[v], y[c][v]);
+                }
             }
         };
         // the previous neighbour of incidence j is next(j - 1) (carried in registers, no
@@ -601,11 +643,13 @@ __device__ __forceinline__ void mf_tile_rows(const StepArgs& a, const StepCtx& s
 #pragma unroll
         for (int j = 0; j < BATCH; ++j) {
             if (k + j >= ke) break;
-            const double* K = sK + (k + j) * 28;
+            const double* K = sK + (k + j) * L::kst;
             const bool restart = rec[j].w && k + j != kb;
+            if constexpr (DIFF) rel_to_own(un[j]);
             if (restart) {
 #pragma unroll
                 for (int d = 0; d < 3; ++d) up[d] = ld_ro<VEC>(un_base + (rec[j].y * W3 + d * n_s));
+                if constexpr (DIFF) rel_to_own(up);
             }
             if (j == 0 || restart) incidence(up, un[j], al[j], K);
             else incidence(un[j > 0 ? j - 1 : 0], un[j], al[j], K);
@@ -631,7 +675,7 @@ __device__ __forceinline__ void mf_tile_rows(const StepArgs& a, const StepCtx& s
     }
 }
 
-template <int VEC, bool APPLY, int BATCH, int MINB, int NS>
+template <int VEC, bool APPLY, int BATCH, int MINB, int NS, bool DIFF>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_step_matrix_free(const StepArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -660,7 +704,7 @@ k_step_matrix_free(const StepArgs a) {
 #pragma unroll
             for (int k = 0; k < kMaxFields; ++k) s_coef[k] = cv[k];
         }
-        mf_issue_tile<APPLY>(a, r0, r1, k0, k1, smem, bar);
+        mf_issue_tile<APPLY, DIFF>(a, r0, r1, k0, k1, smem, bar);
         // warm L2 for the tile that starts about when this one ends (one wave of CTAs
         // later): its K^ rows and fan records, so that its own TMA does not wait on DRAM
         const int64_t f0 = r0 + int64_t(gridDim.y > 0 ? kMfPrefetchWave : 0) * a.mf_rows * mf_wave_ctas(a);
@@ -669,14 +713,15 @@ k_step_matrix_free(const StepArgs a) {
             const int32_t q0 = __ldg(a.inc_ptr + f0), q1 = __ldg(a.inc_ptr + f1);
             if (q1 > q0) {
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                             :: "l"(a.Krow + size_t(q0) * 28), "r"(uint32_t(q1 - q0) * 224u) : "memory");
+                             :: "l"(a.Krow + size_t(q0) * MfLayout<DIFF>::kst),
+                                "r"(uint32_t(q1 - q0) * MfLayout<DIFF>::kbytes) : "memory");
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
                              :: "l"(a.fan + q0), "r"(uint32_t(q1 - q0) * 16u) : "memory");
             }
         }
     }
-    double* slot = reinterpret_cast<double*>(smem + mf_tile_bytes(a)) + size_t(threadIdx.x) * 6 * VEC;
-    mf_tile_rows<VEC, APPLY, BATCH, NS>(a, sc, s_coef, r0, r1, smem, slot, bar, 0);
+    double* slot = reinterpret_cast<double*>(smem + mf_tile_bytes<DIFF>(a)) + size_t(threadIdx.x) * 6 * VEC;
+    mf_tile_rows<VEC, APPLY, BATCH, NS, DIFF>(a, sc, s_coef, r0, r1, smem, slot, bar, 0);
 }
 
 __global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
@@ -808,11 +853,11 @@ static cudaError_t launch_a1(const StepArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int VEC, bool APPLY, int BATCH, int MINB, int NS>
+template <int VEC, bool APPLY, int BATCH, int MINB, int NS, bool DIFF>
 static cudaError_t launch_a2_ns(const StepArgs& a, cudaStream_t st) {
     if (a.V == 0) return cudaSuccess;
     const int P = a.n_s / VEC;
-    const size_t smem = size_t(a.mf_smem_inc) * 240 + size_t(a.n_fields) * a.mf_rows * 32 +
+    const size_t smem = size_t(a.mf_smem_inc) * MfLayout<DIFF>::inc + size_t(a.n_fields) * a.mf_rows * 32 +
                         size_t(a.mf_rows * a.mf_groups) * 6 * VEC * sizeof(double);
     // the shared-memory opt-in is a per-device function attribute: once per device and
     // template instance (contexts of one process may live on different devices)
@@ -821,7 +866,7 @@ static cudaError_t launch_a2_ns(const StepArgs& a, cudaStream_t st) {
     cudaGetDevice(&dev);
     const uint64_t bit = uint64_t(1) << (dev & 63);
     if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS>,
+        cudaError_t e = cudaFuncSetAttribute(k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS, DIFF>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(bit, std::memory_order_release);
@@ -833,7 +878,7 @@ static cudaError_t launch_a2_ns(const StepArgs& a, cudaStream_t st) {
         static int sms[64] = {0};
         const int d = dev & 63;
         if (per_sm[d] == 0) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[d], k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS>,
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[d], k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS, DIFF>,
                                                           a.mf_rows * a.mf_groups, smem);
             cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, dev);
             per_sm[d] = std::max(per_sm[d], 1);
@@ -842,17 +887,24 @@ static cudaError_t launch_a2_ns(const StepArgs& a, cudaStream_t st) {
         const bool on = e ? std::atoi(e) != 0 : true;
         b.mf_prefetch = on ? int32_t(int64_t(per_sm[d]) * sms[d] / std::max<unsigned>(grid.y, 1)) : 0;
     }
-    k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(b);
+    k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS, DIFF><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(b);
     return cudaGetLastError();
 }
 
 template <int VEC, bool APPLY, int BATCH, int MINB>
 static cudaError_t launch_a2(const StepArgs& a, cudaStream_t st) {
-    if constexpr (VEC == 2) {
-        if (a.n_s == 64) return launch_a2_ns<VEC, APPLY, BATCH, MINB, 64>(a, st);
-        if (a.n_s == 128) return launch_a2_ns<VEC, APPLY, BATCH, MINB, 128>(a, st);
+    if (!mf_diff()) {
+        if constexpr (VEC == 2) {
+            if (a.n_s == 64) return launch_a2_ns<VEC, APPLY, BATCH, MINB, 64, false>(a, st);
+            if (a.n_s == 128) return launch_a2_ns<VEC, APPLY, BATCH, MINB, 128, false>(a, st);
+        }
+        return launch_a2_ns<VEC, APPLY, BATCH, MINB, 0, false>(a, st);
     }
-    return launch_a2_ns<VEC, APPLY, BATCH, MINB, 0>(a, st);
+    if constexpr (VEC == 2) {
+        if (a.n_s == 64) return launch_a2_ns<VEC, APPLY, BATCH, MINB, 64, true>(a, st);
+        if (a.n_s == 128) return launch_a2_ns<VEC, APPLY, BATCH, MINB, 128, true>(a, st);
+    }
+    return launch_a2_ns<VEC, APPLY, BATCH, MINB, 0, true>(a, st);
 }
 
 cudaError_t launch_halo_signal(int32_t n_out, unsigned long long* const* out_flag, const int64_t* step_base,
@@ -901,6 +953,15 @@ cudaError_t launch_step_assembled(const StepArgs& a, cudaStream_t st) {
 // Matrix-free: VEC 2 (even N_s), batches of 2 incidences, >= 2 CTAs/SM; VEC 1 for odd N_s
 // (batch 2, >= 3 CTAs/SM).  The variants measured and dropped are listed in DESIGN.md §5.
 int pick_vec_mf(int32_t n_s) { return n_s % 2 == 0 ? 2 : 1; }
+
+bool mf_diff() {
+    static const bool on = [] {
+        const char* e = std::getenv("ENS_MF_DIFF");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return on;
+}
+int mf_inc_bytes() { return int(mf_diff() ? MfLayout<true>::inc : MfLayout<false>::inc); }
 
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
     const bool ap = a.y_out != nullptr;
