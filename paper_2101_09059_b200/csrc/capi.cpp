@@ -43,6 +43,8 @@ struct Part {
     uint8_t* d_fixed = nullptr;
     int32_t* d_inc_ptr = nullptr;
     int4* d_fan = nullptr;
+    int32_t* d_item_ptr = nullptr;                         // matrix-free item programs (F2w)
+    int4* d_items = nullptr;
     double *d_Krow = nullptr, *d_alpha = nullptr;
     int32_t mf_rows = 1, mf_groups = 1, mf_smem_inc = 0;
     int32_t *d_sym_lptr = nullptr, *d_sym_lidx = nullptr, *d_sym_lcol = nullptr, *d_sym_scol = nullptr;
@@ -322,6 +324,8 @@ ens::StepArgs part_args(const ens_ctx* c, const Part& p) {
     a.Kval = p.d_Kval;
     a.inc_ptr = p.d_inc_ptr;
     a.fan = p.d_fan;
+    a.item_ptr = p.d_item_ptr;
+    a.items = p.d_items;
     a.Krow = p.d_Krow;
     a.alpha = p.d_alpha;
     a.mf_rows = p.mf_rows;
@@ -349,6 +353,7 @@ ens::StepArgs part_args(const ens_ctx* c, const Part& p) {
     a.step_base = c->d_step;
     a.ubuf0 = p.d_u0;
     a.ubuf1 = p.d_u1;
+    a.u_rows = p.n_own + p.n_gh;
     a.flag = c->d_flag;
     a.coef_buf = c->d_coef;
     a.s_global0 = c->s_begin;
@@ -734,6 +739,26 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
                             k18[size_t(k) * 18 + size_t(6 * c + 3 * b + d)] =
                                 fans.Krow[size_t(k0 + k) * 28 + size_t(9 * c + 3 * (b + 1) + d)];
             RC_TRY(upload(c, &P.d_Krow, k18.data(), k18.size()));
+            // item programs of the per-warp streaming kernel (kernels.cu F2w): per row
+            // OWN, then per incidence [PREV at a chain start] INC, then OLD
+            std::vector<int32_t> iptr(size_t(P.n_own) + 1);
+            std::vector<int4> items;
+            items.reserve(size_t(P.n_own) * 2 + rec.size() * 2);
+            for (int64_t i = 0; i < P.n_own; ++i) {
+                iptr[size_t(i)] = int32_t(items.size());
+                const int32_t kb = ip[size_t(i)], ke = ip[size_t(i) + 1];
+                const int32_t ii = int32_t(i);
+                items.push_back(make_int4(ii, ii, 0, ens::kItemOwn | (kb == ke ? ens::kItemLastApply : 0)));
+                for (int32_t k = kb; k < ke; ++k) {
+                    const ens::FanRec& r = rec[size_t(k)];
+                    if (k == kb || r.restart) items.push_back(make_int4(r.n_prev, ii, 0, ens::kItemPrev));
+                    items.push_back(make_int4(r.n_next, r.e, k, ens::kItemInc | (k + 1 == ke ? ens::kItemLastApply : 0)));
+                }
+                items.push_back(make_int4(ii, ii, 0, ens::kItemOld | (int32_t(fx[size_t(i)]) << 8)));
+            }
+            iptr[size_t(P.n_own)] = int32_t(items.size());
+            RC_TRY(upload(c, &P.d_item_ptr, iptr.data(), iptr.size()));
+            RC_TRY(upload(c, &P.d_items, items.data(), items.size()));
         } else {
             RC_TRY(upload(c, &P.d_Krow, fans.Krow.data() + size_t(k0) * 28, size_t(k1 - k0) * 28));
         }

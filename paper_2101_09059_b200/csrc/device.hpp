@@ -12,6 +12,8 @@
 namespace ens {
 
 constexpr int kMaxFields = 4;
+// kinds of the matrix-free item programs (StepArgs::items, kernels.cu F2w)
+constexpr int kItemOwn = 0, kItemPrev = 1, kItemInc = 2, kItemOld = 3, kItemLastApply = 32;
 
 struct StepArgs {
     int64_t V = 0;            // rows handled by this launch: rows [row0, row0 + V)
@@ -36,6 +38,9 @@ struct StepArgs {
     int32_t mf_groups = 1;              // realisation groups (threads) per row per CTA
     int32_t mf_smem_inc = 0;            // max incidences staged by one CTA
     int32_t mf_prefetch = 0;            // L2 prefetch distance in tiles (set by the launcher)
+    // matrix-free item programs (kernels.cu F2w; built by capi.cpp when DIFF is on)
+    const int32_t* item_ptr = nullptr;  // [rows + 1]
+    const int4* items = nullptr;        // {node, elem | row, K^ row, kind | flags}
     // update coefficients
     const double* c1 = nullptr;
     const double* c2a = nullptr;        // null => scalars c2, c3
@@ -54,6 +59,7 @@ struct StepArgs {
     int64_t step_off = 0;
     double* ubuf0 = nullptr;
     double* ubuf1 = nullptr;
+    int64_t u_rows = 0;                 // rows of each state buffer (owned + ghosts)
     unsigned long long* flag = nullptr; // min over (step << 24 | s) of non-finite results
     double* coef_buf = nullptr;         // [2][kMaxFields] load coefficients of steps of each parity
     int32_t s_global0 = 0;
@@ -87,6 +93,7 @@ cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st);
 // realisations per thread of the step kernels for a given N_s (4, 2 or 1)
 int pick_vec(int32_t n_s);      // assembled kernel
 int pick_vec_mf(int32_t n_s);   // matrix-free kernel
+bool mf_warp_stream();     // matrix-free: per-warp TMA item streams (ENS_MF_WARP)
 bool mf_diff();            // matrix-free: neighbours relative to u_i, (prev, next) K^ columns only (ENS_MF_DIFF, default 1)
 int mf_inc_bytes();        // matrix-free: shared-memory bytes per incidence (K^ image + fan record)
 // coef_buf[(step & 1)] = the load coefficients of step *step_base (after host changes)

@@ -15,7 +15,11 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
+#include <vector>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <mutex>
 
 #include "device.hpp"
 
@@ -724,6 +728,213 @@ k_step_matrix_free(const StepArgs a) {
     mf_tile_rows<VEC, APPLY, BATCH, NS, DIFF>(a, sc, s_coef, r0, r1, smem, slot, bar, 0);
 }
 
+// ---- F2w: the matrix-free step as per-warp TMA item streams ------------------------------
+// Same arithmetic as F2 (DIFF form, same order: bit-identical), different data movement.
+// The host lays every row out as a short ITEM program (capi.cpp; int4 each):
+//   OWN  {i, i, -, kind}          u_i[3][64], c1_i[64], F_k(i) [n_fields][4]
+//   PREV {p, i, -, kind}          u_p[3][64]: first neighbour of a fan chain
+//   INC  {q, e, k, kind}          u_q[3][64], alpha_e[64], K^ row k [18]: incidence (e, i, p, q)
+//   OLD  {i, i, -, kind | fx<<8}  u_{n-1,i}[3][64]
+// Each warp of a persistent grid owns a contiguous range of rows and walks its items once
+// per 64-realisation slice.  Items move in GROUPS of B: lane j < B issues item j of a group
+// as 1-D bulk copies (cp.async.bulk, the TMA engine) into its slot of a per-warp ring of 2B
+// slots, completing on the slot's mbarrier; group n + 1 is issued when the warp starts
+// computing group n (whose B items it then consumes one by one, all 32 lanes x 2
+// realisations), so B to 2B items are in flight with no register held by a load.  The item
+// descriptors of group n + 2 are loaded (one per lane) while group n + 1 is issued.
+constexpr int kMfwSlice = 64;                 // realisations per unit (32 lanes x VEC 2)
+constexpr uint32_t kMfwU = 0, kMfwA = 1536, kMfwK = 2048, kMfwSlotBytes = 2304;   // 128-B aligned slots (tensor TMA)
+constexpr int kItOwn = kItemOwn, kItPrev = kItemPrev, kItInc = kItemInc, kItOld = kItemOld,
+              kItLastApply = kItemLastApply;
+
+// u[buffer] viewed as a 2-D tensor [rows * 3][n_s] (fp64), box [3][64]: one TMA copy moves
+// u[node][0..3][s0 .. s0 + 64) whatever N_s (1-D bulk copies when N_s = 64)
+struct MfwMaps {
+    CUtensorMap u[2];
+};
+
+template <bool APPLY, int WARPS, int B>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+k_step_mf_warp(const StepArgs a, const __grid_constant__ MfwMaps maps) {
+    constexpr int SLOTS = 2 * B;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = int(threadIdx.x) & 31, wid = int(threadIdx.x) >> 5;
+    unsigned char* ring = smem + size_t(wid) * SLOTS * kMfwSlotBytes;
+    int4* tags = reinterpret_cast<int4*>(smem + size_t(WARPS) * SLOTS * kMfwSlotBytes) + wid * SLOTS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(WARPS) * SLOTS * (kMfwSlotBytes + sizeof(int4))) +
+                     wid * SLOTS;
+    const uint32_t ring_s = uint32_t(__cvta_generic_to_shared(ring));
+    const uint32_t bar_s = uint32_t(__cvta_generic_to_shared(bars));
+    if (lane < SLOTS) mbar_init(bar_s + 8u * lane, 1);
+    __syncwarp();
+
+    const StepCtx sc = step_ctx(a);
+    const int n_s = a.n_s;
+    double coef[kMaxFields];
+    if (!APPLY) {
+        const double* cb = step_coef(a, sc);
+#pragma unroll
+        for (int k = 0; k < kMaxFields; ++k) coef[k] = k < a.n_fields ? cb[k] : 0.0;
+    }
+    // this warp's rows [ra, rb) -> items [qa, qb), walked once per slice
+    const int64_t nw = int64_t(gridDim.x) * WARPS, w = int64_t(blockIdx.x) * WARPS + wid;
+    const int64_t ra = a.row0 + a.V * w / nw, rb = a.row0 + a.V * (w + 1) / nw;
+    if (ra >= rb) return;
+    const int32_t qa = __ldg(a.item_ptr + ra), cnt = __ldg(a.item_ptr + rb) - qa;
+    const int32_t total = cnt * (n_s / kMfwSlice);
+    const int32_t ngroups = (total + B - 1) / B;
+
+    // item j of group n (lanes j < B): its descriptor, slice in bits 16.. of .w; the lane's
+    // (slice, local index) cursor advances by B items per group
+    int32_t ld_sl = 0, ld_loc = lane;
+    while (lane < B && ld_loc >= cnt) { ld_loc -= cnt; ++ld_sl; }
+    int32_t ld_g = lane;
+    auto load_item = [&]() {
+        int4 it = make_int4(0, 0, 0, -1);
+        if (lane < B && ld_g < total) {
+            it = __ldg(a.items + qa + ld_loc);
+            it.w |= ld_sl << 16;
+        }
+        ld_g += B;
+        ld_loc += B;
+        while (ld_loc >= cnt) { ld_loc -= cnt; ++ld_sl; }
+        return it;
+    };
+    auto issue = [&](int32_t n, const int4& it) {
+        if (it.w < 0) return;
+        const int slot = (n & 1) * B + lane;
+        const uint32_t dst = ring_s + uint32_t(slot) * kMfwSlotBytes, bar = bar_s + 8u * slot;
+        const int kind = it.w & 15;
+        const int s0 = (it.w >> 16) * kMfwSlice;
+        tags[slot] = it;
+        if (APPLY && kind == kItOld) {                   // nothing to move: completes at once
+            mbar_expect_tx(bar, 0u);
+            return;
+        }
+        uint32_t bytes = 3u * kMfwSlice * 8u;
+        if (kind == kItInc) bytes += kMfwSlice * 8u + 144u;
+        else if (kind == kItOwn && !APPLY) bytes += kMfwSlice * 8u + uint32_t(a.n_fields) * 32u;
+        mbar_expect_tx(bar, bytes);
+        const bool old = kind == kItOld;
+        if (n_s == kMfwSlice) {
+            tma_bulk_g2s(dst + kMfwU, (old ? sc.uo : sc.un) + int64_t(it.x) * 3 * n_s, 3u * kMfwSlice * 8u, bar);
+        } else {        // u_n = buffer (step & 1), u_{n-1} the other (step_ctx)
+            const CUtensorMap* m = &maps.u[int((sc.step & 1) ^ (old ? 1 : 0))];
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                         " [%0], [%1, {%2, %3}], [%4];"
+                         :: "r"(dst + kMfwU), "l"(reinterpret_cast<uint64_t>(m)), "r"(s0), "r"(it.x * 3), "r"(bar)
+                         : "memory");
+        }
+        if (kind == kItInc) {
+            tma_bulk_g2s(dst + kMfwA, a.alpha + int64_t(it.y) * n_s + s0, kMfwSlice * 8u, bar);
+            tma_bulk_g2s(dst + kMfwK, a.Krow + int64_t(it.z) * 18, 144u, bar);
+        } else if (kind == kItOwn && !APPLY) {
+            tma_bulk_g2s(dst + kMfwA, a.c1 + int64_t(it.x) * n_s + s0, kMfwSlice * 8u, bar);
+            for (int f = 0; f < a.n_fields; ++f)
+                tma_bulk_g2s(dst + kMfwK + 32u * f, a.Fk + (int64_t(f) * a.fk_rows + it.x) * 4, 32u, bar);
+        }
+    };
+
+    int4 pf = load_item();
+    issue(0, pf);
+    pf = load_item();
+
+    double y[3][2];
+    Vec<2> uo[3], up[3];
+    Upd<2> upd;
+    int32_t cur_row = 0;
+    const int v0 = 2 * lane;
+    for (int32_t n = 0; n < ngroups; ++n) {
+        if (n + 1 < ngroups) {                           // group n - 1's slots are free
+            issue(n + 1, pf);
+            pf = load_item();
+        }
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            if (n * B + j >= total) break;
+            const int slot = (n & 1) * B + j;
+            mbar_wait(bar_s + 8u * slot, uint32_t(n >> 1) & 1u);
+            const int4 t = tags[slot];
+            const double* S = reinterpret_cast<const double*>(ring + size_t(slot) * kMfwSlotBytes);
+            const int kind = t.w & 15;
+            Vec<2> ux[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const double2 x = *reinterpret_cast<const double2*>(S + d * kMfwSlice + v0);
+                ux[d].v[0] = x.x; ux[d].v[1] = x.y;
+            }
+            if (kind == kItInc) {
+                const double2 xa = *reinterpret_cast<const double2*>(S + kMfwA / 8 + v0);
+#pragma unroll
+                for (int d = 0; d < 3; ++d) { ux[d].v[0] -= uo[d].v[0]; ux[d].v[1] -= uo[d].v[1]; }
+                const double* K = S + kMfwK / 8;
+                const double alv[2] = {xa.x, xa.y};
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double tp[2], tn[2];
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) {
+                        tp[v] = K[6 * c] * up[0].v[v];
+                        tn[v] = K[6 * c + 3] * ux[0].v[v];
+                    }
+#pragma unroll
+                    for (int d = 1; d < 3; ++d) {
+                        const double k_prev = K[6 * c + d], k_next = K[6 * c + 3 + d];
+#pragma unroll
+                        for (int v = 0; v < 2; ++v) {
+                            tp[v] = fma(k_prev, up[d].v[v], tp[v]);
+                            tn[v] = fma(k_next, ux[d].v[v], tn[v]);
+                        }
+                    }
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) y[c][v] = fma(alv[v], tp[v] + tn[v], y[c][v]);
+                }
+#pragma unroll
+                for (int d = 0; d < 3; ++d) up[d] = ux[d];
+                if (APPLY && (t.w & kItLastApply)) store_y<2>(a, cur_row, (t.w >> 16) * kMfwSlice + v0, y);
+            } else if (kind == kItPrev) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    up[d].v[0] = ux[d].v[0] - uo[d].v[0];
+                    up[d].v[1] = ux[d].v[1] - uo[d].v[1];
+                }
+            } else if (kind == kItOwn) {
+                cur_row = t.y;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    y[c][0] = y[c][1] = 0.0;
+                    uo[c] = ux[c];
+                }
+                if (!APPLY) {
+                    const double2 xa = *reinterpret_cast<const double2*>(S + kMfwA / 8 + v0);
+                    upd.c1.v[0] = xa.x; upd.c1.v[1] = xa.y;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        double f = 0.0;
+#pragma unroll
+                        for (int fk = 0; fk < kMaxFields; ++fk)
+                            if (fk < a.n_fields) f = fma(coef[fk], S[kMfwK / 8 + fk * 4 + c], f);
+                        upd.f[c] = f;
+                    }
+                } else if (t.w & kItLastApply) {
+                    store_y<2>(a, cur_row, (t.w >> 16) * kMfwSlice + v0, y);
+                }
+            } else if (!APPLY) {                         // OLD: the update finishes the row
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    upd.uo[d] = ux[d];
+                    upd.un[d] = uo[d];
+                }
+                upd.c2.v[0] = upd.c2.v[1] = a.c2;
+                upd.c3.v[0] = upd.c3.v[1] = a.c3;
+                upd.fx = uint8_t((t.w >> 8) & 0xff);
+                upd_store<2>(a, sc, t.y, (t.w >> 16) * kMfwSlice + v0, y, upd);
+            }
+        }
+        __syncwarp();                                    // group n's slots are free for group n + 2
+    }
+}
+
 __global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
 
 // FP64 FMA throughput probe (the ALU roofline of the matrix-free step):
@@ -963,8 +1174,102 @@ bool mf_diff() {
 }
 int mf_inc_bytes() { return int(mf_diff() ? MfLayout<true>::inc : MfLayout<false>::inc); }
 
+bool mf_warp_stream() {
+    static const bool on = [] {
+        const char* e = std::getenv("ENS_MF_WARP");
+        return e ? std::atoi(e) != 0 : false;
+    }();
+    return on;
+}
+
+// Tensor map of one state buffer [rows * 3][n_s] fp64 with a [3][64] box, encoded once per
+// (buffer, rows, n_s) through the driver entry point (no -lcuda) and cached.
+static cudaError_t mfw_u_map(const double* base, int64_t rows, int n_s, CUtensorMap* out) {
+    struct Entry {
+        const double* base;
+        int64_t rows;
+        int n_s;
+        CUtensorMap map;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Entry& e : cache)
+        if (e.base == base && e.rows == rows && e.n_s == n_s) {
+            *out = e.map;
+            return cudaSuccess;
+        }
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    Entry en{base, rows, n_s, {}};
+    const cuuint64_t dims[2] = {cuuint64_t(n_s), cuuint64_t(rows) * 3};
+    const cuuint64_t strides[1] = {cuuint64_t(n_s) * sizeof(double)};
+    const cuuint32_t box[2] = {cuuint32_t(kMfwSlice), 3u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = encode(&en.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
+                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    if (cache.size() >= 64) cache.erase(cache.begin());
+    cache.push_back(en);
+    *out = en.map;
+    return cudaSuccess;
+}
+
+template <bool APPLY, int WARPS, int B>
+static cudaError_t launch_mf_warp_t(const StepArgs& a, cudaStream_t st) {
+    if (a.V == 0) return cudaSuccess;
+    const size_t smem = size_t(WARPS) * 2 * B * (kMfwSlotBytes + sizeof(int4) + sizeof(uint64_t));
+    static std::atomic<uint64_t> attr_set{0};
+    static int sms[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (!(attr_set.load(std::memory_order_acquire) & bit)) {
+        cudaError_t e = cudaFuncSetAttribute(k_step_mf_warp<APPLY, WARPS, B>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+        attr_set.fetch_or(bit, std::memory_order_release);
+    }
+    MfwMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    if (a.n_s != kMfwSlice) {
+        cudaError_t e = mfw_u_map(a.ubuf0, a.u_rows, a.n_s, &maps.u[0]);
+        if (e == cudaSuccess) e = mfw_u_map(a.ubuf1, a.u_rows, a.n_s, &maps.u[1]);
+        if (e != cudaSuccess) return e;
+    }
+    // one CTA per SM (persistent); fewer when the rows would leave warps empty
+    const int64_t max_ctas = (a.V + WARPS - 1) / WARPS;
+    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(sms[dev & 63], max_ctas)));
+    k_step_mf_warp<APPLY, WARPS, B><<<grid, WARPS * 32, smem, st>>>(a, maps);
+    return cudaGetLastError();
+}
+
+template <bool APPLY>
+static cudaError_t launch_mf_warp(const StepArgs& a, cudaStream_t st) {
+    static const int cfg = [] {
+        const char* e = std::getenv("ENS_MFW_CFG");
+        return e ? std::atoi(e) : 0;
+    }();
+    switch (cfg) {
+        case 1: return launch_mf_warp_t<APPLY, 16, 2>(a, st);
+        case 2: return launch_mf_warp_t<APPLY, 12, 4>(a, st);
+        case 3: return launch_mf_warp_t<APPLY, 8, 6>(a, st);
+        default: return launch_mf_warp_t<APPLY, 16, 3>(a, st);
+    }
+}
+
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
     const bool ap = a.y_out != nullptr;
+    if (mf_warp_stream() && a.items && !a.c2a && a.n_s % kMfwSlice == 0)
+        return ap ? launch_mf_warp<true>(a, st) : launch_mf_warp<false>(a, st);
     if (pick_vec_mf(a.n_s) == 2) return ap ? launch_a2<2, true, 2, 2>(a, st) : launch_a2<2, false, 2, 2>(a, st);
     return ap ? launch_a2<1, true, 2, 3>(a, st) : launch_a2<1, false, 2, 3>(a, st);
 }
