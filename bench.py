@@ -27,6 +27,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# the device function each --kernel runs (matrix-free: per-warp TMA item streams when the
+# library chose them, ens_info.mf_variant)
+_KERNEL_FN = {"assembled": lambda info: "k_step_assembled",
+              "assembled_sym": lambda info: "k_step_assembled_sym",
+              "matrix_free": lambda info: "k_step_mf_warp" if info.get("mf_variant") else "k_step_matrix_free"}
 METRIC = ("ensemble DOF-updates/s (N_s×DOF×steps/s) and fused-step HBM GB/s vs peak")
 FALLBACK_HBM_GBS = 6650.0      # /opt/skills/guides/B200_PROFILING.md fallback
 
@@ -299,6 +304,7 @@ def _time_kernel(kernel, args, cfg, m, tr, world, rank, local, stream, barrier, 
     return {"value": world * cfg.n_s * 3 * m.n_nodes * args.steps / el, "unit": "DOF-updates/s",
             "ms_per_step": 1e3 * el / args.steps, "achieved_GBs": ach, "frac": ach / peak,
             "algorithmic_bytes_per_launch": info["bytes_per_step"], "achieved_fp64_TFLOPs": tf,
+            "kernel_fn": _KERNEL_FN[kernel](info),
             "algorithmic_flops_per_launch": info["flops_per_step"]}
 
 
@@ -471,8 +477,7 @@ def main(argv=None):
                        "l2": f"inputs larger than L2: {info['bytes_per_step'] / 1e9:.3f} GB streamed per step vs 126 MB L2 (no flush)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": {"assembled": "k_step_assembled", "assembled_sym": "k_step_assembled_sym",
-                                    "matrix_free": "k_step_matrix_free"}[args.kernel],
+                         "kernel": _KERNEL_FN[args.kernel](info),
                          "algorithmic_bytes_per_launch": info["bytes_per_step"],
                          "read_stream_GBs": read_gbs, "frac_of_read_stream": achieved / read_gbs if read_gbs else None,
                          "fp64": {"achieved_TFLOPs": tf_head, "peak_TFLOPs": fp64_peak,

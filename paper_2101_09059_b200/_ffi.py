@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libens.so")
+LIB_PATH = os.environ.get("ENS_LIB_PATH") or os.path.join(_HERE, "libens.so")   # override: A/B builds only
 
 ENS_OK, ENS_E_ARG, ENS_E_MESH, ENS_E_OOM, ENS_E_CUDA, ENS_E_NCCL, ENS_E_DIVERGED, ENS_E_STATE, \
     ENS_E_UNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7, -8
@@ -48,7 +48,7 @@ class EnsInfo(C.Structure):
                 ("device_bytes", C.c_int64), ("rcm_bandwidth", C.c_int32),
                 ("n_owned", C.c_int64), ("halo_bytes_per_step", C.c_int64),
                 ("launches_per_step", C.c_int32), ("reassemble_every", C.c_int32), ("graph_steps", C.c_int32),
-                ("halo", C.c_int32)]
+                ("halo", C.c_int32), ("mf_variant", C.c_int32)]
 
 
 EXPORTS = [
@@ -76,7 +76,7 @@ def lib():
     if _lib is not None:
         return _lib
     from . import build as _build
-    if _build.stale() and os.path.exists(_build.NVCC):
+    if LIB_PATH == _build.LIB and _build.stale() and os.path.exists(_build.NVCC):
         _build.build()
     if not os.path.exists(LIB_PATH):
         raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")

@@ -1177,7 +1177,7 @@ int mf_inc_bytes() { return int(mf_diff() ? MfLayout<true>::inc : MfLayout<false
 bool mf_warp_stream() {
     static const bool on = [] {
         const char* e = std::getenv("ENS_MF_WARP");
-        return e ? std::atoi(e) != 0 : false;
+        return e ? std::atoi(e) != 0 : true;
     }();
     return on;
 }
@@ -1252,18 +1252,12 @@ static cudaError_t launch_mf_warp_t(const StepArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// 16 warps x 6 slots of 2304 B (B = 3 items per group): 221 KB of ring per SM.  Measured
+// and dropped: 16 x 4, 12 x 8 and 8 x 12 slots; the descriptors staged in
+// shared memory by cp.async or by bulk copies instead of one register load per group.
 template <bool APPLY>
 static cudaError_t launch_mf_warp(const StepArgs& a, cudaStream_t st) {
-    static const int cfg = [] {
-        const char* e = std::getenv("ENS_MFW_CFG");
-        return e ? std::atoi(e) : 0;
-    }();
-    switch (cfg) {
-        case 1: return launch_mf_warp_t<APPLY, 16, 2>(a, st);
-        case 2: return launch_mf_warp_t<APPLY, 12, 4>(a, st);
-        case 3: return launch_mf_warp_t<APPLY, 8, 6>(a, st);
-        default: return launch_mf_warp_t<APPLY, 16, 3>(a, st);
-    }
+    return launch_mf_warp_t<APPLY, 16, 3>(a, st);
 }
 
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
