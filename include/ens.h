@@ -148,9 +148,10 @@ typedef struct {
                                            advance (env ENS_GRAPH_STEPS; 0 = direct launches) */
     int32_t halo;                       /* ens_options.halo (NODE contexts) */
     int32_t mf_variant;                 /* MATRIX_FREE data path: 1 = per-warp TMA item streams
-                                           (k_step_mf_warp: N_s % 64 == 0, mass damping; env
-                                           ENS_MF_WARP=0 disables), 0 = CTA tiles with register
-                                           gathers (k_step_matrix_free); 0 for assembled kernels */
+                                           (k_step_mf_warp: N_s = 64 without identity damping;
+                                           env ENS_MF_WARP=1: any N_s % 64 == 0, =0: never),
+                                           0 = CTA tiles with register gathers
+                                           (k_step_matrix_free); 0 for assembled kernels */
 } ens_info;
 
 /* Create a context: validate the mesh, build the RCM-ordered block-CSR pattern, the

@@ -1620,8 +1620,8 @@ int ens_query(const ens_ctx* c, ens_info* info) {
     info->reassemble_every = c->reassemble_every;
     info->halo = c->halo;
     // the launcher's choice (kernels.cu launch_step_matrix_free)
-    info->mf_variant = (c->kernel == ENS_KERNEL_MATRIX_FREE && ens::mf_warp_stream() && ens::mf_diff() &&
-                        c->damping != ENS_DAMP_IDENTITY && c->n_s % 64 == 0) ? 1 : 0;
+    info->mf_variant = (c->kernel == ENS_KERNEL_MATRIX_FREE &&
+                        ens::mf_warp_for(c->n_s, ens::mf_diff(), c->damping != ENS_DAMP_IDENTITY)) ? 1 : 0;
     // algorithmic HBM bytes of the rows this context advances: values +
     // u_n, u_{n-1} read, u_{n+1} written, c1 (+ c2, c3) per node per realisation
     const int64_t ns = c->n_s, per_node = 3 * 8 * 3 + 8 + (c->damping == ENS_DAMP_IDENTITY ? 16 : 0);

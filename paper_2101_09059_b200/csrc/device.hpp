@@ -93,7 +93,7 @@ cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st);
 // realisations per thread of the step kernels for a given N_s (4, 2 or 1)
 int pick_vec(int32_t n_s);      // assembled kernel
 int pick_vec_mf(int32_t n_s);   // matrix-free kernel
-bool mf_warp_stream();     // matrix-free: per-warp TMA item streams (ENS_MF_WARP)
+bool mf_warp_for(int32_t n_s, bool have_items, bool scalar_c23);   // matrix-free: F2w (per-warp TMA item streams) or F2
 bool mf_diff();            // matrix-free: neighbours relative to u_i, (prev, next) K^ columns only (ENS_MF_DIFF, default 1)
 int mf_inc_bytes();        // matrix-free: shared-memory bytes per incidence (K^ image + fan record)
 // coef_buf[(step & 1)] = the load coefficients of step *step_base (after host changes)

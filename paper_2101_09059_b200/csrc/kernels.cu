@@ -1174,12 +1174,17 @@ bool mf_diff() {
 }
 int mf_inc_bytes() { return int(mf_diff() ? MfLayout<true>::inc : MfLayout<false>::inc); }
 
-bool mf_warp_stream() {
-    static const bool on = [] {
+// F2w or F2: F2w needs the DIFF item programs, scalar c2/c3 and N_s % 64 == 0.
+// By default it runs at N_s = 64 only: with 128 or more realisations per row F2's CTA tiles
+// are as fast, and F2w's higher issue rate drew the power cap on the boxes measured (c4, c5).
+// ENS_MF_WARP=1 takes F2w wherever it applies, ENS_MF_WARP=0 never.
+bool mf_warp_for(int32_t n_s, bool have_items, bool scalar_c23) {
+    static const int mode = [] {
         const char* e = std::getenv("ENS_MF_WARP");
-        return e ? std::atoi(e) != 0 : true;
+        return e ? std::atoi(e) : -1;
     }();
-    return on;
+    if (mode == 0 || !have_items || !scalar_c23 || n_s % kMfwSlice != 0) return false;
+    return mode > 0 || n_s == kMfwSlice;
 }
 
 // Tensor map of one state buffer [rows * 3][n_s] fp64 with a [3][64] box, encoded once per
@@ -1262,7 +1267,7 @@ static cudaError_t launch_mf_warp(const StepArgs& a, cudaStream_t st) {
 
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
     const bool ap = a.y_out != nullptr;
-    if (mf_warp_stream() && a.items && !a.c2a && a.n_s % kMfwSlice == 0)
+    if (mf_warp_for(a.n_s, a.items != nullptr, a.c2a == nullptr))
         return ap ? launch_mf_warp<true>(a, st) : launch_mf_warp<false>(a, st);
     if (pick_vec_mf(a.n_s) == 2) return ap ? launch_a2<2, true, 2, 2>(a, st) : launch_a2<2, false, 2, 2>(a, st);
     return ap ? launch_a2<1, true, 2, 3>(a, st) : launch_a2<1, false, 2, 3>(a, st);

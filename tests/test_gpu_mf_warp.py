@@ -1,5 +1,6 @@
 """The per-warp TMA item-stream form of the matrix-free step (kernels.cu F2w,
-k_step_mf_warp; the library's choice for N_s % 64 == 0 with mass damping) on a B200 (-m gpu).
+k_step_mf_warp; the library's choice at N_s = 64 without identity damping; ENS_MF_WARP=1
+takes it for any N_s % 64 == 0, exercised here in subprocesses) on a B200 (-m gpu).
 
 F2w computes exactly F2's arithmetic in F2's order, so it is held to the
 oracle's bars (SpMM <= 1e-12, steps <= 1e-9 relative L2) and, against F2 itself
@@ -31,10 +32,10 @@ def _mats(m, n_s, seed):
     return E, h
 
 
-@pytest.mark.parametrize("n_s", [64, 128])
+@pytest.mark.parametrize("n_s", [64])
 def test_mf_warp_vs_oracle_nonmanifold(n_s):
     """Fan restarts (bowtie vertices) and a second component through the item programs:
-    PREV items at every chain start; N_s = 128 takes the 2-D tensor copies of u."""
+    PREV items at every chain start."""
     m = meshmod.shuffle_nodes(_nonmanifold_mesh(), 11)
     E, h = _mats(m, n_s, 43)
     ens, om = _pair(m, E, h, kernel="matrix_free", damping="mass", c_d=150.0)
@@ -75,8 +76,9 @@ print(json.dumps({{"mf_variant": ens.info()["mf_variant"], "step": s}}))
 
 @pytest.mark.parametrize("n_s", [64, 128, 192])
 def test_mf_warp_bitexact_vs_tile_kernel(n_s, tmp_path):
-    """Same inputs through F2 (ENS_MF_WARP=0) and F2w: states after 400 pulsatile steps
-    (two load fields staged per OWN item) and one product y = K x, bit for bit."""
+    """Same inputs through F2 (ENS_MF_WARP=0) and F2w (ENS_MF_WARP=1; N_s > 64 takes the
+    2-D tensor copies of u): states after 400 pulsatile steps (two load fields staged per
+    OWN item) and one product y = K x, bit for bit."""
     res = {}
     for flag in ("0", "1"):
         out = str(tmp_path / f"mf{flag}.npz")
@@ -119,7 +121,7 @@ def test_mf_warp_not_used_for_identity_damping_or_odd_ns():
     """The launcher falls back to F2 where F2w does not apply (mode-2 damping stages c2, c3;
     N_s not a multiple of 64)."""
     m = meshmod.cylinder(12, 23)
-    for n_s, damping in ((64, "identity"), (48, "mass")):
+    for n_s, damping in ((64, "identity"), (48, "mass"), (96, "none")):
         E, h = _mats(m, n_s, 3)
         ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, kernel="matrix_free",
                               damping=damping, c_d=10.0)
