@@ -1258,7 +1258,7 @@ static cudaError_t launch_mf_warp_t(const StepArgs& a, cudaStream_t st) {
 }
 
 // 16 warps x 6 slots of 2304 B (B = 3 items per group): 221 KB of ring per SM.  Measured
-// and dropped: 16 x 4, 12 x 8 and 8 x 12 slots; the descriptors staged in
+// and dropped: 16 x 4, 12 x 8, 8 x 12, 20 x 4 and 24 x 2 slots; the descriptors staged in
 // shared memory by cp.async or by bulk copies instead of one register load per group.
 template <bool APPLY>
 static cudaError_t launch_mf_warp(const StepArgs& a, cudaStream_t st) {
