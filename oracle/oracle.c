@@ -73,6 +73,14 @@ int orc_validate_mesh(int64_t V, int64_t F, const double* xyz, const int32_t* tr
     for (int64_t k = 0; k + 2 < 3 * F; k++)
         if (cmp_pair(pairs + 2 * k, pairs + 2 * (k + 2)) == 0) { *bad = pairs[2 * k]; rc = 4; break; }
     free(pairs);
+    if (rc) return rc;
+    /* a node in no triangle has lumped mass 0 (m_i = rho sum_e A_e zeta/3), */
+    /* the divisor of Eq. 22's update: rejected                                           */
+    char* used = (char*)calloc((size_t)(V > 0 ? V : 1), 1);
+    for (int64_t k = 0; k < 3 * F; k++) used[tris[k]] = 1;
+    for (int64_t i = 0; i < V; i++)
+        if (!used[i]) { *bad = i; rc = 5; break; }
+    free(used);
     return rc;
 }
 

@@ -715,12 +715,19 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
         const int Pg = c->n_s / ens::pick_vec_mf(c->n_s);
         P.mf_groups = std::min(Pg, 256);
         P.mf_rows = std::max(1, std::min(256 / P.mf_groups, 32));
+        // launch_rows tiles [row0, row0 + rows) from row0: the whole range (no halo), and with
+        // a halo the boundary ranges [0, b_lo), [n_own - b_hi, n_own) and the interior
+        // [b_lo, n_own - b_hi) — every tiling launched sizes the shared-memory image
+        std::vector<std::pair<int64_t, int64_t>> tilings = {{0, P.n_own}};
+        if (pl.b_lo || pl.b_hi)
+            tilings.insert(tilings.end(), {{0, pl.b_lo}, {P.n_own - pl.b_hi, P.n_own}, {pl.b_lo, P.n_own - pl.b_hi}});
         for (;;) {
             int32_t mx = 0;
-            for (int64_t r0 = 0; r0 < P.n_own; r0 += P.mf_rows) {
-                const int64_t r1 = std::min<int64_t>(r0 + P.mf_rows, P.n_own);
-                mx = std::max(mx, ip[size_t(r1)] - ip[size_t(r0)]);
-            }
+            for (const auto& tl : tilings)
+                for (int64_t r0 = tl.first; r0 < tl.second; r0 += P.mf_rows) {
+                    const int64_t r1 = std::min<int64_t>(r0 + P.mf_rows, tl.second);
+                    mx = std::max(mx, ip[size_t(r1)] - ip[size_t(r0)]);
+                }
             P.mf_smem_inc = mx;
             if (int64_t(mx) * ens::mf_inc_bytes() <= 96 * 1024 || P.mf_rows == 1) break;
             P.mf_rows = std::max(1, P.mf_rows / 2);
@@ -982,7 +989,8 @@ int arg_check(const ens_mesh* mesh, const ens_materials* mat) {
     const int vcode = ens::validate_mesh(m, &bad);
     if (vcode) {
         static const char* what[] = {"", "node index out of range in element ", "repeated node in element ",
-                                     "degenerate (zero-area) element ", "edge shared by more than two triangles at node "};
+                                     "degenerate (zero-area) element ", "edge shared by more than two triangles at node ",
+                                     "node in no triangle (zero lumped mass): node "};
         return fail(nullptr, ENS_E_MESH, std::string(what[vcode]) + std::to_string(bad));
     }
     return ENS_OK;

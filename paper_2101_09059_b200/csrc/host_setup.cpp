@@ -53,6 +53,12 @@ int validate_mesh(const MeshView& m, int64_t* bad) {
     std::sort(keys.begin(), keys.end());
     for (size_t k = 0; k + 2 < keys.size(); ++k)
         if (keys[k] == keys[k + 2]) { *bad = int64_t(keys[k] >> 32); return 4; }
+    // every node must lie in a triangle: its lumped mass rho sum A_e zeta/3
+    // is the divisor of c1, so an unreferenced node would turn the first step into NaN
+    std::vector<char> used(size_t(m.V), 0);
+    for (int64_t k = 0; k < 3 * m.F; ++k) used[size_t(m.tris[k])] = 1;
+    for (int64_t i = 0; i < m.V; ++i)
+        if (!used[size_t(i)]) { *bad = i; return 5; }
     return 0;
 }
 

@@ -12,6 +12,7 @@
 // fma(): the per-realisation arithmetic is identical whatever N_s, VEC or the launch
 // geometry, which makes ensemble runs bit-identical to single-realisation runs.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
@@ -570,8 +571,8 @@ __device__ __forceinline__ void mf_tile_rows(const StepArgs& a, const StepCtx& s
     mbar_wait(bar, phase);
     if (!valid) return;
 
-    // 32-bit element offsets (V * 3 * N_s and F * N_s stay below 2^31 up to config c5)
-    const int W3 = 3 * n_s;
+    // 64-bit element offsets: V * 3 * N_s and F * N_s may exceed 2^31 (c5 at N_s >= 1,024)
+    const int64_t W3 = 3 * int64_t(n_s);
     const double* al_base = a.alpha + s0;
     const int32_t k0 = __ldg(a.inc_ptr + r0);
     const int32_t kb = __ldg(a.inc_ptr + i) - k0, ke = __ldg(a.inc_ptr + i + 1) - k0;
@@ -591,7 +592,7 @@ __device__ __forceinline__ void mf_tile_rows(const StepArgs& a, const StepCtx& s
                 rec[j] = sRec[k + j];
 #pragma unroll
                 for (int d = 0; d < 3; ++d) un[j][d] = ld_ro<VEC>(un_base + (rec[j].z * W3 + d * n_s));
-                al[j] = ld_ro<VEC>(al_base + rec[j].x * n_s);
+                al[j] = ld_ro<VEC>(al_base + int64_t(rec[j].x) * n_s);
             }
         }
         // incidence (e, i, prev, next): y += alpha_e (K_own u_i + K_prev u_prev + K_next u_next)
@@ -700,6 +701,9 @@ k_step_matrix_free(const StepArgs a) {
         // the incidence range and the load coefficients are independent loads: both in
         // flight at once, then s_coef, then the expect_tx arrive that publishes it
         const int32_t k0 = __ldg(a.inc_ptr + r0), k1 = __ldg(a.inc_ptr + r1);
+        // the host sizes mf_smem_inc over every tiling it launches (capi.cpp build_part);
+        // a tile beyond it would overrun the shared-memory image: fail loudly, never corrupt
+        if (k1 - k0 > a.mf_smem_inc) __trap();
         if (!APPLY) {
             const double* cb = step_coef(a, sc);
             double cv[kMaxFields];
@@ -1084,19 +1088,29 @@ static cudaError_t launch_a2_ns(const StepArgs& a, cudaStream_t st) {
     }
     dim3 grid(unsigned((a.V + a.mf_rows - 1) / a.mf_rows), unsigned((P + a.mf_groups - 1) / a.mf_groups));
     StepArgs b = a;
-    {   // tiles resident at once (one wave): the L2 prefetch distance, in tiles
-        static int per_sm[64] = {0};
-        static int sms[64] = {0};
-        const int d = dev & 63;
-        if (per_sm[d] == 0) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[d], k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS, DIFF>,
-                                                          a.mf_rows * a.mf_groups, smem);
-            cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, dev);
-            per_sm[d] = std::max(per_sm[d], 1);
+    {   // tiles resident at once (one wave): the L2 prefetch distance, in tiles.  Occupancy
+        // depends on the block shape and shared memory of this context, so it is cached per
+        // (device, threads, smem) under a lock (contexts may differ and run on several threads)
+        static std::mutex mu;
+        static std::vector<std::array<int64_t, 4>> cache;     // {dev, threads, smem, resident CTAs}
+        const int threads = a.mf_rows * a.mf_groups;
+        int64_t resident = 0;
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            for (const auto& q : cache)
+                if (q[0] == dev && q[1] == threads && q[2] == int64_t(smem)) resident = q[3];
+            if (resident == 0) {
+                int per_sm = 0, sms = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS, DIFF>,
+                                                              threads, smem);
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                resident = int64_t(std::max(per_sm, 1)) * std::max(sms, 1);
+                cache.push_back({int64_t(dev), int64_t(threads), int64_t(smem), resident});
+            }
         }
         const char* e = std::getenv("ENS_MF_PREFETCH");
         const bool on = e ? std::atoi(e) != 0 : true;
-        b.mf_prefetch = on ? int32_t(int64_t(per_sm[d]) * sms[d] / std::max<unsigned>(grid.y, 1)) : 0;
+        b.mf_prefetch = on ? int32_t(resident / std::max<unsigned>(grid.y, 1)) : 0;
     }
     k_step_matrix_free<VEC, APPLY, BATCH, MINB, NS, DIFF><<<grid, unsigned(a.mf_rows * a.mf_groups), smem, st>>>(b);
     return cudaGetLastError();

@@ -71,6 +71,7 @@ def test_validate_codes_match_oracle():
     x = m.xyz.copy(); x[m.tris[5, 2]] = x[m.tris[5, 0]] + 0.5 * (x[m.tris[5, 1]] - x[m.tris[5, 0]])
     cases.append((x, m.tris))
     cases.append((m.xyz, np.concatenate([m.tris, m.tris[:1]])))
+    cases.append((np.concatenate([m.xyz, [[9.0, 9.0, 9.0]]]), m.tris))     # node in no triangle
     cases.append((m.xyz, m.tris))
     for xyz, tris in cases:
         assert solver.host_validate(xyz, tris) == oracle.validate_mesh(xyz, tris)

@@ -175,6 +175,9 @@ def test_validate_mesh_errors():
     assert oracle.validate_mesh(x, m.tris)[0] == 3
     t = np.concatenate([m.tris, m.tris[:1]])
     assert oracle.validate_mesh(m.xyz, t)[0] == 4
+    # a node in no triangle (zero lumped mass)
+    x = np.concatenate([m.xyz, [[9.0, 9.0, 9.0]]])
+    assert oracle.validate_mesh(x, m.tris) == (5, m.n_nodes)
 
 
 # ---------------------------------------------------------------------------------
@@ -441,6 +444,58 @@ def test_sdof_damped_mode1():
     oracle.run_raw(row_ptr, col, Kval, c1, c2, c3, None, un, unm1, dt=dt, nsteps=5000,
                    F=np.full((1, 1, 3), f))
     assert un[0, 0, 0] == pytest.approx(f / k, rel=1e-12)
+
+
+def _damped_sdof_closed_form(m, k, f, c, dt, n):
+    """Exact solution of the damped central-difference recurrence of Eq. 22
+    for one DOF from rest (u_{-1} = u_0 = 0), in extended precision and from the physical
+    parameters only: D u_{n+1} = dt^2 f - (dt^2 k - 2m) u_n - (m - dt c/2) u_{n-1},
+    D = m + dt c/2.  Characteristic roots of D l^2 - (2m - dt^2 k) l + (m - dt c/2) = 0 are
+    r e^{+-i th} (underdamped), so u_n = u* + r^n (C1 cos n th + C2 sin n th) with
+    u* = f/k, C1 = -u*, C2 = u* (r - cos th) / sin th."""
+    L = np.longdouble
+    m, k, f, c, dt = L(m), L(k), L(f), L(c), L(dt)
+    D = m + dt * c / 2
+    q = m - dt * c / 2
+    b = 2 * m - dt * dt * k
+    assert b * b < 4 * D * q, "underdamped case only"
+    r = np.sqrt(q / D)
+    th = np.arccos(b / (2 * D * r))
+    us = f / k
+    C1, C2 = -us, us * (r - np.cos(th)) / np.sin(th)
+    idx = np.arange(1, n + 1).astype(L)
+    return us + r ** idx * (C1 * np.cos(idx * th) + C2 * np.sin(idx * th))
+
+
+@pytest.mark.parametrize("m", [0.5, 3.0])
+def test_sdof_damped_modes_trajectory(m):
+    """orc_coeffs' damping forms (DESIGN.md §2 #4): mode 1 C~ = c_d M~
+    (c = c_d m), mode 2 C~ = c_d I (c = c_d, the literal f_v = -c_d u').
+    The whole 10^4-step oracle trajectory of a damped SDOF with m != 1 (where the two modes
+    differ) must match the closed form of the damped recurrence in extended precision; a
+    swapped mode, a mis-scaled c or a wrong sign in c2/c3 fails it."""
+    k, f, cd = 40.0, 1.0, 0.8
+    dt = 0.5 * 2.0 / math.sqrt(k / m)
+    n = 10_000
+    row_ptr = np.array([0, 1]); col = np.array([0], np.int32)
+    Kval = np.diag([k] * 3).reshape(1, 1, 9)
+    traj = {}
+    for mode, c in ((1, cd * m), (2, cd)):
+        c1, c2, c3 = oracle.coeffs(np.array([[m]]), dt, mode, cd)
+        un = np.zeros((1, 1, 3)); unm1 = np.zeros((1, 1, 3))
+        out = np.empty(n)
+        for t in range(n):
+            oracle.run_raw(row_ptr, col, Kval, c1, c2, c3, None, un, unm1, dt=dt, nsteps=1,
+                           step0=t, F=np.full((1, 1, 3), f))
+            out[t] = un[0, 0, 0]
+        ref = _damped_sdof_closed_form(m, k, f, c, dt, n)
+        err = np.max(np.abs(out.astype(np.longdouble) - ref)) / np.max(np.abs(ref))
+        assert err <= 1e-12, (mode, float(err))
+        # the decay: the transient shrinks by r^n; after 10^4 steps only f/k is left
+        assert out[-1] == pytest.approx(f / k, rel=1e-9)
+        traj[mode] = out
+    # the two forms differ when m != 1 (they coincide at m = 1, the old pin's case)
+    assert np.max(np.abs(traj[1][:200] - traj[2][:200])) > 1e-3 * f / k
 
 
 def _crit_dt(om, s):
