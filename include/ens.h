@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define ENS_ABI_VERSION 1
+#define ENS_ABI_VERSION 2
 
 enum {
     ENS_OK = 0,
@@ -127,7 +127,23 @@ typedef struct {
                                with p2p_procs == 1 it holds part `rank` and must be connected to the
                                other ranks with ens_p2p_export / ens_p2p_connect before ens_step. */
     int32_t p2p_procs;      /* halo == P2P: 1 = one part per process (CUDA IPC), 0 = all parts here */
+    int32_t mf_variant;     /* kernel == MATRIX_FREE: the device data path of the same arithmetic
+                               (ENS_MF_*).  AUTO (0): STAGED where it applies (N_s % 64 == 0), else
+                               TILES.  Asking for a path that does not apply to the context
+                               (STAGED: N_s % 64 != 0; WARP: N_s % 64 != 0 or damping == IDENTITY)
+                               returns ENS_E_UNSUPPORTED.  Ignored by the assembled kernels. */
 } ens_options;
+
+/* Matrix-free data paths (ens_options.mf_variant, ens_info.mf_variant).  All three compute
+ * the same sums in the same order per row (bit-identical results):
+ *   TILES  (1)  k_step_matrix_free: CTA tiles of rows, K^ rows staged by TMA, u and alpha
+ *               gathered through L1 into registers; any N_s.
+ *   WARP   (2)  k_step_mf_warp: per-warp rings of per-operand TMA copies (item programs).
+ *   STAGED (3)  k_step_mf_staged: warp-specialised persistent CTAs; a producer warp stages
+ *               whole tiles (the u_n rows of the tile's node set, its alpha rows, records and
+ *               K^) by runs of consecutive ids into an mbarrier ring, consumer warps compute
+ *               from shared memory. */
+enum { ENS_MF_AUTO = 0, ENS_MF_TILES = 1, ENS_MF_WARP = 2, ENS_MF_STAGED = 3 };
 
 typedef struct ens_ctx ens_ctx;
 
@@ -147,11 +163,8 @@ typedef struct {
     int32_t graph_steps;                /* ens_step replays a CUDA graph of this many steps + 1 counter
                                            advance (env ENS_GRAPH_STEPS; 0 = direct launches) */
     int32_t halo;                       /* ens_options.halo (NODE contexts) */
-    int32_t mf_variant;                 /* MATRIX_FREE data path: 1 = per-warp TMA item streams
-                                           (k_step_mf_warp: N_s = 64 without identity damping;
-                                           env ENS_MF_WARP=1: any N_s % 64 == 0, =0: never),
-                                           0 = CTA tiles with register gathers
-                                           (k_step_matrix_free); 0 for assembled kernels */
+    int32_t mf_variant;                 /* MATRIX_FREE: the data path in use (ENS_MF_TILES / WARP /
+                                           STAGED); 0 for the assembled kernels */
 } ens_info;
 
 /* Create a context: validate the mesh, build the RCM-ordered block-CSR pattern, the

@@ -30,6 +30,15 @@ struct DevBuf {
     size_t bytes = 0;
 };
 
+// Matrix-free F3 tiles of one launched row range [row0, row0 + rows) (device.hpp MfTile).
+struct MfTileSet {
+    int64_t row0 = 0, rows = 0;
+    int32_t ntiles = 0, stage_bytes = 0;
+    ens::MfTile* d_tiles = nullptr;
+    int2* d_runs = nullptr;
+    unsigned char* d_blob = nullptr;
+};
+
 // One node partition held on this device: owned rows [lo, hi) of the RCM order, ghosts.
 struct Part {
     ens::PartPlan plan;
@@ -47,6 +56,7 @@ struct Part {
     int4* d_items = nullptr;
     double *d_Krow = nullptr, *d_alpha = nullptr;
     int32_t mf_rows = 1, mf_groups = 1, mf_smem_inc = 0;
+    std::vector<MfTileSet> mfs;                            // matrix-free F3 tiles, per launched row range
     int32_t *d_sym_lptr = nullptr, *d_sym_lidx = nullptr, *d_sym_lcol = nullptr, *d_sym_scol = nullptr;
     int2* d_sym_urange = nullptr;
     int64_t n_stored = 0;                                  // value blocks held (assembled kernels)
@@ -84,6 +94,7 @@ struct ens_ctx {
     int64_t V = 0, F = 0, nnzb = 0;
     int32_t n_s = 0, s_begin = 0;
     int32_t kernel = 0, damping = 0, dist = 0, rank = 0, world = 1;
+    int32_t mf_variant = 0;                 // matrix-free data path in use (ENS_MF_*), resolved at create
     double dt = 0.0, dt_cfl = 0.0, c_d = 0.0;
     double c2 = 2.0, c3 = 1.0;
     int32_t bandwidth = 0;
@@ -267,6 +278,7 @@ int check_opts(const ens_options* opt) {
         return fail(nullptr, ENS_E_UNSUPPORTED,
                     "reassemble_every needs an assembled kernel (per-realisation geometry breaks the shared K^_e)");
     if (opt->halo < 0 || opt->halo > 1) return fail(nullptr, ENS_E_ARG, "opt->halo must be 0 (NCCL) or 1 (P2P)");
+    if (opt->mf_variant < 0 || opt->mf_variant > 3) return fail(nullptr, ENS_E_ARG, "opt->mf_variant must be 0..3 (ENS_MF_*)");
     if (opt->p2p_procs && (opt->halo != ENS_HALO_P2P || opt->dist != ENS_DIST_NODE))
         return fail(nullptr, ENS_E_ARG, "opt->p2p_procs needs dist = NODE and halo = P2P");
     if (opt->halo == ENS_HALO_P2P && opt->nccl_comm)
@@ -360,10 +372,22 @@ ens::StepArgs part_args(const ens_ctx* c, const Part& p) {
     return a;
 }
 
-cudaError_t launch_rows(const ens_ctx* c, ens::StepArgs a, int64_t row0, int64_t rows, cudaStream_t st) {
+cudaError_t launch_rows(const ens_ctx* c, const Part& p, ens::StepArgs a, int64_t row0, int64_t rows, cudaStream_t st) {
     if (rows <= 0) return cudaSuccess;
     a.row0 = row0;
     a.V = rows;
+    if (c->kernel == ENS_KERNEL_MATRIX_FREE && c->mf_variant == ENS_MF_STAGED) {
+        // the tile set built for exactly this row range (build_part)
+        const MfTileSet* ts = nullptr;
+        for (const MfTileSet& t : p.mfs)
+            if (t.row0 == row0 && t.rows == rows) ts = &t;
+        if (!ts) return cudaErrorInvalidValue;
+        a.mfs_tiles = ts->d_tiles;
+        a.mfs_runs = ts->d_runs;
+        a.mfs_blob = ts->d_blob;
+        a.mfs_ntiles = ts->ntiles;
+        a.mfs_stage_bytes = ts->stage_bytes;
+    }
     switch (c->kernel) {
         case ENS_KERNEL_MATRIX_FREE: return ens::launch_step_matrix_free(a, st);
         case ENS_KERNEL_ASSEMBLED_SYM: return ens::launch_step_assembled_sym(a, st);
@@ -409,7 +433,7 @@ int launch_interior(ens_ctx* c, int64_t k, cudaStream_t st) {
     for (Part& p : c->parts) {
         ens::StepArgs a = part_args(c, p);
         a.step_off = k;
-        CUDA_TRY(c, launch_rows(c, a, p.plan.b_lo, p.n_own - p.plan.b_lo - p.plan.b_hi, st));
+        CUDA_TRY(c, launch_rows(c, p, a, p.plan.b_lo, p.n_own - p.plan.b_lo - p.plan.b_hi, st));
     }
     return ENS_OK;
 }
@@ -433,8 +457,8 @@ int enqueue_step_p2p(ens_ctx* c, int64_t k, cudaStream_t st) {
         a.fwd_ptr = p.d_fwd_ptr;
         a.fwd_dst = p.d_fwd_dst;
         a.peer_buf = p.d_peer_buf;
-        CUDA_TRY(c, launch_rows(c, a, 0, p.plan.b_lo, hs));
-        CUDA_TRY(c, launch_rows(c, a, p.n_own - p.plan.b_hi, p.plan.b_hi, hs));
+        CUDA_TRY(c, launch_rows(c, p, a, 0, p.plan.b_lo, hs));
+        CUDA_TRY(c, launch_rows(c, p, a, p.n_own - p.plan.b_hi, p.plan.b_hi, hs));
         CUDA_TRY(c, ens::launch_halo_signal(p.n_out, p.d_out_flag, c->d_step, k, hs));
     }
     RC_TRY(launch_interior(c, k, st));
@@ -448,7 +472,7 @@ int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
     if (!c->has_halo()) {
         ens::StepArgs a = part_args(c, c->parts[0]);
         a.step_off = k;
-        CUDA_TRY(c, launch_rows(c, a, 0, c->parts[0].n_own, st));
+        CUDA_TRY(c, launch_rows(c, c->parts[0], a, 0, c->parts[0].n_own, st));
         return ENS_OK;
     }
     cudaStream_t hs;
@@ -457,8 +481,8 @@ int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
     for (Part& p : c->parts) {
         ens::StepArgs a = part_args(c, p);
         a.step_off = k;
-        CUDA_TRY(c, launch_rows(c, a, 0, p.plan.b_lo, hs));
-        CUDA_TRY(c, launch_rows(c, a, p.n_own - p.plan.b_hi, p.plan.b_hi, hs));
+        CUDA_TRY(c, launch_rows(c, p, a, 0, p.plan.b_lo, hs));
+        CUDA_TRY(c, launch_rows(c, p, a, p.n_own - p.plan.b_hi, p.plan.b_hi, hs));
         CUDA_TRY(c, ens::launch_pack(int64_t(p.plan.send_rows.size()), c->n_s, p.d_send_rows, c->d_step, k, p.d_u0,
                                      p.d_u1, p.d_sendbuf, hs));
     }
@@ -532,6 +556,116 @@ struct Global {
     const std::vector<int32_t>* contrib;       // e * 9 + a * 3 + b
 };
 
+// Matrix-free F3 tiles of rows [row0, row0 + rows) (device.hpp MfTile, kernels.cu
+// k_step_mf_staged): greedily the longest run of at most kMfsMaxRows consecutive rows whose
+// stage image -- blob, u_n rows of the node set, alpha rows of the elements, F_k -- fits the
+// stage budget and moves in at most kMfsMaxRuns runs.
+int build_mf_tiles(ens_ctx* c, const std::vector<int32_t>& ip, const std::vector<ens::FanRec>& rec,
+                   const std::vector<double>& k18, int64_t row0, int64_t rows, MfTileSet& out) {
+    const ens::MfsShape sh = ens::mf_staged_shape();
+    const int64_t R = ens::kMfsMaxRows;
+    const size_t US = size_t(c->n_s) * 24, AS = size_t(c->n_s) * 8;
+    struct Lay {
+        std::vector<int32_t> nodes, elems;     // neighbour nodes outside the own rows; elements (sorted)
+        std::vector<int2> urun, erun;
+        size_t blob_bytes = 0, bytes = 0;
+    };
+    auto runs_of = [](const std::vector<int32_t>& v, std::vector<int2>& r) {
+        for (size_t k = 0; k < v.size(); ++k) {
+            if (!r.empty() && r.back().x + r.back().y == v[k]) ++r.back().y;
+            else r.push_back(make_int2(v[k], 1));
+        }
+    };
+    auto layout = [&](int64_t r0, int64_t n, Lay& L) {
+        L.nodes.clear();
+        L.elems.clear();
+        L.urun.clear();
+        L.erun.clear();
+        for (int32_t k = ip[size_t(r0)]; k < ip[size_t(r0 + n)]; ++k) {
+            for (int32_t q : {rec[size_t(k)].n_prev, rec[size_t(k)].n_next})
+                if (q < r0 || q >= r0 + n) L.nodes.push_back(q);
+            L.elems.push_back(rec[size_t(k)].e);
+        }
+        std::sort(L.nodes.begin(), L.nodes.end());
+        L.nodes.erase(std::unique(L.nodes.begin(), L.nodes.end()), L.nodes.end());
+        std::sort(L.elems.begin(), L.elems.end());
+        L.elems.erase(std::unique(L.elems.begin(), L.elems.end()), L.elems.end());
+        L.urun.push_back(make_int2(int32_t(r0), int32_t(n)));
+        runs_of(L.nodes, L.urun);
+        runs_of(L.elems, L.erun);
+        const size_t ninc = size_t(ip[size_t(r0 + n)] - ip[size_t(r0)]);
+        L.blob_bytes = (ens::kMfsHdrBytes + ninc * ens::kMfsRecBytes + size_t(n + 1) * 4 + 127) & ~size_t(127);
+        L.bytes = L.blob_bytes + size_t(n + int64_t(L.nodes.size())) * US + L.elems.size() * AS;   // + F_k
+    };
+    std::vector<ens::MfTile> tiles;
+    std::vector<int2> runs;
+    std::vector<unsigned char> blob;
+    Lay best, L;
+    for (int64_t r = row0; r < row0 + rows;) {
+        int64_t nb = 0;
+        for (int64_t n = 1; n <= R && r + n <= row0 + rows; ++n) {
+            layout(r, n, L);
+            if (L.bytes + size_t(ens::kMaxFields * n * 32) > size_t(sh.stage_bytes) ||
+                L.urun.size() + L.erun.size() > size_t(ens::kMfsMaxRuns))
+                break;
+            std::swap(best, L);
+            nb = n;
+        }
+        if (nb == 0)
+            return fail(c, ENS_E_UNSUPPORTED, "matrix-free staged: the operands of row " + std::to_string(r) +
+                                                  " exceed one shared-memory stage");
+        ens::MfTile t{};
+        t.run0 = int32_t(runs.size());
+        t.n_runs = int32_t(best.urun.size());
+        t.n_eruns = int32_t(best.erun.size());
+        runs.insert(runs.end(), best.urun.begin(), best.urun.end());
+        runs.insert(runs.end(), best.erun.begin(), best.erun.end());
+        t.blob = int64_t(blob.size());
+        t.blob_bytes = int32_t(best.blob_bytes);
+        t.u_base = int32_t(best.blob_bytes);
+        t.a_base = int32_t(best.blob_bytes + size_t(nb + int64_t(best.nodes.size())) * US);
+        t.f_base = int32_t(best.bytes);
+        t.stage_bytes = int32_t(best.bytes);
+        t.r0 = int32_t(r);
+        t.nrows = int32_t(nb);
+        tiles.push_back(t);
+        auto uslot = [&](int32_t q) -> uint32_t {
+            if (q >= r && q < r + nb) return uint32_t(q - r);
+            return uint32_t(nb + (std::lower_bound(best.nodes.begin(), best.nodes.end(), q) - best.nodes.begin()));
+        };
+        auto eslot = [&](int32_t e) {
+            return uint32_t(std::lower_bound(best.elems.begin(), best.elems.end(), e) - best.elems.begin());
+        };
+        const int32_t k0 = ip[size_t(r)], k1 = ip[size_t(r + nb)];
+        std::vector<unsigned char> b(best.blob_bytes, 0);
+        const int32_t rowoff = ens::kMfsHdrBytes + (k1 - k0) * ens::kMfsRecBytes;
+        const int32_t hdr[8] = {int32_t(r), int32_t(nb), t.u_base, rowoff, t.f_base, 0, 0, 0};
+        std::memcpy(b.data(), hdr, sizeof(hdr));
+        for (int32_t k = k0; k < k1; ++k) {
+            const ens::FanRec& fr = rec[size_t(k)];
+            const int32_t rc[4] = {int32_t(t.a_base + eslot(fr.e) * AS), int32_t(t.u_base + uslot(fr.n_next) * US),
+                                   int32_t(t.u_base + uslot(fr.n_prev) * US), fr.restart};
+            unsigned char* dst = b.data() + ens::kMfsHdrBytes + size_t(k - k0) * ens::kMfsRecBytes;
+            std::memcpy(dst, rc, 16);
+            std::memcpy(dst + 16, k18.data() + size_t(k) * 18, 18 * sizeof(double));
+        }
+        for (int64_t j = 0; j <= nb; ++j) {
+            const int32_t o = ip[size_t(r + j)] - k0;
+            std::memcpy(b.data() + rowoff + 4 * j, &o, 4);
+        }
+        blob.insert(blob.end(), b.begin(), b.end());
+        r += nb;
+    }
+    out.row0 = row0;
+    out.rows = rows;
+    out.ntiles = int32_t(tiles.size());
+    out.stage_bytes = sh.stage_bytes;
+    RC_TRY(upload(c, &out.d_tiles, tiles.data(), tiles.size()));
+    RC_TRY(upload(c, &out.d_runs, runs.data(), runs.size()));
+    RC_TRY(upload(c, &out.d_blob, blob.data(), blob.size()));
+    return ENS_OK;
+}
+
 int build_part(ens_ctx* c, Part& P, const Global& G) {
     const auto& pl = P.plan;
     const auto& pat = *G.pat;
@@ -602,8 +736,21 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
                 int32_t g = pat.iperm[size_t(G.m->tris[3 * e + a])];
                 if (g >= lo && g < hi) mark[size_t(e)] = 1;
             }
-        for (int64_t e = 0; e < G.m->F; ++e)
-            if (mark[size_t(e)]) elems.push_back(int32_t(e));
+        if (c->kernel == ENS_KERNEL_MATRIX_FREE) {
+            // matrix-free: elements numbered by first touch in row (fan) order, so that the
+            // elements of consecutive rows are mostly consecutive (F3 copies alpha by runs)
+            const ens::Fans& fans = *G.fans;
+            for (int32_t k = fans.ptr[size_t(lo)]; k < fans.ptr[size_t(hi)]; ++k) {
+                const int32_t e = fans.rec[size_t(k)].e;
+                if (mark[size_t(e)] == 1) {
+                    mark[size_t(e)] = 2;
+                    elems.push_back(e);
+                }
+            }
+        } else {
+            for (int64_t e = 0; e < G.m->F; ++e)
+                if (mark[size_t(e)]) elems.push_back(int32_t(e));
+        }
     }
     std::vector<int32_t> eloc(size_t(G.m->F), -1);
     for (size_t k = 0; k < elems.size(); ++k) eloc[size_t(elems[k])] = int32_t(k);
@@ -732,7 +879,7 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
             if (int64_t(mx) * ens::mf_inc_bytes() <= 96 * 1024 || P.mf_rows == 1) break;
             P.mf_rows = std::max(1, P.mf_rows / 2);
         }
-        if (int64_t(P.mf_smem_inc) * ens::mf_inc_bytes() > 200 * 1024)
+        if (c->mf_variant == ENS_MF_TILES && int64_t(P.mf_smem_inc) * ens::mf_inc_bytes() > 200 * 1024)
             return fail(c, ENS_E_UNSUPPORTED, "a node has too many incident elements for the matrix-free kernel");
         static_assert(sizeof(ens::FanRec) == sizeof(int4), "FanRec layout");
         RC_TRY(upload(c, &P.d_inc_ptr, ip.data(), ip.size()));
@@ -764,8 +911,16 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
                 items.push_back(make_int4(ii, ii, 0, ens::kItemOld | (int32_t(fx[size_t(i)]) << 8)));
             }
             iptr[size_t(P.n_own)] = int32_t(items.size());
-            RC_TRY(upload(c, &P.d_item_ptr, iptr.data(), iptr.size()));
-            RC_TRY(upload(c, &P.d_items, items.data(), items.size()));
+            if (c->mf_variant == ENS_MF_WARP) {
+                RC_TRY(upload(c, &P.d_item_ptr, iptr.data(), iptr.size()));
+                RC_TRY(upload(c, &P.d_items, items.data(), items.size()));
+            }
+            if (c->mf_variant == ENS_MF_STAGED)
+                for (const auto& tl : tilings) {
+                    if (tl.second <= tl.first) continue;
+                    P.mfs.emplace_back();
+                    RC_TRY(build_mf_tiles(c, ip, rec, k18, tl.first, tl.second - tl.first, P.mfs.back()));
+                }
         } else {
             RC_TRY(upload(c, &P.d_Krow, fans.Krow.data() + size_t(k0) * 28, size_t(k1 - k0) * 28));
         }
@@ -871,6 +1026,18 @@ int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, cons
     c->F = F;
     c->n_s = mat->n_s;
     c->s_begin = mat->s_begin;
+    if (c->kernel == ENS_KERNEL_MATRIX_FREE) {        // the data path (ens.h ENS_MF_*)
+        const int32_t req = opt ? opt->mf_variant : int32_t(ENS_MF_AUTO);
+        const bool diff = ens::mf_diff();
+        const bool staged_ok = diff && ens::mf_staged_applies(c->n_s);
+        const bool warp_ok = diff && c->n_s % 64 == 0 && c->damping != ENS_DAMP_IDENTITY;
+        if (req == ENS_MF_AUTO) c->mf_variant = staged_ok ? ENS_MF_STAGED : ENS_MF_TILES;
+        else if (req == ENS_MF_STAGED && !staged_ok)
+            return fail(c, ENS_E_UNSUPPORTED, "mf_variant STAGED needs n_s % 64 == 0 (and the DIFF form)");
+        else if (req == ENS_MF_WARP && !warp_ok)
+            return fail(c, ENS_E_UNSUPPORTED, "mf_variant WARP needs n_s % 64 == 0 and damping != IDENTITY");
+        else c->mf_variant = req;
+    }
 
     // S0: pattern (RCM + block CSR)
     ens::Pattern pat = ens::build_pattern(m);
@@ -1355,7 +1522,7 @@ int ens_apply_stiffness(ens_ctx* c, const double* u, double* y) {
         ens::StepArgs a = part_args(c, p);
         a.ubuf0 = a.ubuf1 = p.d_scratch_u;
         a.y_out = p.d_scratch_y;
-        CUDA_TRY(c, launch_rows(c, a, 0, p.n_own, c->stream));
+        CUDA_TRY(c, launch_rows(c, p, a, 0, p.n_own, c->stream));
         CUDA_TRY(c, ens::launch_dev_to_abi(p.n_own, c->n_s, p.d_map_abi, Vabi, p.d_scratch_y, c->d_stage, c->stream));
     }
     CUDA_TRY(c, cudaMemcpyAsync(y, c->d_stage, size_t(Vabi) * 3 * size_t(c->n_s) * sizeof(double),
@@ -1627,9 +1794,7 @@ int ens_query(const ens_ctx* c, ens_info* info) {
     info->graph_steps = c->use_graphs() ? c->graph_steps : 0;
     info->reassemble_every = c->reassemble_every;
     info->halo = c->halo;
-    // the launcher's choice (kernels.cu launch_step_matrix_free)
-    info->mf_variant = (c->kernel == ENS_KERNEL_MATRIX_FREE &&
-                        ens::mf_warp_for(c->n_s, ens::mf_diff(), c->damping != ENS_DAMP_IDENTITY)) ? 1 : 0;
+    info->mf_variant = c->kernel == ENS_KERNEL_MATRIX_FREE ? c->mf_variant : 0;
     // algorithmic HBM bytes of the rows this context advances: values +
     // u_n, u_{n-1} read, u_{n+1} written, c1 (+ c2, c3) per node per realisation
     const int64_t ns = c->n_s, per_node = 3 * 8 * 3 + 8 + (c->damping == ENS_DAMP_IDENTITY ? 16 : 0);

@@ -15,6 +15,30 @@ constexpr int kMaxFields = 4;
 // kinds of the matrix-free item programs (StepArgs::items, kernels.cu F2w)
 constexpr int kItemOwn = 0, kItemPrev = 1, kItemInc = 2, kItemOld = 3, kItemLastApply = 32;
 
+// Matrix-free F3 (kernels.cu k_step_mf_staged): one tile = up to kMfsMaxRows consecutive
+// rows whose operands fit one shared-memory stage, laid out [blob | u_n | alpha | F_k]:
+//   blob  = header int32[8] {r0, nrows, u-image offset, row-offset offset, F_k offset, 0, 0, 0}
+//           (byte offsets within the stage), then per incidence a 160-B record (int4 {alpha
+//           byte offset, next-node byte offset, prev-node byte offset, restart} + the 18 K^
+//           coefficients of the (prev, next) columns), then int32 row offsets [nrows + 1]
+//           into the records; padded to 128 B
+//   u_n   = the tile's node set, own rows first, each row [3][n_s] (n_s * 24 B)
+//   alpha = the tile's elements, each row [n_s] (n_s * 8 B)
+//   F_k   = the own rows' load fields, [n_fields][nrows][4] (32 B rows; n_fields is known
+//           only at ens_set_traction, the host budgets kMaxFields)
+// The node and element sets move as runs of consecutive ids (one bulk copy per run).
+constexpr int kMfsHdrBytes = 32;
+constexpr int kMfsRecBytes = 160;
+constexpr int kMfsMaxRuns = 30;          // u runs + alpha runs per tile (lanes 0..29 of the producer)
+constexpr int kMfsMaxRows = 16;
+struct MfTile {
+    int32_t run0, n_runs, n_eruns, blob_bytes;   // runs[run0, run0 + n_runs) u runs, then n_eruns alpha runs
+    int64_t blob;                                 // byte offset of the tile's blob in mfs_blob
+    int32_t u_base, a_base, f_base;               // stage byte offsets of the u, alpha and F_k images
+    int32_t stage_bytes;                          // bytes of blob + u + alpha (+ F_k: n_fields * nrows * 32)
+    int32_t r0, nrows, pad0, pad1;
+};
+
 struct StepArgs {
     int64_t V = 0;            // rows handled by this launch: rows [row0, row0 + V)
     int64_t row0 = 0;
@@ -41,6 +65,13 @@ struct StepArgs {
     // matrix-free item programs (kernels.cu F2w; built by capi.cpp when DIFF is on)
     const int32_t* item_ptr = nullptr;  // [rows + 1]
     const int4* items = nullptr;        // {node, elem | row, K^ row, kind | flags}
+    // matrix-free tile stages (kernels.cu F3) of the launched row range
+    const MfTile* mfs_tiles = nullptr;
+    const int2* mfs_runs = nullptr;     // {first id, count}
+    const unsigned char* mfs_blob = nullptr;
+    int32_t mfs_ntiles = 0;
+    int32_t mfs_stage_bytes = 0;        // bytes per stage (shared memory = stages * this + barriers)
+    int32_t mfs_prefetch = 0;           // 1: the producer warms L2 with the next tile's runs (launcher)
     // update coefficients
     const double* c1 = nullptr;
     const double* c2a = nullptr;        // null => scalars c2, c3
@@ -93,7 +124,11 @@ cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st);
 // realisations per thread of the step kernels for a given N_s (4, 2 or 1)
 int pick_vec(int32_t n_s);      // assembled kernel
 int pick_vec_mf(int32_t n_s);   // matrix-free kernel
-bool mf_warp_for(int32_t n_s, bool have_items, bool scalar_c23);   // matrix-free: F2w (per-warp TMA item streams) or F2
+// matrix-free F3 (tile stages): applies to N_s % 64 == 0 with N_s / 64 <= consumer warps
+bool mf_staged_applies(int32_t n_s);
+// F3 launch shape: consumer warps, stages, and the stage byte budget of one tile
+struct MfsShape { int consumers, stages, stage_bytes; };
+MfsShape mf_staged_shape();
 bool mf_diff();            // matrix-free: neighbours relative to u_i, (prev, next) K^ columns only (ENS_MF_DIFF, default 1)
 int mf_inc_bytes();        // matrix-free: shared-memory bytes per incidence (K^ image + fan record)
 // coef_buf[(step & 1)] = the load coefficients of step *step_base (after host changes)

@@ -212,7 +212,9 @@ __device__ __forceinline__ void upd_load(const StepArgs& a, const StepCtx& sc, c
         if (load_un) u.un[c] = ld_ro<VEC>(sc.un + off);
         u.uo[c] = ld_rw<VEC>(sc.uo + off);
         double f = 0.0;
-        for (int k = 0; k < a.n_fields; ++k) f = fma(coef[k], __ldg(a.Fk + (int64_t(k) * a.fk_rows + i) * 4 + c), f);
+#pragma unroll
+        for (int k = 0; k < kMaxFields; ++k)
+            if (k < a.n_fields) f = fma(coef[k], __ldg(a.Fk + (int64_t(k) * a.fk_rows + i) * 4 + c), f);
         u.f[c] = f;
     }
 }
@@ -601,23 +603,17 @@ __device__ __forceinline__ void mf_tile_rows(const StepArgs& a, const StepCtx& s
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 if constexpr (DIFF) {        // prev / next already relative to u_i
-                    double tp[VEC], tn[VEC];
+                    // one chain per (c, v): prev_0..2 then next_0..2 (the order of F3)
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) {
-                        tp[v] = K[6 * c] * prev[0].v[v];
-                        tn[v] = K[6 * c + 3] * next[0].v[v];
+                        double t = K[6 * c] * prev[0].v[v];
+                        t = fma(K[6 * c + 1], prev[1].v[v], t);
+                        t = fma(K[6 * c + 2], prev[2].v[v], t);
+                        t = fma(K[6 * c + 3], next[0].v[v], t);
+                        t = fma(K[6 * c + 4], next[1].v[v], t);
+                        t = fma(K[6 * c + 5], next[2].v[v], t);
+                        y[c][v] = fma(alj.v[v], t, y[c][v]);
                     }
-#pragma unroll
-                    for (int d = 1; d < 3; ++d) {
-                        const double k_prev = K[6 * c + d], k_next = K[6 * c + 3 + d];
-#pragma unroll
-                        for (int v = 0; v < VEC; ++v) {
-                            tp[v] = fma(k_prev, prev[d].v[v], tp[v]);
-                            tn[v] = fma(k_next, next[d].v[v], tn[v]);
-                        }
-                    }
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) y[c][v] = fma(alj.v[v], tp[v] + tn[v], y[c][v]);
                 } else {
                     // three independent 3-term chains (own, prev, next), then their sum: short
                     // dependency chains for the FP64 pipe
@@ -875,23 +871,16 @@ k_step_mf_warp(const StepArgs a, const __grid_constant__ MfwMaps maps) {
                 const double alv[2] = {xa.x, xa.y};
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    double tp[2], tn[2];
 #pragma unroll
-                    for (int v = 0; v < 2; ++v) {
-                        tp[v] = K[6 * c] * up[0].v[v];
-                        tn[v] = K[6 * c + 3] * ux[0].v[v];
+                    for (int v = 0; v < 2; ++v) {       // one chain: prev_0..2, next_0..2 (F2, F3)
+                        double t = K[6 * c] * up[0].v[v];
+                        t = fma(K[6 * c + 1], up[1].v[v], t);
+                        t = fma(K[6 * c + 2], up[2].v[v], t);
+                        t = fma(K[6 * c + 3], ux[0].v[v], t);
+                        t = fma(K[6 * c + 4], ux[1].v[v], t);
+                        t = fma(K[6 * c + 5], ux[2].v[v], t);
+                        y[c][v] = fma(alv[v], t, y[c][v]);
                     }
-#pragma unroll
-                    for (int d = 1; d < 3; ++d) {
-                        const double k_prev = K[6 * c + d], k_next = K[6 * c + 3 + d];
-#pragma unroll
-                        for (int v = 0; v < 2; ++v) {
-                            tp[v] = fma(k_prev, up[d].v[v], tp[v]);
-                            tn[v] = fma(k_next, ux[d].v[v], tn[v]);
-                        }
-                    }
-#pragma unroll
-                    for (int v = 0; v < 2; ++v) y[c][v] = fma(alv[v], tp[v] + tn[v], y[c][v]);
                 }
 #pragma unroll
                 for (int d = 0; d < 3; ++d) up[d] = ux[d];
@@ -937,6 +926,251 @@ k_step_mf_warp(const StepArgs a, const __grid_constant__ MfwMaps maps) {
         }
         __syncwarp();                                    // group n's slots are free for group n + 2
     }
+}
+
+// ---- F3: the matrix-free step as warp-specialised tile stages -----------------------------
+// Same arithmetic as F2 (DIFF form, same order per row: bit-identical), different data
+// movement.  A persistent CTA per SM walks a contiguous range of host-built tiles (device.hpp
+// MfTile: up to R consecutive rows whose operands fit one stage).  One PRODUCER warp fills an
+// S-stage ring: per tile one 1-D bulk copy (cp.async.bulk, the TMA engine) per run of
+// consecutive u_n rows (own rows, then the neighbours), per run of alpha rows, and one for
+// the tile's blob (incidence records, K^ coefficients, row offsets), all completing on the
+// stage's FULL mbarrier; the lanes of the warp issue one run each.  CW CONSUMER warps
+// (N_s / 64 per row, lanes = realisation pairs) wait on FULL, gather every operand of their
+// row from shared memory, finish the update with u_{n-1}, c1 and F_k loaded from global
+// memory before the gather (their latency hides behind it), store u_{n+1}, and arrive on the
+// stage's EMPTY mbarrier, which the producer waits for before refilling the stage.  No
+// consumer waits for another: a warp moves to the next stage as soon as it has landed.
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
+
+// NS: N_s at compile time (64) or 0 (runtime); C23: per-row c2, c3 arrays (identity damping)
+template <bool APPLY, int CW, int S, int NS, bool C23>
+__global__ void __launch_bounds__((CW + 1) * 32, 1)
+k_step_mf_staged(const StepArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t SB = uint32_t(a.mfs_stage_bytes);
+    const uint32_t smem_s = uint32_t(__cvta_generic_to_shared(smem));
+    const uint32_t bar0 = smem_s + uint32_t(S) * SB;          // full[S], then empty[S]
+    const int wid = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            mbar_init(bar0 + 8u * s, 1);
+            mbar_init(bar0 + 8u * (S + s), CW);
+        }
+    }
+    __syncthreads();
+    const StepCtx sc = step_ctx(a);
+    const int n_s = NS ? NS : a.n_s;
+    const int32_t nt = a.mfs_ntiles;
+    const int32_t ta = int32_t(int64_t(nt) * blockIdx.x / gridDim.x);
+    const int32_t tb = int32_t(int64_t(nt) * (blockIdx.x + 1) / gridDim.x);
+    const uint32_t US = uint32_t(n_s) * 24u, AS = uint32_t(n_s) * 8u;
+
+    if (wid == CW) {                                          // ---- producer warp
+        // Descriptors are software-pipelined: the tile two ahead and the runs of the next
+        // one are loaded while this one is issued, so no global load latency sits between
+        // a stage becoming free and its refill.
+        const int nf = APPLY ? 0 : a.n_fields;
+        MfTile d1{}, d2{};
+        int2 run1 = make_int2(0, 0);
+        auto load_runs = [&](const MfTile& q) {
+            int2 r = make_int2(0, 0);
+            if (lane < q.n_runs + q.n_eruns) r = __ldg(a.mfs_runs + q.run0 + lane);
+            return r;
+        };
+        if (ta < tb) d1 = a.mfs_tiles[ta];
+        if (ta + 1 < tb) d2 = a.mfs_tiles[ta + 1];
+        if (ta < tb) run1 = load_runs(d1);
+        for (int32_t t = ta; t < tb; ++t) {
+            const int it = int(t - ta), s = it % S;
+            const uint32_t full = bar0 + 8u * s, stage = smem_s + uint32_t(s) * SB;
+            const MfTile d = d1;
+            const int2 run = run1;
+            d1 = d2;
+            if (t + 2 < tb) d2 = a.mfs_tiles[t + 2];
+            if (t + 1 < tb) run1 = load_runs(d1);
+            const int nr = d.n_runs + d.n_eruns;
+            // stage slot of each run: exclusive prefix of the counts within the u runs and
+            // within the alpha runs
+            const bool is_u = lane < d.n_runs;
+            int x = lane < nr ? run.y : 0;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, off);
+                if (lane >= off && ((lane - off < d.n_runs) == is_u)) x += y;
+            }
+            const uint32_t slot = uint32_t(x - (lane < nr ? run.y : 0));
+            if (it >= S) mbar_wait(bar0 + 8u * (S + s), uint32_t(it / S - 1) & 1u);
+            if (lane == 0) mbar_expect_tx(full, uint32_t(d.stage_bytes) + uint32_t(nf * d.nrows) * 32u);
+            __syncwarp();
+            if (is_u) {
+                tma_bulk_g2s(stage + uint32_t(d.u_base) + slot * US, sc.un + int64_t(run.x) * 3 * n_s,
+                             uint32_t(run.y) * US, full);
+            } else if (lane < nr) {
+                tma_bulk_g2s(stage + uint32_t(d.a_base) + slot * AS, a.alpha + int64_t(run.x) * n_s,
+                             uint32_t(run.y) * AS, full);
+            } else if (lane == 30) {
+                for (int k = 0; k < nf; ++k)
+                    tma_bulk_g2s(stage + uint32_t(d.f_base) + uint32_t(k * d.nrows) * 32u,
+                                 a.Fk + (int64_t(k) * a.fk_rows + d.r0) * 4, uint32_t(d.nrows) * 32u, full);
+            } else if (lane == 31) {
+                tma_bulk_g2s(stage, a.mfs_blob + d.blob, uint32_t(d.blob_bytes), full);
+            }
+            // warm L2 with the u_n and alpha runs of the next tile (its descriptors are in
+            // registers already): its stage fill then hits L2 (ENS_MFS_PF=1, measured)
+            if (a.mfs_prefetch && t + 1 < tb && lane < d1.n_runs + d1.n_eruns) {
+                const bool u = lane < d1.n_runs;
+                const void* src = u ? static_cast<const void*>(sc.un + int64_t(run1.x) * 3 * n_s)
+                                    : static_cast<const void*>(a.alpha + int64_t(run1.x) * n_s);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                             :: "l"(src), "r"(uint32_t(run1.y) * (u ? US : AS)) : "memory");
+            }
+        }
+        return;
+    }
+
+    // ---- consumer warps.  Units = (row, 64-realisation slice) pairs, H = N_s / 64 per row,
+    // numbered consecutively over this CTA's tiles; warp wid takes units wid, wid + CW, ...
+    const int H = n_s >> 6;
+    const int dwr = CW / H, dh = CW - dwr * H;                // unit step CW = dwr rows + dh slices
+    auto ld2 = [&](const unsigned char* p) {
+        const double2 v = *reinterpret_cast<const double2*>(p);
+        Vec<2> r;
+        r.v[0] = v.x; r.v[1] = v.y;
+        return r;
+    };
+    // one incidence: y[c] += alpha * (K^[c, prev] . prev + K^[c, next] . next), prev / next
+    // relative to u_i, one chain per (c, v) in the order prev_0..2, next_0..2
+    auto incidence = [&](double (&y)[3][2], const Vec<2> (&pv)[3], const Vec<2> (&nx)[3], const Vec<2>& al,
+                         const unsigned char* rp) {
+        const double2* K2 = reinterpret_cast<const double2*>(rp + 16);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            // K[6c .. 6c + 5] = (prev_0, prev_1, prev_2, next_0, next_1, next_2): 16-B aligned pairs
+            const double2 k01 = K2[3 * c], k23 = K2[3 * c + 1], k45 = K2[3 * c + 2];
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                double t = k01.x * pv[0].v[v];
+                t = fma(k01.y, pv[1].v[v], t);
+                t = fma(k23.x, pv[2].v[v], t);
+                t = fma(k23.y, nx[0].v[v], t);
+                t = fma(k45.x, nx[1].v[v], t);
+                t = fma(k45.y, nx[2].v[v], t);
+                y[c][v] = fma(al.v[v], t, y[c][v]);
+            }
+        }
+    };
+    __shared__ double s_coef[kMaxFields];
+    if (!APPLY && wid == 0 && lane < kMaxFields)
+        s_coef[lane] = lane < a.n_fields ? a.coef_buf[(sc.step & 1) * kMaxFields + lane] : 0.0;
+    asm volatile("bar.sync 1, %0;" :: "r"(CW * 32) : "memory");   // consumers only
+    int32_t ubase = 0;                                        // units of the tiles before this one
+    for (int32_t t = ta; t < tb; ++t) {
+        const int it = int(t - ta), s = it % S;
+        const unsigned char* st = smem + size_t(s) * SB;
+        mbar_wait(bar0 + 8u * s, uint32_t(it / S) & 1u);
+        const int4 hdr = *reinterpret_cast<const int4*>(st);  // {r0, nrows, u image, row offsets}
+        const int32_t f_base = *reinterpret_cast<const int32_t*>(st + 16);
+        const int32_t nunits = hdr.y * H;
+        int32_t uu = wid - ubase % CW;
+        if (uu < 0) uu += CW;
+        int wr = uu, h = 0;                                   // uu = wr * H + h
+        if (H > 1) { wr = uu / H; h = uu - wr * H; }
+        for (; uu < nunits; uu += CW) {
+            const int64_t i = hdr.x + wr;
+            const int s0 = h * 64 + 2 * lane;                 // this lane's realisations s0, s0 + 1
+            const uint32_t lofs = uint32_t(s0) * 8u;
+            const int32_t* roff = reinterpret_cast<const int32_t*>(st + hdr.w);
+            const int32_t kb = roff[wr], ke = roff[wr + 1];
+            const unsigned char* rec0 = st + kMfsHdrBytes;
+            // update operands from global memory first: their latency hides behind the gather
+            Vec<2> c1v, c2v, c3v, uold[3];
+            uint8_t fx = 0;
+            if (!APPLY) {
+                const int64_t ic = i * n_s + s0;
+                c1v = ld_ro<2>(a.c1 + ic);
+                if constexpr (C23) {
+                    c2v = ld_ro<2>(a.c2a + ic);
+                    c3v = ld_ro<2>(a.c3a + ic);
+                }
+                const double* po = sc.uo + 3 * ic - 2 * s0;   // (i * 3 + d) * n_s + s0
+#pragma unroll
+                for (int d = 0; d < 3; ++d) uold[d] = ld_rw<2>(po + d * n_s);
+                fx = a.fixed ? __ldg(a.fixed + i) : uint8_t(0);
+            }
+            const unsigned char* own = st + hdr.z + size_t(wr) * US + lofs;   // own row = slot wr
+            Vec<2> uo[3], pa[3], pb[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) uo[d] = ld2(own + d * AS);
+            auto rel = [&](Vec<2> (&w)[3], int32_t off) {    // w = u[node at off] - u_i
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    w[d] = ld2(st + off + lofs + d * AS);
+                    w[d].v[0] -= uo[d].v[0];
+                    w[d].v[1] -= uo[d].v[1];
+                }
+            };
+            double y[3][2];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) y[c][0] = y[c][1] = 0.0;
+            int32_t k = kb;
+            if (k < ke) rel(pa, reinterpret_cast<const int4*>(rec0 + size_t(k) * kMfsRecBytes)->z);
+            // pairs of incidences: the first takes prev = pa, next = pb, the second prev = pb,
+            // next = pa (the carried neighbour never moves between registers)
+            for (; k + 1 < ke; k += 2) {
+                const unsigned char* rp = rec0 + size_t(k) * kMfsRecBytes;
+                const int4 r = *reinterpret_cast<const int4*>(rp);
+                const int4 r2 = *reinterpret_cast<const int4*>(rp + kMfsRecBytes);
+                if (r.w && k != kb) rel(pa, r.z);           // a further chain starts (rare)
+                rel(pb, r.y);
+                incidence(y, pa, pb, ld2(st + r.x + lofs), rp);
+                if (r2.w) rel(pb, r2.z);
+                rel(pa, r2.y);
+                incidence(y, pb, pa, ld2(st + r2.x + lofs), rp + kMfsRecBytes);
+            }
+            if (k < ke) {
+                const unsigned char* rp = rec0 + size_t(k) * kMfsRecBytes;
+                const int4 r = *reinterpret_cast<const int4*>(rp);
+                if (r.w && k != kb) rel(pa, r.z);
+                rel(pb, r.y);
+                incidence(y, pa, pb, ld2(st + r.x + lofs), rp);
+            }
+            if constexpr (APPLY) {
+                store_y<2>(a, i, s0, y);
+            } else {
+                Upd<2> upd;
+                upd.fx = fx;
+                upd.c1 = c1v;
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    upd.c2.v[v] = C23 ? c2v.v[v] : a.c2;
+                    upd.c3.v[v] = C23 ? c3v.v[v] : a.c3;
+                }
+                const double* fk = reinterpret_cast<const double*>(st + f_base) + wr * 4;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    upd.un[d] = uo[d];
+                    upd.uo[d] = uold[d];
+                    double f = 0.0;
+#pragma unroll
+                    for (int q = 0; q < kMaxFields; ++q)
+                        if (q < a.n_fields) f = fma(s_coef[q], fk[q * hdr.y * 4 + d], f);
+                    upd.f[d] = f;
+                }
+                upd_store<2>(a, sc, i, s0, y, upd);
+            }
+            wr += dwr;
+            h += dh;
+            if (h >= H) { h -= H; ++wr; }
+        }
+        ubase += nunits;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar0 + 8u * (S + s));
+    }
+    if (!APPLY) step_coef(a, sc);      // block 0 thread 0: the next step's load coefficients
 }
 
 __global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
@@ -1188,19 +1422,6 @@ bool mf_diff() {
 }
 int mf_inc_bytes() { return int(mf_diff() ? MfLayout<true>::inc : MfLayout<false>::inc); }
 
-// F2w or F2: F2w needs the DIFF item programs, scalar c2/c3 and N_s % 64 == 0.
-// By default it runs at N_s = 64 only: with 128 or more realisations per row F2's CTA tiles
-// are as fast, and F2w's higher issue rate drew the power cap on the boxes measured (c4, c5).
-// ENS_MF_WARP=1 takes F2w wherever it applies, ENS_MF_WARP=0 never.
-bool mf_warp_for(int32_t n_s, bool have_items, bool scalar_c23) {
-    static const int mode = [] {
-        const char* e = std::getenv("ENS_MF_WARP");
-        return e ? std::atoi(e) : -1;
-    }();
-    if (mode == 0 || !have_items || !scalar_c23 || n_s % kMfwSlice != 0) return false;
-    return mode > 0 || n_s == kMfwSlice;
-}
-
 // Tensor map of one state buffer [rows * 3][n_s] fp64 with a [3][64] box, encoded once per
 // (buffer, rows, n_s) through the driver entry point (no -lcuda) and cached.
 static cudaError_t mfw_u_map(const double* base, int64_t rows, int n_s, CUtensorMap* out) {
@@ -1279,10 +1500,80 @@ static cudaError_t launch_mf_warp(const StepArgs& a, cudaStream_t st) {
     return launch_mf_warp_t<APPLY, 16, 3>(a, st);
 }
 
+// F3 shapes: consumer warps x stages (+ the producer warp; register allocation rounds a CTA
+// to multiples of 4 warps, so 11 + 1 warps leave 168 registers per thread, 15 + 1 only 128).
+// ENS_MFS_SHAPE = "CWxS" picks one of the built ones.
+struct MfsShapeDef { const char* name; int cw, s; };
+static constexpr MfsShapeDef kMfsShapes[] = {{"11x3", 11, 3}, {"11x2", 11, 2}, {"11x4", 11, 4}};
+static int mfs_shape_id() {
+    static const int id = [] {
+        const char* e = std::getenv("ENS_MFS_SHAPE");
+        if (e)
+            for (int k = 0; k < int(sizeof(kMfsShapes) / sizeof(kMfsShapes[0])); ++k)
+                if (!std::strcmp(e, kMfsShapes[k].name)) return k;
+        return 0;
+    }();
+    return id;
+}
+
+static constexpr int kMfsSmemMax = 227 * 1024;
+
+MfsShape mf_staged_shape() {
+    const MfsShapeDef& d = kMfsShapes[mfs_shape_id()];
+    const int sb = ((kMfsSmemMax - 2 * d.s * 8 - 256) / d.s) & ~127;     // 256 B: static shared (s_coef)
+    return {d.cw, d.s, sb};
+}
+
+bool mf_staged_applies(int32_t n_s) { return n_s % 64 == 0; }
+
+template <bool APPLY, int CW, int S, int NS, bool C23>
+static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
+    if (a.mfs_ntiles == 0) return cudaSuccess;
+    const size_t smem = size_t(S) * size_t(a.mfs_stage_bytes) + size_t(2 * S) * 8;
+    static std::atomic<uint64_t> attr_set{0};
+    static int sms[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (!(attr_set.load(std::memory_order_acquire) & bit)) {
+        cudaError_t e = cudaFuncSetAttribute(k_step_mf_staged<APPLY, CW, S, NS, C23>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMfsSmemMax - 256);
+        if (e != cudaSuccess) return e;
+        cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+        attr_set.fetch_or(bit, std::memory_order_release);
+    }
+    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(sms[dev & 63], a.mfs_ntiles)));
+    static const int pf = [] {          // L2 prefetch of the next tile's runs (0 = off)
+        const char* e = std::getenv("ENS_MFS_PF");
+        return e ? std::atoi(e) : 0;
+    }();
+    StepArgs b = a;
+    b.mfs_prefetch = pf;
+    k_step_mf_staged<APPLY, CW, S, NS, C23><<<grid, (CW + 1) * 32, smem, st>>>(b);
+    return cudaGetLastError();
+}
+
+// the hot instance (N_s = 64, scalar c2 / c3) gets N_s at compile time; the others run generic
+template <int CW, int S>
+static cudaError_t launch_mf_staged_shape(const StepArgs& a, cudaStream_t st) {
+    if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false>(a, st);
+    if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true>(a, st);
+    if (a.n_s == 64) return launch_mf_staged_t<false, CW, S, 64, false>(a, st);
+    return launch_mf_staged_t<false, CW, S, 0, false>(a, st);
+}
+
+static cudaError_t launch_mf_staged(const StepArgs& a, cudaStream_t st) {
+    switch (mfs_shape_id()) {
+        case 1: return launch_mf_staged_shape<11, 2>(a, st);
+        case 2: return launch_mf_staged_shape<11, 4>(a, st);
+        default: return launch_mf_staged_shape<11, 3>(a, st);
+    }
+}
+
 cudaError_t launch_step_matrix_free(const StepArgs& a, cudaStream_t st) {
     const bool ap = a.y_out != nullptr;
-    if (mf_warp_for(a.n_s, a.items != nullptr, a.c2a == nullptr))
-        return ap ? launch_mf_warp<true>(a, st) : launch_mf_warp<false>(a, st);
+    if (a.mfs_tiles) return launch_mf_staged(a, st);
+    if (a.items) return ap ? launch_mf_warp<true>(a, st) : launch_mf_warp<false>(a, st);
     if (pick_vec_mf(a.n_s) == 2) return ap ? launch_a2<2, true, 2, 2>(a, st) : launch_a2<2, false, 2, 2>(a, st);
     return ap ? launch_a2<1, true, 2, 3>(a, st) : launch_a2<1, false, 2, 3>(a, st);
 }

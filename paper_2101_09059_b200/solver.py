@@ -17,6 +17,9 @@ DAMPING = {"none": 0, "mass": 1, "identity": 2, 0: 0, 1: 1, 2: 2}
 KERNEL = {"assembled": 0, "matrix_free": 1, "assembled_sym": 2, 0: 0, 1: 1, 2: 2}
 DIST = {"single": 0, "node": 1, "ensemble": 2, 0: 0, 1: 1, 2: 2}
 HALO = {"nccl": 0, "p2p": 1, 0: 0, 1: 1}
+# matrix-free data paths (ens.h ENS_MF_*): same arithmetic, different data movement
+MF_VARIANT = {"auto": 0, "tiles": 1, "warp": 2, "staged": 3, 0: 0, 1: 1, 2: 2, 3: 3}
+MF_KERNEL_FN = {1: "k_step_matrix_free", 2: "k_step_mf_warp", 3: "k_step_mf_staged"}
 
 
 def _c(a, dtype):
@@ -61,12 +64,13 @@ class Ensemble:
                  cfl_safety=0.9, c_d=0.0, damping="none", kernel="assembled", dist="single",
                  s_begin=0, rank=0, world=1, nccl_comm=None, device=None, stream=None,
                  torch_alloc=True, reassemble_every=0, halo="nccl", p2p_procs=False, group=None,
-                 _ctx=None):
+                 mf_variant="auto", _ctx=None):
         """dist="node" splits the RCM rows into `world` parts.  halo="nccl": NCCL
         send/recv with nccl_comm (one part per process) or, without it, device copies
         between all parts held here.  halo="p2p": device-initiated stores into the
         neighbours' ghost rows; p2p_procs=True => one part per process, connected to the
-        other ranks of `group` (torch.distributed, default group) through CUDA IPC."""
+        other ranks of `group` (torch.distributed, default group) through CUDA IPC.
+        mf_variant ("auto", "tiles", "warp", "staged"): the matrix-free data path (ens.h)."""
         self._ctx = None
         self._alloc = None
         self._p2p_group, self._p2p_multi = None, False
@@ -86,6 +90,7 @@ class Ensemble:
         opt.reassemble_every = int(reassemble_every)
         opt.halo = HALO[halo]
         opt.p2p_procs = int(bool(p2p_procs))
+        opt.mf_variant = MF_VARIANT[mf_variant]
         ctx = C.c_void_p()
         check(lib().ens_create(C.byref(mesh), C.byref(mat), C.byref(opt), C.byref(ctx)))
         self._ctx = ctx
