@@ -561,7 +561,8 @@ struct Global {
 // stage image -- blob, u_n rows of the node set, alpha rows of the elements, F_k -- fits the
 // stage budget and moves in at most kMfsMaxRuns runs.
 int build_mf_tiles(ens_ctx* c, const std::vector<int32_t>& ip, const std::vector<ens::FanRec>& rec,
-                   const std::vector<double>& k18, int64_t row0, int64_t rows, MfTileSet& out) {
+                   const std::vector<double>& k18, const std::vector<uint8_t>& fx, int64_t row0, int64_t rows,
+                   MfTileSet& out) {
     const ens::MfsShape sh = ens::mf_staged_shape();
     const int64_t R = ens::kMfsMaxRows;
     const size_t US = size_t(c->n_s) * 24, AS = size_t(c->n_s) * 8;
@@ -650,7 +651,7 @@ int build_mf_tiles(ens_ctx* c, const std::vector<int32_t>& ip, const std::vector
             std::memcpy(dst + 16, k18.data() + size_t(k) * 18, 18 * sizeof(double));
         }
         for (int64_t j = 0; j <= nb; ++j) {
-            const int32_t o = ip[size_t(r + j)] - k0;
+            const int32_t o = (ip[size_t(r + j)] - k0) | (j < nb ? int32_t(fx[size_t(r + j)]) << 24 : 0);
             std::memcpy(b.data() + rowoff + 4 * j, &o, 4);
         }
         blob.insert(blob.end(), b.begin(), b.end());
@@ -919,7 +920,7 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
                 for (const auto& tl : tilings) {
                     if (tl.second <= tl.first) continue;
                     P.mfs.emplace_back();
-                    RC_TRY(build_mf_tiles(c, ip, rec, k18, tl.first, tl.second - tl.first, P.mfs.back()));
+                    RC_TRY(build_mf_tiles(c, ip, rec, k18, fx, tl.first, tl.second - tl.first, P.mfs.back()));
                 }
         } else {
             RC_TRY(upload(c, &P.d_Krow, fans.Krow.data() + size_t(k0) * 28, size_t(k1 - k0) * 28));

@@ -21,7 +21,7 @@ constexpr int kItemOwn = 0, kItemPrev = 1, kItemInc = 2, kItemOld = 3, kItemLast
 //           (byte offsets within the stage), then per incidence a 160-B record (int4 {alpha
 //           byte offset, next-node byte offset, prev-node byte offset, restart} + the 18 K^
 //           coefficients of the (prev, next) columns), then int32 row offsets [nrows + 1]
-//           into the records; padded to 128 B
+//           into the records, each | (the row's Dirichlet bits << 24); padded to 128 B
 //   u_n   = the tile's node set, own rows first, each row [3][n_s] (n_s * 24 B)
 //   alpha = the tile's elements, each row [n_s] (n_s * 8 B)
 //   F_k   = the own rows' load fields, [n_fields][nrows][4] (32 B rows; n_fields is known

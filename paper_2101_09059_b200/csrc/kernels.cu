@@ -1084,11 +1084,12 @@ k_step_mf_staged(const StepArgs a) {
             const int s0 = h * 64 + 2 * lane;                 // this lane's realisations s0, s0 + 1
             const uint32_t lofs = uint32_t(s0) * 8u;
             const int32_t* roff = reinterpret_cast<const int32_t*>(st + hdr.w);
-            const int32_t kb = roff[wr], ke = roff[wr + 1];
+            const int32_t ro = roff[wr];                      // incidence offset | fixed bits << 24
+            const int32_t kb = ro & 0xffffff, ke = roff[wr + 1] & 0xffffff;
             const unsigned char* rec0 = st + kMfsHdrBytes;
             // update operands from global memory first: their latency hides behind the gather
+            // (registers: a shared-memory slot per lane costs stage space, measured slower)
             Vec<2> c1v, c2v, c3v, uold[3];
-            uint8_t fx = 0;
             if (!APPLY) {
                 const int64_t ic = i * n_s + s0;
                 c1v = ld_ro<2>(a.c1 + ic);
@@ -1099,7 +1100,6 @@ k_step_mf_staged(const StepArgs a) {
                 const double* po = sc.uo + 3 * ic - 2 * s0;   // (i * 3 + d) * n_s + s0
 #pragma unroll
                 for (int d = 0; d < 3; ++d) uold[d] = ld_rw<2>(po + d * n_s);
-                fx = a.fixed ? __ldg(a.fixed + i) : uint8_t(0);
             }
             const unsigned char* own = st + hdr.z + size_t(wr) * US + lofs;   // own row = slot wr
             Vec<2> uo[3], pa[3], pb[3];
@@ -1142,12 +1142,14 @@ k_step_mf_staged(const StepArgs a) {
                 store_y<2>(a, i, s0, y);
             } else {
                 Upd<2> upd;
-                upd.fx = fx;
+                upd.fx = uint8_t(uint32_t(ro) >> 24);
                 upd.c1 = c1v;
-#pragma unroll
-                for (int v = 0; v < 2; ++v) {
-                    upd.c2.v[v] = C23 ? c2v.v[v] : a.c2;
-                    upd.c3.v[v] = C23 ? c3v.v[v] : a.c3;
+                if constexpr (C23) {
+                    upd.c2 = c2v;
+                    upd.c3 = c3v;
+                } else {
+                    upd.c2.v[0] = upd.c2.v[1] = a.c2;
+                    upd.c3.v[0] = upd.c3.v[1] = a.c3;
                 }
                 const double* fk = reinterpret_cast<const double*>(st + f_base) + wr * 4;
 #pragma unroll
@@ -1504,7 +1506,8 @@ static cudaError_t launch_mf_warp(const StepArgs& a, cudaStream_t st) {
 // to multiples of 4 warps, so 11 + 1 warps leave 168 registers per thread, 15 + 1 only 128).
 // ENS_MFS_SHAPE = "CWxS" picks one of the built ones.
 struct MfsShapeDef { const char* name; int cw, s; };
-static constexpr MfsShapeDef kMfsShapes[] = {{"11x3", 11, 3}, {"11x2", 11, 2}, {"11x4", 11, 4}};
+static constexpr MfsShapeDef kMfsShapes[] = {{"11x3", 11, 3}, {"11x2", 11, 2}, {"11x4", 11, 4}, {"15x3", 15, 3},
+                                             {"15x4", 15, 4}};
 static int mfs_shape_id() {
     static const int id = [] {
         const char* e = std::getenv("ENS_MFS_SHAPE");
@@ -1520,7 +1523,7 @@ static constexpr int kMfsSmemMax = 227 * 1024;
 
 MfsShape mf_staged_shape() {
     const MfsShapeDef& d = kMfsShapes[mfs_shape_id()];
-    const int sb = ((kMfsSmemMax - 2 * d.s * 8 - 256) / d.s) & ~127;     // 256 B: static shared (s_coef)
+    const int sb = ((kMfsSmemMax - 256 - 2 * d.s * 8) / d.s) & ~127;     // 256 B: static shared (s_coef)
     return {d.cw, d.s, sb};
 }
 
@@ -1566,6 +1569,8 @@ static cudaError_t launch_mf_staged(const StepArgs& a, cudaStream_t st) {
     switch (mfs_shape_id()) {
         case 1: return launch_mf_staged_shape<11, 2>(a, st);
         case 2: return launch_mf_staged_shape<11, 4>(a, st);
+        case 3: return launch_mf_staged_shape<15, 3>(a, st);
+        case 4: return launch_mf_staged_shape<15, 4>(a, st);
         default: return launch_mf_staged_shape<11, 3>(a, st);
     }
 }
