@@ -27,11 +27,12 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# the device function each --kernel runs (matrix-free: per-warp TMA item streams when the
-# library chose them, ens_info.mf_variant)
+# the device function each --kernel runs (matrix-free: the data path the library chose,
+# ens_info.mf_variant)
 _KERNEL_FN = {"assembled": lambda info: "k_step_assembled",
               "assembled_sym": lambda info: "k_step_assembled_sym",
-              "matrix_free": lambda info: "k_step_mf_warp" if info.get("mf_variant") else "k_step_matrix_free"}
+              "matrix_free": lambda info: {1: "k_step_matrix_free", 2: "k_step_mf_warp",
+                                           3: "k_step_mf_staged"}.get(info.get("mf_variant"), "?")}
 METRIC = ("ensemble DOF-updates/s (N_s×DOF×steps/s) and fused-step HBM GB/s vs peak")
 FALLBACK_HBM_GBS = 6650.0      # /opt/skills/guides/B200_PROFILING.md fallback
 

@@ -5,6 +5,7 @@
 #include "ens.h"
 
 #include <algorithm>
+#include <iterator>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -35,7 +36,7 @@ struct MfTileSet {
     int64_t row0 = 0, rows = 0;
     int32_t ntiles = 0, stage_bytes = 0;
     ens::MfTile* d_tiles = nullptr;
-    int2* d_runs = nullptr;
+    int4* d_entries = nullptr;
     unsigned char* d_blob = nullptr;
 };
 
@@ -95,6 +96,7 @@ struct ens_ctx {
     int32_t n_s = 0, s_begin = 0;
     int32_t kernel = 0, damping = 0, dist = 0, rank = 0, world = 1;
     int32_t mf_variant = 0;                 // matrix-free data path in use (ENS_MF_*), resolved at create
+    ens::MfsPlan mfs_plan;                  // F3 shape and tiling (kernels.cu mf_staged_plan)
     double dt = 0.0, dt_cfl = 0.0, c_d = 0.0;
     double c2 = 2.0, c3 = 1.0;
     int32_t bandwidth = 0;
@@ -383,10 +385,11 @@ cudaError_t launch_rows(const ens_ctx* c, const Part& p, ens::StepArgs a, int64_
             if (t.row0 == row0 && t.rows == rows) ts = &t;
         if (!ts) return cudaErrorInvalidValue;
         a.mfs_tiles = ts->d_tiles;
-        a.mfs_runs = ts->d_runs;
+        a.mfs_entries = ts->d_entries;
         a.mfs_blob = ts->d_blob;
         a.mfs_ntiles = ts->ntiles;
         a.mfs_stage_bytes = ts->stage_bytes;
+        a.mfs_shape = c->mfs_plan.shape;
     }
     switch (c->kernel) {
         case ENS_KERNEL_MATRIX_FREE: return ens::launch_step_matrix_free(a, st);
@@ -556,113 +559,238 @@ struct Global {
     const std::vector<int32_t>* contrib;       // e * 9 + a * 3 + b
 };
 
-// Matrix-free F3 tiles of rows [row0, row0 + rows) (device.hpp MfTile, kernels.cu
-// k_step_mf_staged): greedily the longest run of at most kMfsMaxRows consecutive rows whose
-// stage image -- blob, u_n rows of the node set, alpha rows of the elements, F_k -- fits the
-// stage budget and moves in at most kMfsMaxRuns runs.
-int build_mf_tiles(ens_ctx* c, const std::vector<int32_t>& ip, const std::vector<ens::FanRec>& rec,
-                   const std::vector<double>& k18, const std::vector<uint8_t>& fx, int64_t row0, int64_t rows,
-                   MfTileSet& out) {
-    const ens::MfsShape sh = ens::mf_staged_shape();
-    const int64_t R = ens::kMfsMaxRows;
-    const size_t US = size_t(c->n_s) * 24, AS = size_t(c->n_s) * 8;
-    struct Lay {
-        std::vector<int32_t> nodes, elems;     // neighbour nodes outside the own rows; elements (sorted)
-        std::vector<int2> urun, erun;
-        size_t blob_bytes = 0, bytes = 0;
-    };
-    auto runs_of = [](const std::vector<int32_t>& v, std::vector<int2>& r) {
-        for (size_t k = 0; k < v.size(); ++k) {
-            if (!r.empty() && r.back().x + r.back().y == v[k]) ++r.back().y;
-            else r.push_back(make_int2(v[k], 1));
-        }
-    };
-    auto layout = [&](int64_t r0, int64_t n, Lay& L) {
-        L.nodes.clear();
-        L.elems.clear();
-        L.urun.clear();
-        L.erun.clear();
-        for (int32_t k = ip[size_t(r0)]; k < ip[size_t(r0 + n)]; ++k) {
-            for (int32_t q : {rec[size_t(k)].n_prev, rec[size_t(k)].n_next})
-                if (q < r0 || q >= r0 + n) L.nodes.push_back(q);
-            L.elems.push_back(rec[size_t(k)].e);
-        }
-        std::sort(L.nodes.begin(), L.nodes.end());
-        L.nodes.erase(std::unique(L.nodes.begin(), L.nodes.end()), L.nodes.end());
-        std::sort(L.elems.begin(), L.elems.end());
-        L.elems.erase(std::unique(L.elems.begin(), L.elems.end()), L.elems.end());
-        L.urun.push_back(make_int2(int32_t(r0), int32_t(n)));
-        runs_of(L.nodes, L.urun);
-        runs_of(L.elems, L.erun);
-        const size_t ninc = size_t(ip[size_t(r0 + n)] - ip[size_t(r0)]);
-        L.blob_bytes = (ens::kMfsHdrBytes + ninc * ens::kMfsRecBytes + size_t(n + 1) * 4 + 127) & ~size_t(127);
-        L.bytes = L.blob_bytes + size_t(n + int64_t(L.nodes.size())) * US + L.elems.size() * AS;   // + F_k
-    };
-    std::vector<ens::MfTile> tiles;
-    std::vector<int2> runs;
-    std::vector<unsigned char> blob;
-    Lay best, L;
-    for (int64_t r = row0; r < row0 + rows;) {
-        int64_t nb = 0;
-        for (int64_t n = 1; n <= R && r + n <= row0 + rows; ++n) {
-            layout(r, n, L);
-            if (L.bytes + size_t(ens::kMaxFields * n * 32) > size_t(sh.stage_bytes) ||
-                L.urun.size() + L.erun.size() > size_t(ens::kMfsMaxRuns))
-                break;
-            std::swap(best, L);
-            nb = n;
-        }
-        if (nb == 0)
-            return fail(c, ENS_E_UNSUPPORTED, "matrix-free staged: the operands of row " + std::to_string(r) +
-                                                  " exceed one shared-memory stage");
-        ens::MfTile t{};
-        t.run0 = int32_t(runs.size());
-        t.n_runs = int32_t(best.urun.size());
-        t.n_eruns = int32_t(best.erun.size());
-        runs.insert(runs.end(), best.urun.begin(), best.urun.end());
-        runs.insert(runs.end(), best.erun.begin(), best.erun.end());
-        t.blob = int64_t(blob.size());
-        t.blob_bytes = int32_t(best.blob_bytes);
-        t.u_base = int32_t(best.blob_bytes);
-        t.a_base = int32_t(best.blob_bytes + size_t(nb + int64_t(best.nodes.size())) * US);
-        t.f_base = int32_t(best.bytes);
-        t.stage_bytes = int32_t(best.bytes);
-        t.r0 = int32_t(r);
-        t.nrows = int32_t(nb);
-        tiles.push_back(t);
-        auto uslot = [&](int32_t q) -> uint32_t {
-            if (q >= r && q < r + nb) return uint32_t(q - r);
-            return uint32_t(nb + (std::lower_bound(best.nodes.begin(), best.nodes.end(), q) - best.nodes.begin()));
-        };
-        auto eslot = [&](int32_t e) {
-            return uint32_t(std::lower_bound(best.elems.begin(), best.elems.end(), e) - best.elems.begin());
-        };
-        const int32_t k0 = ip[size_t(r)], k1 = ip[size_t(r + nb)];
-        std::vector<unsigned char> b(best.blob_bytes, 0);
-        const int32_t rowoff = ens::kMfsHdrBytes + (k1 - k0) * ens::kMfsRecBytes;
-        const int32_t hdr[8] = {int32_t(r), int32_t(nb), t.u_base, rowoff, t.f_base, 0, 0, 0};
-        std::memcpy(b.data(), hdr, sizeof(hdr));
-        for (int32_t k = k0; k < k1; ++k) {
-            const ens::FanRec& fr = rec[size_t(k)];
-            const int32_t rc[4] = {int32_t(t.a_base + eslot(fr.e) * AS), int32_t(t.u_base + uslot(fr.n_next) * US),
-                                   int32_t(t.u_base + uslot(fr.n_prev) * US), fr.restart};
-            unsigned char* dst = b.data() + ens::kMfsHdrBytes + size_t(k - k0) * ens::kMfsRecBytes;
-            std::memcpy(dst, rc, 16);
-            std::memcpy(dst + 16, k18.data() + size_t(k) * 18, 18 * sizeof(double));
-        }
-        for (int64_t j = 0; j <= nb; ++j) {
-            const int32_t o = (ip[size_t(r + j)] - k0) | (j < nb ? int32_t(fx[size_t(r + j)]) << 24 : 0);
-            std::memcpy(b.data() + rowoff + 4 * j, &o, 4);
-        }
-        blob.insert(blob.end(), b.begin(), b.end());
-        r += nb;
+// ---- matrix-free F3 tiles (device.hpp MfTile, kernels.cu k_step_mf_staged) ---------------
+// A tile is a compact patch of at most kMfsMaxRows rows: its stage holds the u_n rows of the
+// patch and of its 1-ring, so a round patch moves fewer neighbour rows per own row than a
+// strip of consecutive RCM rows (measured on c2: 6.3 vs 9.0 KB per row at 76 KB stages).
+struct MfLayout {
+    std::vector<int32_t> rows;                 // own rows (ascending)
+    std::vector<int2> uspan, espan;            // other nodes / elements as spans {first, count}
+    int64_t n_unodes = 0, n_elems = 0;         // rows in the spans (gaps included)
+    size_t blob_bytes = 0, bytes = 0;          // bytes: blob + u + alpha (F_k budgeted separately)
+    int entries = 0;
+};
+
+// spans covering the sorted ids v, merging gaps of at most `gap` ids (one copy each)
+static void spans_of(const std::vector<int32_t>& v, int gap, std::vector<int2>& out, int64_t& total) {
+    out.clear();
+    total = 0;
+    for (int32_t x : v) {
+        if (!out.empty() && x - (out.back().x + out.back().y) <= gap) out.back().y = x - out.back().x + 1;
+        else out.push_back(make_int2(x, 1));
     }
+    for (const int2& sp : out) total += sp.y;
+}
+
+static int count_runs(const std::vector<int32_t>& v) {
+    int n = 0;
+    for (size_t k = 0; k < v.size(); ++k)
+        if (k == 0 || v[k] != v[k - 1] + 1) ++n;
+    return n;
+}
+
+// gaps merged into one bulk copy (ENS_MFS_GAP_U / _A): fewer TMA copies for a few more bytes
+static int mfs_gap(bool u) {
+    static const int gu = [] { const char* e = std::getenv("ENS_MFS_GAP_U"); return e ? std::atoi(e) : 0; }();
+    static const int ga = [] { const char* e = std::getenv("ENS_MFS_GAP_A"); return e ? std::atoi(e) : 0; }();
+    return u ? gu : ga;
+}
+
+static void mf_layout(const std::vector<int32_t>& ip, const std::vector<ens::FanRec>& rec, std::vector<int32_t> rows,
+                      size_t US, size_t AS, MfLayout& L) {
+    std::sort(rows.begin(), rows.end());
+    L.rows = rows;
+    std::vector<int32_t> nodes, elems, other;
+    size_t ninc = 0;
+    for (int32_t r : rows)
+        for (int32_t k = ip[size_t(r)]; k < ip[size_t(r) + 1]; ++k) {
+            nodes.push_back(rec[size_t(k)].n_prev);
+            nodes.push_back(rec[size_t(k)].n_next);
+            elems.push_back(rec[size_t(k)].e);
+            ++ninc;
+        }
+    std::sort(nodes.begin(), nodes.end());
+    nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
+    std::set_difference(nodes.begin(), nodes.end(), rows.begin(), rows.end(), std::back_inserter(other));
+    std::sort(elems.begin(), elems.end());
+    elems.erase(std::unique(elems.begin(), elems.end()), elems.end());
+    spans_of(other, mfs_gap(true), L.uspan, L.n_unodes);
+    spans_of(elems, mfs_gap(false), L.espan, L.n_elems);
+    L.blob_bytes = (size_t(ens::kMfsHdrBytes) + ninc * ens::kMfsRecBytes + (2 * rows.size() + 1) * 4 + 127) & ~size_t(127);
+    L.bytes = L.blob_bytes + (rows.size() + size_t(L.n_unodes)) * US + size_t(L.n_elems) * AS;
+    const int own_runs = count_runs(rows);
+    L.entries = 2 * own_runs + int(L.uspan.size() + L.espan.size()) + 1;   // u + F_k per own run
+}
+
+// Greedy patches of rows [row0, row0 + rows): seed = the first unassigned row (RCM order); grow
+// by the unassigned neighbour adding the fewest new nodes to the tile's node set (ties: lowest
+// id) while the stage image fits.
+static std::vector<std::vector<int32_t>> mf_patches(const std::vector<int32_t>& ip, const std::vector<ens::FanRec>& rec,
+                                                    int64_t n_loc, int64_t row0, int64_t rows, size_t US, size_t AS,
+                                                    size_t SB, const ens::MfsPlan& plan) {
+    auto nbrs = [&](int32_t r, std::vector<int32_t>& v) {
+        v.clear();
+        for (int32_t k = ip[size_t(r)]; k < ip[size_t(r) + 1]; ++k) {
+            v.push_back(rec[size_t(k)].n_prev);
+            v.push_back(rec[size_t(k)].n_next);
+        }
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+    };
+    std::vector<std::vector<int32_t>> tiles;
+    MfLayout L;
+    if (!plan.patches) {                   // strips of consecutive rows
+        for (int64_t r = row0; r < row0 + rows;) {
+            std::vector<int32_t> tile = {int32_t(r)};
+            while (int(tile.size()) < plan.max_rows && r + int64_t(tile.size()) < row0 + rows) {
+                tile.push_back(int32_t(r + int64_t(tile.size())));
+                mf_layout(ip, rec, tile, US, AS, L);
+                if (L.bytes + size_t(ens::kMaxFields) * tile.size() * 32 > SB || L.entries > ens::kMfsMaxEntries - 8) {
+                    tile.pop_back();
+                    break;
+                }
+            }
+            r += int64_t(tile.size());
+            tiles.push_back(tile);
+        }
+        return tiles;
+    }
+    std::vector<std::vector<int32_t>> nb(static_cast<size_t>(rows));
+    for (int64_t r = 0; r < rows; ++r) nbrs(int32_t(row0 + r), nb[size_t(r)]);
+    auto in_range = [&](int32_t x) { return x >= row0 && x < row0 + rows; };
+    std::vector<char> assigned(static_cast<size_t>(rows), 0);
+    std::vector<int32_t> mark(static_cast<size_t>(n_loc), -1);
+    for (int64_t seed = row0; seed < row0 + rows; ++seed) {
+        if (assigned[size_t(seed - row0)]) continue;
+        const int32_t tid = int32_t(tiles.size());
+        std::vector<int32_t> tile = {int32_t(seed)};
+        assigned[size_t(seed - row0)] = 1;
+        mark[size_t(seed)] = tid;
+        for (int32_t z : nb[size_t(seed - row0)]) mark[size_t(z)] = tid;
+        while (int(tile.size()) < plan.max_rows) {
+            int32_t best = -1, bc = 1 << 30;
+            for (int32_t x : tile)
+                for (int32_t y : nb[size_t(x - row0)]) {
+                    if (!in_range(y) || assigned[size_t(y - row0)]) continue;
+                    int32_t cost = mark[size_t(y)] != tid;
+                    for (int32_t z : nb[size_t(y - row0)]) cost += mark[size_t(z)] != tid;
+                    if (cost < bc || (cost == bc && y < best)) { bc = cost; best = y; }
+                }
+            if (best < 0) break;
+            tile.push_back(best);
+            mf_layout(ip, rec, tile, US, AS, L);
+            if (L.bytes + size_t(ens::kMaxFields) * tile.size() * 32 > SB || L.entries > ens::kMfsMaxEntries - 8) {
+                tile.pop_back();
+                break;
+            }
+            assigned[size_t(best - row0)] = 1;
+            mark[size_t(best)] = tid;
+            for (int32_t z : nb[size_t(best - row0)]) mark[size_t(z)] = tid;
+        }
+        tiles.push_back(tile);
+    }
+    return tiles;
+}
+
+// Upload the tile set of one launched row range: copy entries and blobs (final element ids).
+int build_mf_tiles(ens_ctx* c, const std::vector<int32_t>& ip, const std::vector<ens::FanRec>& rec,
+                   const std::vector<double>& k18, const std::vector<uint8_t>& fx,
+                   std::vector<std::vector<int32_t>> patches, int64_t row0, int64_t rows, MfTileSet& out) {
+    const ens::MfsShape sh = ens::mf_staged_shape(c->mfs_plan.shape);
+    const size_t US = size_t(c->n_s) * 24, AS = size_t(c->n_s) * 8;
+    std::vector<ens::MfTile> tiles;
+    std::vector<int4> entries;
+    std::vector<unsigned char> blob;
+    MfLayout L;
+    for (size_t pi = 0; pi < patches.size(); ++pi) {
+        mf_layout(ip, rec, patches[pi], US, AS, L);
+        if (L.entries > ens::kMfsMaxEntries ||
+            L.bytes + size_t(ens::kMaxFields) * L.rows.size() * 32 > size_t(sh.stage_bytes)) {
+            if (L.rows.size() == 1)
+                return fail(c, ENS_E_UNSUPPORTED, "matrix-free staged: the operands of row " +
+                                                      std::to_string(L.rows[0]) + " exceed one shared-memory stage");
+            const size_t h = L.rows.size() / 2;       // split and retry (element ids changed)
+            patches.insert(patches.begin() + int64_t(pi) + 1, std::vector<int32_t>(L.rows.begin() + int64_t(h), L.rows.end()));
+            patches[pi].assign(L.rows.begin(), L.rows.begin() + int64_t(h));
+            --pi;
+            continue;
+        }
+        const int32_t nr = int32_t(L.rows.size());
+        const int32_t u_base = int32_t(L.blob_bytes);
+        const int32_t a_base = int32_t(L.blob_bytes + (L.rows.size() + size_t(L.n_unodes)) * US);
+        const int32_t f_base = int32_t(L.bytes);
+        ens::MfTile t{};
+        t.entry0 = int32_t(entries.size());
+        t.nrows = nr;
+        t.stage_bytes = int32_t(L.bytes);
+        auto add_runs = [&](const std::vector<int32_t>& v, int kind, int32_t base, size_t unit) {
+            for (size_t k = 0; k < v.size();) {
+                size_t n = 1;
+                while (k + n < v.size() && v[k + n] == v[k] + int32_t(n)) ++n;
+                entries.push_back(make_int4(kind, v[k], int32_t(n), base + int32_t(k * unit)));
+                k += n;
+            }
+        };
+        auto add_spans = [&](const std::vector<int2>& v, int kind, int32_t base, size_t unit) {
+            int64_t k = 0;
+            for (const int2& sp : v) {
+                entries.push_back(make_int4(kind, sp.x, sp.y, base + int32_t(k * int64_t(unit))));
+                k += sp.y;
+            }
+        };
+        add_runs(L.rows, ens::kMfsU, u_base, US);
+        add_spans(L.uspan, ens::kMfsU, u_base + int32_t(L.rows.size() * US), US);
+        add_spans(L.espan, ens::kMfsA, a_base, AS);
+        add_runs(L.rows, ens::kMfsF, f_base, 32);
+        entries.push_back(make_int4(ens::kMfsBlob, int32_t(blob.size() / 16), int32_t(L.blob_bytes), 0));
+        t.n_entries = int32_t(entries.size()) - t.entry0;
+        tiles.push_back(t);
+        auto span_slot = [](const std::vector<int2>& v, int32_t q) -> int32_t {
+            int32_t k = 0;
+            for (const int2& sp : v) {
+                if (q >= sp.x && q < sp.x + sp.y) return k + (q - sp.x);
+                k += sp.y;
+            }
+            return -1;
+        };
+        auto uslot = [&](int32_t q) -> int32_t {
+            auto it = std::lower_bound(L.rows.begin(), L.rows.end(), q);
+            if (it != L.rows.end() && *it == q) return int32_t(it - L.rows.begin());
+            return nr + span_slot(L.uspan, q);
+        };
+        auto eslot = [&](int32_t e) { return span_slot(L.espan, e); };
+        size_t ninc = 0;
+        for (int32_t r : L.rows) ninc += size_t(ip[size_t(r) + 1] - ip[size_t(r)]);
+        std::vector<unsigned char> b(L.blob_bytes, 0);
+        const int32_t roff = ens::kMfsHdrBytes + int32_t(ninc) * ens::kMfsRecBytes;
+        const int32_t rid = roff + (nr + 1) * 4;
+        const int32_t hdr[8] = {nr, u_base, roff, f_base, rid, 0, 0, 0};
+        std::memcpy(b.data(), hdr, sizeof(hdr));
+        int32_t q = 0;
+        for (int32_t j = 0; j < nr; ++j) {
+            const int32_t r = L.rows[size_t(j)];
+            const int32_t o = q | int32_t(fx[size_t(r)]) << 24;
+            std::memcpy(b.data() + roff + 4 * j, &o, 4);
+            std::memcpy(b.data() + rid + 4 * j, &r, 4);
+            for (int32_t k = ip[size_t(r)]; k < ip[size_t(r) + 1]; ++k, ++q) {
+                const ens::FanRec& fr = rec[size_t(k)];
+                const int32_t rc[4] = {a_base + eslot(fr.e) * int32_t(AS), u_base + uslot(fr.n_next) * int32_t(US),
+                                       u_base + uslot(fr.n_prev) * int32_t(US), fr.restart};
+                unsigned char* dst = b.data() + ens::kMfsHdrBytes + size_t(q) * ens::kMfsRecBytes;
+                std::memcpy(dst, rc, 16);
+                std::memcpy(dst + 16, k18.data() + size_t(k) * 18, 18 * sizeof(double));
+            }
+        }
+        std::memcpy(b.data() + roff + 4 * nr, &q, 4);
+        blob.insert(blob.end(), b.begin(), b.end());
+    }
+    if (blob.size() / 16 >= (size_t(1) << 31)) return fail(c, ENS_E_UNSUPPORTED, "matrix-free staged: tile blobs exceed 32 GB");
     out.row0 = row0;
     out.rows = rows;
     out.ntiles = int32_t(tiles.size());
     out.stage_bytes = sh.stage_bytes;
     RC_TRY(upload(c, &out.d_tiles, tiles.data(), tiles.size()));
-    RC_TRY(upload(c, &out.d_runs, runs.data(), runs.size()));
+    RC_TRY(upload(c, &out.d_entries, entries.data(), entries.size()));
     RC_TRY(upload(c, &out.d_blob, blob.data(), blob.size()));
     return ENS_OK;
 }
@@ -883,6 +1011,33 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
         if (c->mf_variant == ENS_MF_TILES && int64_t(P.mf_smem_inc) * ens::mf_inc_bytes() > 200 * 1024)
             return fail(c, ENS_E_UNSUPPORTED, "a node has too many incident elements for the matrix-free kernel");
         static_assert(sizeof(ens::FanRec) == sizeof(int4), "FanRec layout");
+        std::vector<std::vector<std::vector<int32_t>>> patches;     // F3: per launched range
+        if (c->mf_variant == ENS_MF_STAGED) {
+            const ens::MfsShape sh = ens::mf_staged_shape(c->mfs_plan.shape);
+            const size_t US = size_t(n_s) * 24, AS = size_t(n_s) * 8;
+            for (const auto& tl : tilings)
+                patches.push_back(tl.second > tl.first
+                                      ? mf_patches(ip, rec, n_loc, tl.first, tl.second - tl.first, US, AS, size_t(sh.stage_bytes), c->mfs_plan)
+                                      : std::vector<std::vector<int32_t>>());
+            // elements renumbered by first touch in the (whole-range) tile order: each tile's
+            // alpha rows then move in few runs
+            std::vector<int32_t> new_of(static_cast<size_t>(Fl), -1);
+            int32_t next = 0;
+            for (const auto& tile : patches[0]) {
+                std::vector<int32_t> rs(tile);
+                std::sort(rs.begin(), rs.end());
+                for (int32_t r : rs)
+                    for (int32_t k = ip[size_t(r)]; k < ip[size_t(r) + 1]; ++k)
+                        if (new_of[size_t(rec[size_t(k)].e)] < 0) new_of[size_t(rec[size_t(k)].e)] = next++;
+            }
+            for (auto& x : new_of)
+                if (x < 0) x = next++;
+            std::vector<double> al2(al.size());
+            for (int64_t e = 0; e < Fl; ++e)
+                std::copy_n(al.data() + size_t(e) * size_t(n_s), n_s, al2.data() + size_t(new_of[size_t(e)]) * size_t(n_s));
+            al.swap(al2);
+            for (auto& r : rec) r.e = new_of[size_t(r.e)];
+        }
         RC_TRY(upload(c, &P.d_inc_ptr, ip.data(), ip.size()));
         RC_TRY(upload(c, &P.d_fan, reinterpret_cast<const int4*>(rec.data()), rec.size()));
         if (ens::mf_diff()) {      // (prev, next) columns only: K^_e[a,a] u_i cancels (kernels.cu DIFF)
@@ -917,10 +1072,11 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
                 RC_TRY(upload(c, &P.d_items, items.data(), items.size()));
             }
             if (c->mf_variant == ENS_MF_STAGED)
-                for (const auto& tl : tilings) {
-                    if (tl.second <= tl.first) continue;
+                for (size_t q = 0; q < tilings.size(); ++q) {
+                    if (tilings[q].second <= tilings[q].first) continue;
                     P.mfs.emplace_back();
-                    RC_TRY(build_mf_tiles(c, ip, rec, k18, fx, tl.first, tl.second - tl.first, P.mfs.back()));
+                    RC_TRY(build_mf_tiles(c, ip, rec, k18, fx, patches[q], tilings[q].first,
+                                          tilings[q].second - tilings[q].first, P.mfs.back()));
                 }
         } else {
             RC_TRY(upload(c, &P.d_Krow, fans.Krow.data() + size_t(k0) * 28, size_t(k1 - k0) * 28));
@@ -1038,6 +1194,7 @@ int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, cons
         else if (req == ENS_MF_WARP && !warp_ok)
             return fail(c, ENS_E_UNSUPPORTED, "mf_variant WARP needs n_s % 64 == 0 and damping != IDENTITY");
         else c->mf_variant = req;
+        c->mfs_plan = ens::mf_staged_plan(c->n_s);
     }
 
     // S0: pattern (RCM + block CSR)

@@ -15,28 +15,34 @@ constexpr int kMaxFields = 4;
 // kinds of the matrix-free item programs (StepArgs::items, kernels.cu F2w)
 constexpr int kItemOwn = 0, kItemPrev = 1, kItemInc = 2, kItemOld = 3, kItemLastApply = 32;
 
-// Matrix-free F3 (kernels.cu k_step_mf_staged): one tile = up to kMfsMaxRows consecutive
-// rows whose operands fit one shared-memory stage, laid out [blob | u_n | alpha | F_k]:
-//   blob  = header int32[8] {r0, nrows, u-image offset, row-offset offset, F_k offset, 0, 0, 0}
-//           (byte offsets within the stage), then per incidence a 160-B record (int4 {alpha
-//           byte offset, next-node byte offset, prev-node byte offset, restart} + the 18 K^
-//           coefficients of the (prev, next) columns), then int32 row offsets [nrows + 1]
-//           into the records, each | (the row's Dirichlet bits << 24); padded to 128 B
-//   u_n   = the tile's node set, own rows first, each row [3][n_s] (n_s * 24 B)
+// Matrix-free F3 (kernels.cu k_step_mf_staged): one tile = up to kMfsMaxRows rows (a compact
+// patch of the mesh, grown greedily on the host) whose operands fit one shared-memory stage,
+// laid out [blob | u_n | alpha | F_k]:
+//   blob  = header int32[8] {nrows, u-image offset, row-offset offset, F_k offset, row-id
+//           offset, 0, 0, 0} (byte offsets within the stage), then per incidence a 160-B
+//           record (int4 {alpha byte offset, next-node byte offset, prev-node byte offset,
+//           restart} + the 18 K^ coefficients of the (prev, next) columns), then int32 row
+//           offsets [nrows + 1] into the records, each | (the row's Dirichlet bits << 24),
+//           then int32 row ids [nrows]; padded to 128 B
+//   u_n   = the tile's node set, its own rows first (tile order), each row [3][n_s] (n_s * 24 B)
 //   alpha = the tile's elements, each row [n_s] (n_s * 8 B)
 //   F_k   = the own rows' load fields, [n_fields][nrows][4] (32 B rows; n_fields is known
 //           only at ens_set_traction, the host budgets kMaxFields)
-// The node and element sets move as runs of consecutive ids (one bulk copy per run).
+// The stage is filled by the tile's COPY ENTRIES (one bulk copy each; int4 {kind, first,
+// count, stage byte offset}): kMfsU u_n rows [first, first + count); kMfsA alpha rows;
+// kMfsF own rows of every load field (offset + k * nrows * 32 for field k); kMfsBlob the
+// blob (first = its offset in mfs_blob / 16, count = bytes).
 constexpr int kMfsHdrBytes = 32;
 constexpr int kMfsRecBytes = 160;
-constexpr int kMfsMaxRuns = 30;          // u runs + alpha runs per tile (lanes 0..29 of the producer)
-constexpr int kMfsMaxRows = 16;
+constexpr int kMfsMaxRows = 32;
+#ifndef ENS_MFS_MAX_ENTRIES
+#define ENS_MFS_MAX_ENTRIES 96
+#endif
+constexpr int kMfsMaxEntries = ENS_MFS_MAX_ENTRIES;   // copy entries per tile (32 per producer lane slot)
+enum { kMfsU = 0, kMfsA = 1, kMfsF = 2, kMfsBlob = 3 };
 struct MfTile {
-    int32_t run0, n_runs, n_eruns, blob_bytes;   // runs[run0, run0 + n_runs) u runs, then n_eruns alpha runs
-    int64_t blob;                                 // byte offset of the tile's blob in mfs_blob
-    int32_t u_base, a_base, f_base;               // stage byte offsets of the u, alpha and F_k images
-    int32_t stage_bytes;                          // bytes of blob + u + alpha (+ F_k: n_fields * nrows * 32)
-    int32_t r0, nrows, pad0, pad1;
+    int32_t entry0, n_entries;    // copy entries [entry0, entry0 + n_entries) of mfs_entries
+    int32_t nrows, stage_bytes;   // bytes of blob + u + alpha (+ F_k: n_fields * nrows * 32)
 };
 
 struct StepArgs {
@@ -67,11 +73,11 @@ struct StepArgs {
     const int4* items = nullptr;        // {node, elem | row, K^ row, kind | flags}
     // matrix-free tile stages (kernels.cu F3) of the launched row range
     const MfTile* mfs_tiles = nullptr;
-    const int2* mfs_runs = nullptr;     // {first id, count}
+    const int4* mfs_entries = nullptr;  // copy entries {kind, first, count, stage offset}
     const unsigned char* mfs_blob = nullptr;
     int32_t mfs_ntiles = 0;
     int32_t mfs_stage_bytes = 0;        // bytes per stage (shared memory = stages * this + barriers)
-    int32_t mfs_prefetch = 0;           // 1: the producer warms L2 with the next tile's runs (launcher)
+    int32_t mfs_shape = 0;              // consumer warps x stages (kernels.cu kMfsShapes)
     // update coefficients
     const double* c1 = nullptr;
     const double* c2a = nullptr;        // null => scalars c2, c3
@@ -128,7 +134,10 @@ int pick_vec_mf(int32_t n_s);   // matrix-free kernel
 bool mf_staged_applies(int32_t n_s);
 // F3 launch shape: consumer warps, stages, and the stage byte budget of one tile
 struct MfsShape { int consumers, stages, stage_bytes; };
-MfsShape mf_staged_shape();
+MfsShape mf_staged_shape(int shape);
+// per-context plan: shape index, tiling (patches or strips of consecutive rows), rows per tile
+struct MfsPlan { int shape = 0; bool patches = false; int max_rows = 16; };
+MfsPlan mf_staged_plan(int32_t n_s);
 bool mf_diff();            // matrix-free: neighbours relative to u_i, (prev, next) K^ columns only (ENS_MF_DIFF, default 1)
 int mf_inc_bytes();        // matrix-free: shared-memory bytes per incidence (K^ image + fan record)
 // coef_buf[(step & 1)] = the load coefficients of step *step_base (after host changes)

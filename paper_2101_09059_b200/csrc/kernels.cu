@@ -970,63 +970,61 @@ k_step_mf_staged(const StepArgs a) {
     const uint32_t US = uint32_t(n_s) * 24u, AS = uint32_t(n_s) * 8u;
 
     if (wid == CW) {                                          // ---- producer warp
-        // Descriptors are software-pipelined: the tile two ahead and the runs of the next
-        // one are loaded while this one is issued, so no global load latency sits between
-        // a stage becoming free and its refill.
+        // Each lane issues copy entries lane, lane + 32, lane + 64 of the tile.  The entries
+        // of the next tile are loaded while this one is issued (software-pipelined), so no
+        // global load latency sits between a stage becoming free and its refill.
+        constexpr int EPL = kMfsMaxEntries / 32;
         const int nf = APPLY ? 0 : a.n_fields;
-        MfTile d1{}, d2{};
-        int2 run1 = make_int2(0, 0);
-        auto load_runs = [&](const MfTile& q) {
-            int2 r = make_int2(0, 0);
-            if (lane < q.n_runs + q.n_eruns) r = __ldg(a.mfs_runs + q.run0 + lane);
-            return r;
+        // tile descriptors two ahead (dn2), entries one ahead (en, from dn already in registers):
+        // no load waits on another load inside the loop
+        MfTile dn{}, dn2{};
+        int4 en[EPL];
+        auto load_entries = [&]() {
+#pragma unroll
+            for (int q = 0; q < EPL; ++q)
+                en[q] = lane + 32 * q < dn.n_entries ? __ldg(a.mfs_entries + dn.entry0 + lane + 32 * q)
+                                                     : make_int4(-1, 0, 0, 0);
         };
-        if (ta < tb) d1 = a.mfs_tiles[ta];
-        if (ta + 1 < tb) d2 = a.mfs_tiles[ta + 1];
-        if (ta < tb) run1 = load_runs(d1);
+        if (ta < tb) {
+            dn = a.mfs_tiles[ta];
+            load_entries();
+        }
+        if (ta + 1 < tb) dn2 = a.mfs_tiles[ta + 1];
         for (int32_t t = ta; t < tb; ++t) {
             const int it = int(t - ta), s = it % S;
             const uint32_t full = bar0 + 8u * s, stage = smem_s + uint32_t(s) * SB;
-            const MfTile d = d1;
-            const int2 run = run1;
-            d1 = d2;
-            if (t + 2 < tb) d2 = a.mfs_tiles[t + 2];
-            if (t + 1 < tb) run1 = load_runs(d1);
-            const int nr = d.n_runs + d.n_eruns;
-            // stage slot of each run: exclusive prefix of the counts within the u runs and
-            // within the alpha runs
-            const bool is_u = lane < d.n_runs;
-            int x = lane < nr ? run.y : 0;
+            const MfTile d = dn;
+            int4 e[EPL];
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, off);
-                if (lane >= off && ((lane - off < d.n_runs) == is_u)) x += y;
+            for (int q = 0; q < EPL; ++q) e[q] = en[q];
+            if (t + 1 < tb) {
+                dn = dn2;
+                load_entries();
+                if (t + 2 < tb) dn2 = a.mfs_tiles[t + 2];
             }
-            const uint32_t slot = uint32_t(x - (lane < nr ? run.y : 0));
             if (it >= S) mbar_wait(bar0 + 8u * (S + s), uint32_t(it / S - 1) & 1u);
             if (lane == 0) mbar_expect_tx(full, uint32_t(d.stage_bytes) + uint32_t(nf * d.nrows) * 32u);
             __syncwarp();
-            if (is_u) {
-                tma_bulk_g2s(stage + uint32_t(d.u_base) + slot * US, sc.un + int64_t(run.x) * 3 * n_s,
-                             uint32_t(run.y) * US, full);
-            } else if (lane < nr) {
-                tma_bulk_g2s(stage + uint32_t(d.a_base) + slot * AS, a.alpha + int64_t(run.x) * n_s,
-                             uint32_t(run.y) * AS, full);
-            } else if (lane == 30) {
-                for (int k = 0; k < nf; ++k)
-                    tma_bulk_g2s(stage + uint32_t(d.f_base) + uint32_t(k * d.nrows) * 32u,
-                                 a.Fk + (int64_t(k) * a.fk_rows + d.r0) * 4, uint32_t(d.nrows) * 32u, full);
-            } else if (lane == 31) {
-                tma_bulk_g2s(stage, a.mfs_blob + d.blob, uint32_t(d.blob_bytes), full);
+            // one bulk-copy call site per entry slot (a lane-varying copy compiles to a loop over
+            // the active lanes): source and size are selected arithmetically, not by branches
+#pragma unroll
+            for (int q = 0; q < EPL; ++q) {
+                const int4 x = e[q];
+                if (x.x < 0 || x.x == kMfsF) continue;
+                const unsigned char* src =
+                    x.x == kMfsU ? reinterpret_cast<const unsigned char*>(sc.un) + int64_t(x.y) * US
+                    : x.x == kMfsA ? reinterpret_cast<const unsigned char*>(a.alpha) + int64_t(x.y) * AS
+                                   : a.mfs_blob + int64_t(x.y) * 16;
+                const uint32_t bytes = x.x == kMfsU ? uint32_t(x.z) * US : x.x == kMfsA ? uint32_t(x.z) * AS : uint32_t(x.z);
+                tma_bulk_g2s(stage + uint32_t(x.w), src, bytes, full);
             }
-            // warm L2 with the u_n and alpha runs of the next tile (its descriptors are in
-            // registers already): its stage fill then hits L2 (ENS_MFS_PF=1, measured)
-            if (a.mfs_prefetch && t + 1 < tb && lane < d1.n_runs + d1.n_eruns) {
-                const bool u = lane < d1.n_runs;
-                const void* src = u ? static_cast<const void*>(sc.un + int64_t(run1.x) * 3 * n_s)
-                                    : static_cast<const void*>(a.alpha + int64_t(run1.x) * n_s);
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                             :: "l"(src), "r"(uint32_t(run1.y) * (u ? US : AS)) : "memory");
+#pragma unroll
+            for (int q = 0; q < EPL; ++q) {                  // own-row load fields (nf copies each)
+                const int4 x = e[q];
+                if (x.x != kMfsF) continue;
+                for (int k = 0; k < nf; ++k)
+                    tma_bulk_g2s(stage + uint32_t(x.w) + uint32_t(k * d.nrows) * 32u,
+                                 a.Fk + (int64_t(k) * a.fk_rows + x.y) * 4, uint32_t(x.z) * 32u, full);
             }
         }
         return;
@@ -1035,7 +1033,6 @@ k_step_mf_staged(const StepArgs a) {
     // ---- consumer warps.  Units = (row, 64-realisation slice) pairs, H = N_s / 64 per row,
     // numbered consecutively over this CTA's tiles; warp wid takes units wid, wid + CW, ...
     const int H = n_s >> 6;
-    const int dwr = CW / H, dh = CW - dwr * H;                // unit step CW = dwr rows + dh slices
     auto ld2 = [&](const unsigned char* p) {
         const double2 v = *reinterpret_cast<const double2*>(p);
         Vec<2> r;
@@ -1072,36 +1069,37 @@ k_step_mf_staged(const StepArgs a) {
         const int it = int(t - ta), s = it % S;
         const unsigned char* st = smem + size_t(s) * SB;
         mbar_wait(bar0 + 8u * s, uint32_t(it / S) & 1u);
-        const int4 hdr = *reinterpret_cast<const int4*>(st);  // {r0, nrows, u image, row offsets}
-        const int32_t f_base = *reinterpret_cast<const int32_t*>(st + 16);
-        const int32_t nunits = hdr.y * H;
-        int32_t uu = wid - ubase % CW;
-        if (uu < 0) uu += CW;
-        int wr = uu, h = 0;                                   // uu = wr * H + h
-        if (H > 1) { wr = uu / H; h = uu - wr * H; }
-        for (; uu < nunits; uu += CW) {
-            const int64_t i = hdr.x + wr;
+        const int4 hdr = *reinterpret_cast<const int4*>(st);  // {nrows, u image, row offsets, F_k}
+        const int32_t* rowid = reinterpret_cast<const int32_t*>(st + *reinterpret_cast<const int32_t*>(st + 16));
+        const int32_t nunits = hdr.x * H;
+        // Units go round-robin to the CW consumer warps.  (Weighting the warps of the SMSP that
+        // also holds the producer less was measured slower: the most loaded warp releases each
+        // stage last, which holds the producer back.)
+        auto unit = [&](int32_t uu) {
+            int wr = uu, h = 0;                               // uu = wr * H + h
+            if (H > 1) { wr = uu / H; h = uu - wr * H; }
+            const int64_t i = rowid[wr];
             const int s0 = h * 64 + 2 * lane;                 // this lane's realisations s0, s0 + 1
             const uint32_t lofs = uint32_t(s0) * 8u;
-            const int32_t* roff = reinterpret_cast<const int32_t*>(st + hdr.w);
+            const int32_t* roff = reinterpret_cast<const int32_t*>(st + hdr.z);
             const int32_t ro = roff[wr];                      // incidence offset | fixed bits << 24
             const int32_t kb = ro & 0xffffff, ke = roff[wr + 1] & 0xffffff;
             const unsigned char* rec0 = st + kMfsHdrBytes;
             // update operands from global memory first: their latency hides behind the gather
             // (registers: a shared-memory slot per lane costs stage space, measured slower)
             Vec<2> c1v, c2v, c3v, uold[3];
+            const int64_t ic = i * n_s + s0;
+            const double* po = sc.uo + 3 * ic - 2 * s0;       // (i * 3 + d) * n_s + s0
             if (!APPLY) {
-                const int64_t ic = i * n_s + s0;
                 c1v = ld_ro<2>(a.c1 + ic);
                 if constexpr (C23) {
                     c2v = ld_ro<2>(a.c2a + ic);
                     c3v = ld_ro<2>(a.c3a + ic);
                 }
-                const double* po = sc.uo + 3 * ic - 2 * s0;   // (i * 3 + d) * n_s + s0
 #pragma unroll
                 for (int d = 0; d < 3; ++d) uold[d] = ld_rw<2>(po + d * n_s);
             }
-            const unsigned char* own = st + hdr.z + size_t(wr) * US + lofs;   // own row = slot wr
+            const unsigned char* own = st + hdr.y + size_t(wr) * US + lofs;   // own row = slot wr
             Vec<2> uo[3], pa[3], pb[3];
 #pragma unroll
             for (int d = 0; d < 3; ++d) uo[d] = ld2(own + d * AS);
@@ -1151,7 +1149,7 @@ k_step_mf_staged(const StepArgs a) {
                     upd.c2.v[0] = upd.c2.v[1] = a.c2;
                     upd.c3.v[0] = upd.c3.v[1] = a.c3;
                 }
-                const double* fk = reinterpret_cast<const double*>(st + f_base) + wr * 4;
+                const double* fk = reinterpret_cast<const double*>(st + hdr.w) + wr * 4;
 #pragma unroll
                 for (int d = 0; d < 3; ++d) {
                     upd.un[d] = uo[d];
@@ -1159,15 +1157,15 @@ k_step_mf_staged(const StepArgs a) {
                     double f = 0.0;
 #pragma unroll
                     for (int q = 0; q < kMaxFields; ++q)
-                        if (q < a.n_fields) f = fma(s_coef[q], fk[q * hdr.y * 4 + d], f);
+                        if (q < a.n_fields) f = fma(s_coef[q], fk[q * hdr.x * 4 + d], f);
                     upd.f[d] = f;
                 }
                 upd_store<2>(a, sc, i, s0, y, upd);
             }
-            wr += dwr;
-            h += dh;
-            if (h >= H) { h -= H; ++wr; }
-        }
+        };
+        int32_t uu = wid - ubase % CW;
+        if (uu < 0) uu += CW;
+        for (; uu < nunits; uu += CW) unit(uu);
         ubase += nunits;
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 8u * (S + s));
@@ -1507,22 +1505,39 @@ static cudaError_t launch_mf_warp(const StepArgs& a, cudaStream_t st) {
 // ENS_MFS_SHAPE = "CWxS" picks one of the built ones.
 struct MfsShapeDef { const char* name; int cw, s; };
 static constexpr MfsShapeDef kMfsShapes[] = {{"11x3", 11, 3}, {"11x2", 11, 2}, {"11x4", 11, 4}, {"15x3", 15, 3},
-                                             {"15x4", 15, 4}};
-static int mfs_shape_id() {
+                                             {"15x2", 15, 2}};
+// the context's shape (StepArgs::mfs_shape, chosen at create: ens_mf_staged_plan)
+static int mfs_env_shape() {
     static const int id = [] {
         const char* e = std::getenv("ENS_MFS_SHAPE");
         if (e)
             for (int k = 0; k < int(sizeof(kMfsShapes) / sizeof(kMfsShapes[0])); ++k)
                 if (!std::strcmp(e, kMfsShapes[k].name)) return k;
-        return 0;
+        return -1;
     }();
     return id;
 }
 
 static constexpr int kMfsSmemMax = 227 * 1024;
 
-MfsShape mf_staged_shape() {
-    const MfsShapeDef& d = kMfsShapes[mfs_shape_id()];
+// Default plan per N_s (measured on B200, DESIGN.md §5 F3): at N_s = 64 a node row is 1.5 KB
+// and the per-copy cost of the TMA engine dominates, so strips of <= 16 consecutive RCM rows
+// (few long runs) in 3 stages win; at N_s >= 128 the rows are 3 KB+ and the byte volume
+// dominates, so compact patches of <= 32 rows (fewer neighbour rows per own row) in 2 larger
+// stages win.  ENS_MFS_SHAPE / ENS_MFS_TILING / ENS_MFS_MAXROWS override.
+MfsPlan mf_staged_plan(int32_t n_s) {
+    MfsPlan p;
+    const int env = mfs_env_shape();
+    p.shape = env >= 0 ? env : (n_s == 64 ? 0 : 1);
+    const char* t = std::getenv("ENS_MFS_TILING");
+    p.patches = t ? std::strcmp(t, "strip") != 0 : n_s != 64;
+    const char* r = std::getenv("ENS_MFS_MAXROWS");
+    p.max_rows = r ? std::max(1, std::min(kMfsMaxRows, std::atoi(r))) : (p.patches ? kMfsMaxRows : 16);
+    return p;
+}
+
+MfsShape mf_staged_shape(int shape) {
+    const MfsShapeDef& d = kMfsShapes[shape];
     const int sb = ((kMfsSmemMax - 256 - 2 * d.s * 8) / d.s) & ~127;     // 256 B: static shared (s_coef)
     return {d.cw, d.s, sb};
 }
@@ -1546,13 +1561,7 @@ static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
         attr_set.fetch_or(bit, std::memory_order_release);
     }
     const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(sms[dev & 63], a.mfs_ntiles)));
-    static const int pf = [] {          // L2 prefetch of the next tile's runs (0 = off)
-        const char* e = std::getenv("ENS_MFS_PF");
-        return e ? std::atoi(e) : 0;
-    }();
-    StepArgs b = a;
-    b.mfs_prefetch = pf;
-    k_step_mf_staged<APPLY, CW, S, NS, C23><<<grid, (CW + 1) * 32, smem, st>>>(b);
+    k_step_mf_staged<APPLY, CW, S, NS, C23><<<grid, (CW + 1) * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -1566,11 +1575,11 @@ static cudaError_t launch_mf_staged_shape(const StepArgs& a, cudaStream_t st) {
 }
 
 static cudaError_t launch_mf_staged(const StepArgs& a, cudaStream_t st) {
-    switch (mfs_shape_id()) {
+    switch (a.mfs_shape) {
         case 1: return launch_mf_staged_shape<11, 2>(a, st);
         case 2: return launch_mf_staged_shape<11, 4>(a, st);
         case 3: return launch_mf_staged_shape<15, 3>(a, st);
-        case 4: return launch_mf_staged_shape<15, 4>(a, st);
+        case 4: return launch_mf_staged_shape<15, 2>(a, st);
         default: return launch_mf_staged_shape<11, 3>(a, st);
     }
 }

@@ -1,0 +1,157 @@
+"""North-star parity bars for every kernel and data path, on a B200 (-m gpu).
+
+* 10^4 steps at 0.9 dt_crit (exact stability threshold, dense eigenvalues) on the c1 mesh,
+  both damping forms (mode 1 C~ = c_d M~, mode 2 C~ = c_d I: PAPER.md:343 and DESIGN.md
+  reading 4), N_s = 4 and 64: relative L2 of u_n and u_{n-1} <= 1e-9 against the oracle
+  (BASELINE.json north_star), for the assembled half storage (a1s) and
+  every matrix-free data path that applies (TILES, WARP, STAGED).
+* c2 at full size (96 x 262 rings, N_s = 64) in the bench's launch configuration, every
+  kernel: sampled realisations recomputed one by one by the oracle, <= 1e-9 after 10^3 steps.
+* A node-partitioned run (P = 3, NCCL-style and P2P halos) compared directly with the oracle,
+  not only with the unpartitioned CUDA run.
+"""
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+import oracle
+from paper_2101_09059_b200 import solver
+from paper_2101_09059_b200.inputs import configs, fields, loads, mesh as meshmod
+
+pytestmark = pytest.mark.gpu
+RHO, NU, KS = 1.06, 0.5, 5.0 / 6.0
+C_D = {"mass": 250.0, "identity": 25.0}      # 1/s (mode 1); g/s (mode 2, nodal masses ~0.1 g)
+_ORACLE = {}
+
+
+def _crit_dt(om):
+    free = np.repeat(om.fixed == 0, 3)
+    best = np.inf
+    for s in range(om.n_s):
+        K = om.K_sparse(s).toarray()[np.ix_(free, free)]
+        d = 1.0 / np.sqrt(np.repeat(om.m[s], 3)[free])
+        lam = sla.eigvalsh(d[:, None] * K * d[None, :], subset_by_index=[K.shape[0] - 1, K.shape[0] - 1])
+        best = min(best, 2.0 / math.sqrt(lam[-1]))
+    return best
+
+
+def _c1_case(n_s, damping):
+    """The oracle's 10^4-step trajectory on c1 (cached per (N_s, damping) across kernels)."""
+    key = (n_s, damping)
+    if key not in _ORACLE:
+        cfg = configs.make("c1", n_s=n_s)
+        m = cfg.mesh
+        om0 = oracle.OracleModel(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS)
+        dt = 0.9 * _crit_dt(om0)
+        tr = loads.pulsatile(m.xyz, m.tris, period=0.1, systole=0.04, n_tab=101, ramp_T=0.02)
+        om = oracle.OracleModel(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS,
+                                damping=solver.DAMPING[damping], c_d=C_D[damping], dt=dt)
+        om.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+        snaps = {}
+        for chunk in (100, 900, 9000):
+            om.run(chunk)
+            snaps[om.step] = (om.u_n.copy(), om.u_nm1.copy())
+        _ORACLE[key] = (cfg, dt, tr, snaps)
+    return _ORACLE[key]
+
+
+_CASES = [("assembled_sym", "auto")] + [("matrix_free", v) for v in ("tiles", "warp", "staged")]
+
+
+@pytest.mark.parametrize("damping", ["mass", "identity"])
+@pytest.mark.parametrize("n_s", [4, 64])
+@pytest.mark.parametrize("kernel,variant", _CASES)
+def test_1e4_steps_every_kernel(kernel, variant, n_s, damping):
+    if kernel == "matrix_free" and variant in ("warp", "staged") and n_s % 64:
+        pytest.skip("data path needs N_s % 64 == 0")
+    if variant == "warp" and damping == "identity":
+        pytest.skip("WARP keeps c2, c3 scalar (mode 1 / none only)")
+    cfg, dt, tr, snaps = _c1_case(n_s, damping)
+    m = cfg.mesh
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS, dt=dt,
+                          damping=damping, c_d=C_D[damping], kernel=kernel, mf_variant=variant)
+    if kernel == "matrix_free":
+        assert ens.info()["mf_variant"] == solver.MF_VARIANT[variant if variant != "auto" else "staged"]
+    ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    done = 0
+    for step in sorted(snaps):
+        ens.step(step - done)
+        done = step
+        u, up, _, s = ens.get_state()
+        assert s == step
+        ref_u, ref_up = snaps[step]
+        for a, b in ((u, ref_u), (up, ref_up)):
+            assert np.linalg.norm(a - b) <= 1e-9 * np.linalg.norm(b), (step, np.linalg.norm(a - b) / np.linalg.norm(b))
+    ens.close()
+
+
+_C2 = {}
+
+
+def _c2_oracle(samples, steps):
+    if "ref" not in _C2:
+        cfg = configs.make("c2")
+        m = cfg.mesh
+        # dt is the CFL step of the whole ensemble (E_max over all realisations): take it from
+        # an all-realisation context of the kernel under test (identical for every kernel)
+        ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS,
+                              damping="mass", c_d=cfg.c_d, kernel="assembled_sym")
+        dt_all = ens.info()["dt"]
+        ens.close()
+        idx = list(samples)
+        om = oracle.OracleModel(m.xyz, m.tris, m.fixed, cfg.E[idx], cfg.h[idx], rho=RHO, nu=NU, k_shear=KS,
+                                damping=1, c_d=cfg.c_d, dt=dt_all)
+        om.set_traction(cfg.traction.F, cfg.traction.tab_t, cfg.traction.tab_g, 0.0, 0.0)
+        om.run(steps)
+        _C2["ref"] = (cfg, dt_all, om.u_n.copy())
+    return _C2["ref"]
+
+
+@pytest.mark.parametrize("kernel,variant", [("assembled", "auto"), ("assembled_sym", "auto"),
+                                            ("matrix_free", "staged"), ("matrix_free", "warp"),
+                                            ("matrix_free", "tiles")])
+def test_c2_full_size_every_kernel(kernel, variant):
+    """c2 (V = 25,152, N_s = 64, mode-1 damping) in the bench's launch configuration: the
+    oracle recomputes realisations {0, 17, 63} (ensemble equivalence: each alone) once; every
+    kernel / data path must match them to 1e-9 after 10^3 steps."""
+    samples, steps = (0, 17, 63), 1000
+    cfg, dt, ref = _c2_oracle(samples, steps)
+    m = cfg.mesh
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS,
+                          damping="mass", c_d=cfg.c_d, kernel=kernel, mf_variant=variant)
+    assert ens.info()["dt"] == dt
+    ens.set_traction(cfg.traction.F)
+    ens.step(steps)
+    u = ens.get_state(want_prev=False)[0]
+    ens.close()
+    for k, s in enumerate(samples):
+        assert np.linalg.norm(u[s] - ref[k]) <= 1e-9 * np.linalg.norm(ref[k]), s
+
+
+@pytest.mark.parametrize("halo", ["nccl", "p2p"])
+@pytest.mark.parametrize("kernel,variant", [("assembled_sym", "auto"), ("matrix_free", "staged"),
+                                            ("matrix_free", "warp")])
+def test_node_partition_vs_oracle(kernel, variant, halo):
+    """P = 3 parts (one context), compared with the oracle directly: SpMM <= 1e-12, and
+    u_n, u_{n-1} <= 1e-9 after 500 pulsatile steps."""
+    m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(24, 60), 0.01, 3), 7)
+    E, h, _ = fields.sample_materials(m.xyz, m.tris, 64, E_mean=7e6, E_std=7e5, h_mean=0.4, h_std=0.04,
+                                      rho_corr=3.7, seed=8)
+    tr = loads.pulsatile(m.xyz, m.tris, period=0.01, systole=0.004, ramp_T=0.003)
+    par = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, kernel=kernel,
+                          mf_variant=variant, dt=5e-5, damping="mass", c_d=80.0, dist="node", world=3, halo=halo)
+    om = oracle.OracleModel(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, damping=1, c_d=80.0, dt=5e-5)
+    x = np.random.default_rng(3).uniform(-1, 1, (64, m.n_nodes, 3))
+    y, yo = par.apply_stiffness(x), om.spmm(x)
+    assert np.linalg.norm(y - yo) <= 1e-12 * np.linalg.norm(yo)
+    par.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    om.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    par.step(500)
+    om.run(500)
+    u, up, _, s = par.get_state()
+    assert s == 500
+    for a, b in ((u, om.u_n), (up, om.u_nm1)):
+        assert np.linalg.norm(a - b) <= 1e-9 * np.linalg.norm(b)
+    par.close()
