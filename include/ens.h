@@ -165,6 +165,8 @@ typedef struct {
     int32_t halo;                       /* ens_options.halo (NODE contexts) */
     int32_t mf_variant;                 /* MATRIX_FREE: the data path in use (ENS_MF_TILES / WARP /
                                            STAGED); 0 for the assembled kernels */
+    int32_t comm_rank, comm_nranks;     /* NODE with nccl_comm: ncclCommUserRank / ncclCommCount of the
+                                           communicator the halo runs on; -1 otherwise */
 } ens_info;
 
 /* Create a context: validate the mesh, build the RCM-ordered block-CSR pattern, the

@@ -48,7 +48,8 @@ class EnsInfo(C.Structure):
                 ("device_bytes", C.c_int64), ("rcm_bandwidth", C.c_int32),
                 ("n_owned", C.c_int64), ("halo_bytes_per_step", C.c_int64),
                 ("launches_per_step", C.c_int32), ("reassemble_every", C.c_int32), ("graph_steps", C.c_int32),
-                ("halo", C.c_int32), ("mf_variant", C.c_int32)]
+                ("halo", C.c_int32), ("mf_variant", C.c_int32), ("comm_rank", C.c_int32),
+                ("comm_nranks", C.c_int32)]
 
 
 EXPORTS = [

@@ -145,12 +145,18 @@ struct ens_ctx {
     int32_t* d_etri = nullptr;              // [F][3] RCM ids
 
     int32_t graph_steps = 64;               // CUDA graph of this many steps (single part, no halo)
-    cudaGraphExec_t graph = nullptr;
+    // one graph per parity of the step it starts at: the NCCL / device-copy halos receive
+    // into buffer (step + 1) & 1, fixed in the captured nodes (the kernels read the step
+    // from the device counter and need no such split)
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
     bool graph_dirty = true;
 
     bool has_halo() const { return parts.size() > 1 || multi; }
     bool p2p() const { return has_halo() && halo == ENS_HALO_P2P; }
-    bool use_graphs() const { return graph_steps > 0 && (!has_halo() || p2p()) && reassemble_every == 0; }
+    // the step loop runs as CUDA graphs of graph_steps steps with every halo: the NCCL
+    // send/recv (captured on the comm stream forked from the step stream), the device-copy
+    // emulation and the P2P flags are all capturable; re-assembly steps are not
+    bool use_graphs() const { return graph_steps > 0 && reassemble_every == 0; }
 };
 
 namespace {
@@ -232,8 +238,10 @@ int upload(ens_ctx* c, T** out, const T* host, size_t count) {
 }
 
 void drop_graph(ens_ctx* c) {
-    if (c->graph) cudaGraphExecDestroy(c->graph);
-    c->graph = nullptr;
+    for (auto& g : c->graph) {
+        if (g) cudaGraphExecDestroy(g);
+        g = nullptr;
+    }
     c->graph_dirty = true;
 }
 
@@ -447,8 +455,8 @@ int launch_interior(ens_ctx* c, int64_t k, cudaStream_t st) {
 // the interior rows run on the step stream.  Neighbours only ever write ghost rows of the
 // buffer this part is not reading, and only after it published the step before, so two
 // buffers suffice (no acknowledgement needed).
-int enqueue_step_p2p(ens_ctx* c, int64_t k, cudaStream_t st) {
-    const int64_t step = c->step + k;
+int enqueue_step_p2p(ens_ctx* c, int64_t step0, int64_t k, cudaStream_t st) {
+    const int64_t step = step0 + k;
     const bool fork = !reassembly_due(c, step);
     cudaStream_t hs;
     RC_TRY(fork_halo(c, st, fork, &hs));
@@ -468,9 +476,11 @@ int enqueue_step_p2p(ens_ctx* c, int64_t k, cudaStream_t st) {
     return join_halo(c, st, fork);
 }
 
-int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
-    const int64_t step = c->step + k;            // host mirror of *d_step + k
-    if (c->p2p()) return enqueue_step_p2p(c, k, st);
+// step0: the host mirror of *d_step when the step runs (c->step for direct launches; a step
+// of the right parity when captured into a graph)
+int enqueue_step(ens_ctx* c, int64_t step0, int64_t k, cudaStream_t st) {
+    const int64_t step = step0 + k;              // host mirror of *d_step + k
+    if (c->p2p()) return enqueue_step_p2p(c, step0, k, st);
     for (Part& p : c->parts) RC_TRY(reassemble_if_due(c, p, step, st));
     if (!c->has_halo()) {
         ens::StepArgs a = part_args(c, c->parts[0]);
@@ -526,23 +536,25 @@ int enqueue_step(ens_ctx* c, int64_t k, cudaStream_t st) {
 
 // Capture graph_steps steps + the counter advance on a private stream (the caller's stream
 // may be the legacy default stream, which cannot capture).
-int build_graph(ens_ctx* c) {
-    drop_graph(c);
+int build_graph(ens_ctx* c, int parity) {
+    cudaGraphExec_t& ge = c->graph[parity];
+    if (ge) cudaGraphExecDestroy(ge);
+    ge = nullptr;
     cudaStream_t cap = nullptr;
     CUDA_TRY(c, cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     cudaError_t err = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
     int rc = ENS_OK;
-    for (int32_t k = 0; err == cudaSuccess && rc == ENS_OK && k < c->graph_steps; ++k) rc = enqueue_step(c, k, cap);
+    for (int32_t k = 0; err == cudaSuccess && rc == ENS_OK && k < c->graph_steps; ++k)
+        rc = enqueue_step(c, parity, k, cap);
     if (err == cudaSuccess && rc == ENS_OK) err = ens::launch_advance(c->d_step, c->graph_steps, cap);
     cudaGraph_t g = nullptr;
     cudaError_t e2 = cudaStreamEndCapture(cap, &g);
     if (err == cudaSuccess) err = e2;
-    if (err == cudaSuccess && rc == ENS_OK) err = cudaGraphInstantiate(&c->graph, g, 0);
+    if (err == cudaSuccess && rc == ENS_OK) err = cudaGraphInstantiate(&ge, g, 0);
     if (g) cudaGraphDestroy(g);
     cudaStreamDestroy(cap);
     if (rc) return rc;
     if (err != cudaSuccess) return cuda_fail(c, err, "CUDA graph capture of the step loop");
-    c->graph_dirty = false;
     return ENS_OK;
 }
 
@@ -1245,6 +1257,32 @@ int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, cons
             for (int ab = 0; ab < 9; ++ab) contrib[size_t(fillp[size_t(blk[size_t(9 * e + ab)])]++)] = int32_t(9 * e + ab);
     } else {
         fans = ens::build_fans(m, pat.iperm, Khat);
+        if (c->mf_variant == ENS_MF_STAGED) {
+            // every single row's stage image must fit (own + neighbour u rows, alpha rows,
+            // records, F_k): at large N_s a high-degree node may not; AUTO then falls back to
+            // TILES, an explicit STAGED request fails
+            const ens::MfsShape sh = ens::mf_staged_shape(c->mfs_plan.shape);
+            const size_t US = size_t(c->n_s) * 24, AS = size_t(c->n_s) * 8;
+            size_t worst = 0;
+            std::vector<int32_t> nb;
+            for (int64_t i = 0; i < V; ++i) {
+                nb.clear();
+                for (int32_t k = fans.ptr[size_t(i)]; k < fans.ptr[size_t(i) + 1]; ++k) {
+                    nb.push_back(fans.rec[size_t(k)].n_prev);
+                    nb.push_back(fans.rec[size_t(k)].n_next);
+                }
+                std::sort(nb.begin(), nb.end());
+                const size_t nn = size_t(std::unique(nb.begin(), nb.end()) - nb.begin());
+                const size_t ninc = size_t(fans.ptr[size_t(i) + 1] - fans.ptr[size_t(i)]);
+                const size_t blob = (size_t(ens::kMfsHdrBytes) + ninc * ens::kMfsRecBytes + 12 + 127) & ~size_t(127);
+                worst = std::max(worst, blob + (1 + nn) * US + ninc * AS + size_t(ens::kMaxFields) * 32);
+            }
+            if (worst > size_t(sh.stage_bytes)) {
+                if (!opt || opt->mf_variant == ENS_MF_AUTO) c->mf_variant = ENS_MF_TILES;
+                else return fail(c, ENS_E_UNSUPPORTED, "mf_variant STAGED: one row's operands (" + std::to_string(worst) +
+                                                          " B) exceed a shared-memory stage at this N_s");
+            }
+        }
     }
 
     // partitions: one part unless node-partitioned; all parts here unless NCCL is used
@@ -1560,13 +1598,16 @@ int ens_step(ens_ctx* c, int64_t n) {
     }
     int64_t left = n;
     if (c->use_graphs() && n >= c->graph_steps) {
-        if (c->graph_dirty) RC_TRY(build_graph(c));
+        if (c->graph_dirty) drop_graph(c);
+        c->graph_dirty = false;
         for (; left >= c->graph_steps; left -= c->graph_steps) {
-            CUDA_TRY(c, cudaGraphLaunch(c->graph, c->stream));
+            const int par = int(c->step & 1);
+            if (!c->graph[par]) RC_TRY(build_graph(c, par));
+            CUDA_TRY(c, cudaGraphLaunch(c->graph[par], c->stream));
             c->step += c->graph_steps;
         }
     }
-    for (int64_t k = 0; k < left; ++k) RC_TRY(enqueue_step(c, k, c->stream));
+    for (int64_t k = 0; k < left; ++k) RC_TRY(enqueue_step(c, c->step, k, c->stream));
     if (left) CUDA_TRY(c, ens::launch_advance(c->d_step, left, c->stream));
     c->step += left;
     return ENS_OK;
@@ -1953,6 +1994,14 @@ int ens_query(const ens_ctx* c, ens_info* info) {
     info->reassemble_every = c->reassemble_every;
     info->halo = c->halo;
     info->mf_variant = c->kernel == ENS_KERNEL_MATRIX_FREE ? c->mf_variant : 0;
+    info->comm_rank = info->comm_nranks = -1;
+    if (c->nccl_comm && c->nccl && c->nccl->comm_count && c->nccl->comm_user_rank) {
+        int r = -1, n = -1;
+        if (c->nccl->comm_user_rank(c->nccl_comm, &r) == 0 && c->nccl->comm_count(c->nccl_comm, &n) == 0) {
+            info->comm_rank = r;
+            info->comm_nranks = n;
+        }
+    }
     // algorithmic HBM bytes of the rows this context advances: values +
     // u_n, u_{n-1} read, u_{n+1} written, c1 (+ c2, c3) per node per realisation
     const int64_t ns = c->n_s, per_node = 3 * 8 * 3 + 8 + (c->damping == ENS_DAMP_IDENTITY ? 16 : 0);

@@ -21,6 +21,8 @@ const Nccl* nccl_load(std::string* err) {
             nccl.group_start = reinterpret_cast<decltype(nccl.group_start)>(dlsym(h, "ncclGroupStart"));
             nccl.group_end = reinterpret_cast<decltype(nccl.group_end)>(dlsym(h, "ncclGroupEnd"));
             nccl.error_string = reinterpret_cast<decltype(nccl.error_string)>(dlsym(h, "ncclGetErrorString"));
+            nccl.comm_count = reinterpret_cast<decltype(nccl.comm_count)>(dlsym(h, "ncclCommCount"));
+            nccl.comm_user_rank = reinterpret_cast<decltype(nccl.comm_user_rank)>(dlsym(h, "ncclCommUserRank"));
             if (!nccl.ok()) why = "libnccl.so.2 lacks ncclSend/ncclRecv/ncclGroupStart/ncclGroupEnd";
         }
     }

@@ -22,6 +22,8 @@ struct Nccl {
     int (*group_start)() = nullptr;
     int (*group_end)() = nullptr;
     const char* (*error_string)(int) = nullptr;
+    int (*comm_count)(Comm, int*) = nullptr;       // ncclCommCount
+    int (*comm_user_rank)(Comm, int*) = nullptr;   // ncclCommUserRank
     bool ok() const { return send && recv && group_start && group_end; }
 };
 
