@@ -337,6 +337,17 @@ int ens_host_materials(int64_t n_nodes, int64_t n_tris, const double* xyz, const
                        int32_t n_s, const double* E, const double* h, double rho,
                        double cfl_safety, double* alpha, double* mass, double* dt_cfl);
 
+/* The matrix-free STAGED tiling of the whole RCM row range, as ens_create builds it for a
+ * single-part context (kernels.cu k_step_mf_staged; DESIGN.md §5 F3): patches = 1 compact
+ * patches / 0 strips of consecutive rows, at most max_rows rows per tile, stage_bytes = the
+ * budget of one shared-memory stage (<= 0: the library's for this n_s).  Outputs: tile_of[V]
+ * = the tile of each RCM row; tile_bytes[V] (first *n_tiles used) = blob + u_n + alpha bytes
+ * of each tile (F_k excluded), tile_entries[V] = its bulk copies; *budget = the stage budget
+ * used.  Host only. */
+int ens_host_mf_tiles(int64_t n_nodes, int64_t n_tris, const double* xyz, const int32_t* tris, int32_t n_s,
+                      int32_t patches, int32_t max_rows, int64_t stage_bytes, int32_t* tile_of,
+                      int64_t* tile_bytes, int32_t* tile_entries, int64_t* n_tiles, int64_t* budget);
+
 /* ---- test-only: synthetic operators (kernel unit tests, not the user contract) ----- */
 
 /* A context on a caller-given block-CSR pattern (any numbering, used as is) and values:

@@ -58,7 +58,7 @@ EXPORTS = [
     "ens_host_pattern", "ens_host_partition", "ens_host_ghosts", "ens_host_element_stiffness",
     "ens_host_materials", "ens_create_csr", "ens_get_owned", "ens_host_halo_plan", "ens_stress",
     "ens_displacement_stats", "ens_matern_fields", "ens_p2p_export", "ens_p2p_connect", "ens_observe",
-    "ens_observe_wait", "ens_measure_fp64",
+    "ens_observe_wait", "ens_measure_fp64", "ens_host_mf_tiles",
 ]
 P2P_BLOB_BYTES = 256
 
@@ -112,6 +112,7 @@ def lib():
         "ens_observe": (C.c_int, [vp, vp]),
         "ens_observe_wait": (C.c_int, [vp, P(i64)]),
         "ens_measure_fp64": (C.c_int, [i32, P(f64)]),
+        "ens_host_mf_tiles": (C.c_int, [i64, i64, vp, vp, i32, i32, i32, i64, vp, vp, vp, P(i64), P(i64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

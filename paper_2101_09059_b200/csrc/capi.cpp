@@ -2116,6 +2116,46 @@ int ens_host_halo_plan(int64_t n_nodes, const int64_t* row_ptr, const int32_t* c
     return ENS_OK;
 }
 
+int ens_host_mf_tiles(int64_t n_nodes, int64_t n_tris, const double* xyz, const int32_t* tris, int32_t n_s,
+                      int32_t patches, int32_t max_rows, int64_t stage_bytes, int32_t* tile_of,
+                      int64_t* tile_bytes, int32_t* tile_entries, int64_t* n_tiles, int64_t* budget) {
+    if (n_s < 64 || n_s % 64 || max_rows < 1 || max_rows > ens::kMfsMaxRows)
+        return fail(nullptr, ENS_E_ARG, "ens_host_mf_tiles: n_s % 64 == 0 and 1 <= max_rows <= 32");
+    ens::MeshView m{n_nodes, n_tris, xyz, tris};
+    int64_t bad = -1;
+    if (ens::validate_mesh(m, &bad)) return fail(nullptr, ENS_E_MESH, "invalid mesh");
+    const ens::Pattern pat = ens::build_pattern(m);
+    std::vector<double> Khat(size_t(81 * n_tris)), area(static_cast<size_t>(n_tris));
+    for (int64_t e = 0; e < n_tris; ++e)
+        ens::element_stiffness(xyz + 3 * int64_t(tris[3 * e]), xyz + 3 * int64_t(tris[3 * e + 1]),
+                               xyz + 3 * int64_t(tris[3 * e + 2]), 0.5, 5.0 / 6.0, Khat.data() + 81 * e, area.data() + e);
+    const ens::Fans fans = ens::build_fans(m, pat.iperm, Khat);
+    ens::MfsPlan plan = ens::mf_staged_plan(n_s);
+    plan.patches = patches != 0;
+    plan.max_rows = max_rows;
+    const size_t SB = stage_bytes > 0 ? size_t(stage_bytes) : size_t(ens::mf_staged_shape(plan.shape).stage_bytes);
+    const size_t US = size_t(n_s) * 24, AS = size_t(n_s) * 8;
+    // element ids as build_part numbers them for the matrix-free kernels (first touch)
+    std::vector<ens::FanRec> rec = fans.rec;
+    std::vector<int32_t> first(static_cast<size_t>(n_tris), -1);
+    int32_t next = 0;
+    for (auto& r : rec) {
+        if (first[size_t(r.e)] < 0) first[size_t(r.e)] = next++;
+        r.e = first[size_t(r.e)];
+    }
+    const auto tiles = mf_patches(fans.ptr, rec, n_nodes, 0, n_nodes, US, AS, SB, plan);
+    MfLayout L;
+    for (size_t t = 0; t < tiles.size(); ++t) {
+        for (int32_t r : tiles[t]) tile_of[size_t(r)] = int32_t(t);
+        mf_layout(fans.ptr, rec, tiles[t], US, AS, L);
+        tile_bytes[t] = int64_t(L.bytes);
+        tile_entries[t] = L.entries;
+    }
+    *n_tiles = int64_t(tiles.size());
+    *budget = int64_t(SB);
+    return ENS_OK;
+}
+
 int ens_host_element_stiffness(int64_t n_nodes, int64_t n_tris, const double* xyz, const int32_t* tris, double nu,
                                double k_shear, double* Khat, double* area) {
     (void)n_nodes;

@@ -315,6 +315,20 @@ def host_ghosts(row_ptr, col, lo, hi):
     return g[:n.value].copy()
 
 
+def host_mf_tiles(xyz, tris, n_s, patches=True, max_rows=32, stage_bytes=0):
+    """The STAGED matrix-free tiling of the whole row range (ens_host_mf_tiles): returns
+    (tile_of[V] in RCM order, tile_bytes[n_tiles], tile_entries[n_tiles], budget)."""
+    xyz, tris = _c(xyz, np.float64), _c(tris, np.int32)
+    V = xyz.shape[0]
+    tile_of = np.empty(V, np.int32)
+    tb = np.empty(V, np.int64)
+    te = np.empty(V, np.int32)
+    n, budget = C.c_int64(), C.c_int64()
+    check(lib().ens_host_mf_tiles(V, tris.shape[0], _p(xyz), _p(tris), int(n_s), int(bool(patches)), int(max_rows),
+                                  int(stage_bytes), _p(tile_of), _p(tb), _p(te), C.byref(n), C.byref(budget)))
+    return tile_of, tb[:n.value].copy(), te[:n.value].copy(), budget.value
+
+
 def host_element_stiffness(xyz, tris, nu, k_shear):
     xyz, tris = _c(xyz, np.float64), _c(tris, np.int32)
     F = tris.shape[0]

@@ -204,3 +204,27 @@ def test_null_context_is_an_argument_error():
         assert call() == _ffi.ENS_E_ARG, name
         assert L.ens_last_error(None), name
     L.ens_destroy(None)
+
+
+@pytest.mark.parametrize("n_s", [64, 128])
+def test_mf_staged_tiles_partition_and_budget(n_s):
+    """The STAGED matrix-free tiling (ens_host_mf_tiles): every RCM row in exactly one tile,
+    strips are runs of consecutive rows, every tile's stage image (+ the F_k budget) fits the
+    stage and moves in <= 96 bulk copies; compact patches move fewer bytes per row than
+    strips at the same budget (each patch's 1-ring is smaller than a strip's)."""
+    m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(48, 80), 0.02, 4), 3)
+    V = m.n_nodes
+    per_row = {}
+    for patches in (False, True):
+        tile_of, tb, te, budget = solver.host_mf_tiles(m.xyz, m.tris, n_s, patches=patches, max_rows=32,
+                                                       stage_bytes=77312)
+        n = len(tb)
+        assert budget == 77312 and n > 0
+        assert tile_of.min() == 0 and tile_of.max() == n - 1
+        rows_per = np.bincount(tile_of, minlength=n)
+        assert rows_per.sum() == V and rows_per.min() >= 1 and rows_per.max() <= 32
+        assert np.all(tb + 4 * 32 * rows_per <= budget) and np.all(te <= 96) and np.all(te >= 3)
+        if not patches:
+            assert np.all(np.diff(tile_of) >= 0)          # consecutive rows, tiles in row order
+        per_row[patches] = tb.sum() / V
+    assert per_row[True] < per_row[False]
