@@ -965,8 +965,11 @@ k_step_mf_staged(const StepArgs a) {
     const StepCtx sc = step_ctx(a);
     const int n_s = NS ? NS : a.n_s;
     const int32_t nt = a.mfs_ntiles;
-    const int32_t ta = int32_t(int64_t(nt) * blockIdx.x / gridDim.x);
-    const int32_t tb = int32_t(int64_t(nt) * (blockIdx.x + 1) / gridDim.x);
+    // tiles round-robin over the CTAs (tile t = blockIdx.x + it * gridDim.x): all CTAs sweep
+    // one front of ~gridDim.x consecutive tiles, so a node row loaded by one tile is still in
+    // L2 when the tiles one ring later need it (contiguous per-CTA chunks spread the front
+    // over the whole mesh: c4 moved 1.43x its algorithmic DRAM bytes that way)
+    const int32_t ta = int32_t(blockIdx.x), tb = nt, tstep = int32_t(gridDim.x);
     const uint32_t US = uint32_t(n_s) * 24u, AS = uint32_t(n_s) * 8u;
 
     if (wid == CW) {                                          // ---- producer warp
@@ -989,18 +992,18 @@ k_step_mf_staged(const StepArgs a) {
             dn = a.mfs_tiles[ta];
             load_entries();
         }
-        if (ta + 1 < tb) dn2 = a.mfs_tiles[ta + 1];
-        for (int32_t t = ta; t < tb; ++t) {
-            const int it = int(t - ta), s = it % S;
+        if (ta + tstep < tb) dn2 = a.mfs_tiles[ta + tstep];
+        for (int32_t t = ta; t < tb; t += tstep) {
+            const int it = int((t - ta) / tstep), s = it % S;
             const uint32_t full = bar0 + 8u * s, stage = smem_s + uint32_t(s) * SB;
             const MfTile d = dn;
             int4 e[EPL];
 #pragma unroll
             for (int q = 0; q < EPL; ++q) e[q] = en[q];
-            if (t + 1 < tb) {
+            if (t + tstep < tb) {
                 dn = dn2;
                 load_entries();
-                if (t + 2 < tb) dn2 = a.mfs_tiles[t + 2];
+                if (t + 2 * tstep < tb) dn2 = a.mfs_tiles[t + 2 * tstep];
             }
             if (it >= S) mbar_wait(bar0 + 8u * (S + s), uint32_t(it / S - 1) & 1u);
             if (lane == 0) mbar_expect_tx(full, uint32_t(d.stage_bytes) + uint32_t(nf * d.nrows) * 32u);
@@ -1050,6 +1053,14 @@ k_step_mf_staged(const StepArgs a) {
             const double2 k01 = K2[3 * c], k23 = K2[3 * c + 1], k45 = K2[3 * c + 2];
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
+#ifdef ENS_MF_SPLIT
+                double tp = k01.x * pv[0].v[v], tn = k23.y * nx[0].v[v];
+                tp = fma(k01.y, pv[1].v[v], tp);
+                tn = fma(k45.x, nx[1].v[v], tn);
+                tp = fma(k23.x, pv[2].v[v], tp);
+                tn = fma(k45.y, nx[2].v[v], tn);
+                y[c][v] = fma(al.v[v], tp + tn, y[c][v]);
+#else
                 double t = k01.x * pv[0].v[v];
                 t = fma(k01.y, pv[1].v[v], t);
                 t = fma(k23.x, pv[2].v[v], t);
@@ -1057,6 +1068,7 @@ k_step_mf_staged(const StepArgs a) {
                 t = fma(k45.x, nx[1].v[v], t);
                 t = fma(k45.y, nx[2].v[v], t);
                 y[c][v] = fma(al.v[v], t, y[c][v]);
+#endif
             }
         }
     };
@@ -1065,8 +1077,8 @@ k_step_mf_staged(const StepArgs a) {
         s_coef[lane] = lane < a.n_fields ? a.coef_buf[(sc.step & 1) * kMaxFields + lane] : 0.0;
     asm volatile("bar.sync 1, %0;" :: "r"(CW * 32) : "memory");   // consumers only
     int32_t ubase = 0;                                        // units of the tiles before this one
-    for (int32_t t = ta; t < tb; ++t) {
-        const int it = int(t - ta), s = it % S;
+    for (int32_t t = ta; t < tb; t += tstep) {
+        const int it = int((t - ta) / tstep), s = it % S;
         const unsigned char* st = smem + size_t(s) * SB;
         mbar_wait(bar0 + 8u * s, uint32_t(it / S) & 1u);
         const int4 hdr = *reinterpret_cast<const int4*>(st);  // {nrows, u image, row offsets, F_k}
@@ -1149,16 +1161,22 @@ k_step_mf_staged(const StepArgs a) {
                     upd.c2.v[0] = upd.c2.v[1] = a.c2;
                     upd.c3.v[0] = upd.c3.v[1] = a.c3;
                 }
-                const double* fk = reinterpret_cast<const double*>(st + hdr.w) + wr * 4;
+                // f = sum_k coef_k F_k(i): a runtime loop over the fields in use (usually one);
+                // the F_k rows are 32-B aligned in the stage
+                const unsigned char* fk = st + hdr.w + wr * 32;
+                upd.f[0] = upd.f[1] = upd.f[2] = 0.0;
+                for (int q = 0; q < a.n_fields; ++q) {
+                    const double2 f01 = *reinterpret_cast<const double2*>(fk + q * hdr.x * 32);
+                    const double f2 = *reinterpret_cast<const double*>(fk + q * hdr.x * 32 + 16);
+                    const double cq = s_coef[q];
+                    upd.f[0] = fma(cq, f01.x, upd.f[0]);
+                    upd.f[1] = fma(cq, f01.y, upd.f[1]);
+                    upd.f[2] = fma(cq, f2, upd.f[2]);
+                }
 #pragma unroll
                 for (int d = 0; d < 3; ++d) {
                     upd.un[d] = uo[d];
                     upd.uo[d] = uold[d];
-                    double f = 0.0;
-#pragma unroll
-                    for (int q = 0; q < kMaxFields; ++q)
-                        if (q < a.n_fields) f = fma(s_coef[q], fk[q * hdr.x * 4 + d], f);
-                    upd.f[d] = f;
                 }
                 upd_store<2>(a, sc, i, s0, y, upd);
             }
@@ -1522,13 +1540,13 @@ static constexpr int kMfsSmemMax = 227 * 1024;
 
 // Default plan per N_s (measured on B200, DESIGN.md §5 F3): at N_s = 64 a node row is 1.5 KB
 // and the per-copy cost of the TMA engine dominates, so strips of <= 16 consecutive RCM rows
-// (few long runs) in 3 stages win; at N_s >= 128 the rows are 3 KB+ and the byte volume
-// dominates, so compact patches of <= 32 rows (fewer neighbour rows per own row) in 2 larger
-// stages win.  ENS_MFS_SHAPE / ENS_MFS_TILING / ENS_MFS_MAXROWS override.
+// (few long runs) win, 11 consumer warps x 3 stages; at N_s >= 128 the rows are 3 KB+ and the
+// byte volume dominates, so compact patches of <= 32 rows (fewer neighbour rows per own row)
+// win, 15 consumer warps x 3 stages.  ENS_MFS_SHAPE / ENS_MFS_TILING / ENS_MFS_MAXROWS override.
 MfsPlan mf_staged_plan(int32_t n_s) {
     MfsPlan p;
     const int env = mfs_env_shape();
-    p.shape = env >= 0 ? env : (n_s == 64 ? 0 : 1);
+    p.shape = env >= 0 ? env : (n_s == 64 ? 0 : 3);     // 11x3 / 15x3 (kMfsShapes)
     const char* t = std::getenv("ENS_MFS_TILING");
     p.patches = t ? std::strcmp(t, "strip") != 0 : n_s != 64;
     const char* r = std::getenv("ENS_MFS_MAXROWS");
