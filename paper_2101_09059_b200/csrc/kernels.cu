@@ -1151,34 +1151,55 @@ k_step_mf_staged(const StepArgs a) {
             if constexpr (APPLY) {
                 store_y<2>(a, i, s0, y);
             } else {
-                Upd<2> upd;
-                upd.fx = uint8_t(uint32_t(ro) >> 24);
-                upd.c1 = c1v;
-                if constexpr (C23) {
-                    upd.c2 = c2v;
-                    upd.c3 = c3v;
-                } else {
-                    upd.c2.v[0] = upd.c2.v[1] = a.c2;
-                    upd.c3.v[0] = upd.c3.v[1] = a.c3;
-                }
                 // f = sum_k coef_k F_k(i): a runtime loop over the fields in use (usually one);
                 // the F_k rows are 32-B aligned in the stage
                 const unsigned char* fk = st + hdr.w + wr * 32;
-                upd.f[0] = upd.f[1] = upd.f[2] = 0.0;
+                double f[3] = {0.0, 0.0, 0.0};
                 for (int q = 0; q < a.n_fields; ++q) {
                     const double2 f01 = *reinterpret_cast<const double2*>(fk + q * hdr.x * 32);
                     const double f2 = *reinterpret_cast<const double*>(fk + q * hdr.x * 32 + 16);
                     const double cq = s_coef[q];
-                    upd.f[0] = fma(cq, f01.x, upd.f[0]);
-                    upd.f[1] = fma(cq, f01.y, upd.f[1]);
-                    upd.f[2] = fma(cq, f2, upd.f[2]);
+                    f[0] = fma(cq, f01.x, f[0]);
+                    f[1] = fma(cq, f01.y, f[1]);
+                    f[2] = fma(cq, f2, f[2]);
                 }
+                // S2 + S4 (Eq. 22), the same operations as upd_store: r = f - y,
+                // u_{n+1} = fma(c1, r, fma(c2, u_n, -(c3 u_{n-1}))), Dirichlet bits, stored over
+                // u_{n-1}; a non-finite value is an all-ones exponent: one max per realisation
+                const uint32_t fxb = uint32_t(ro) >> 24;
+                uint32_t emax[2] = {0u, 0u};
+                Vec<2> w[3];
 #pragma unroll
                 for (int d = 0; d < 3; ++d) {
-                    upd.un[d] = uo[d];
-                    upd.uo[d] = uold[d];
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) {
+                        const double c2v_ = C23 ? c2v.v[v] : a.c2, c3v_ = C23 ? c3v.v[v] : a.c3;
+                        const double r = f[d] - y[d][v];
+                        const double tt = fma(c2v_, uo[d].v[v], -(c3v_ * uold[d].v[v]));
+                        double x = fma(c1v.v[v], r, tt);
+                        if ((fxb >> d) & 1u) x = 0.0;
+                        emax[v] = max(emax[v], uint32_t(__double2hiint(x)) & 0x7ff00000u);
+                        w[d].v[v] = x;
+                    }
+                    st_vec<2>(const_cast<double*>(po) + d * n_s, w[d]);
                 }
-                upd_store<2>(a, sc, i, s0, y, upd);
+                if (a.fwd_ptr) {          // P2P halo: the same values into the neighbours' ghost rows
+                    const int32_t f1 = __ldg(a.fwd_ptr + i + 1);
+                    for (int32_t q = __ldg(a.fwd_ptr + i); q < f1; ++q) {
+                        const int2 dd = a.fwd_dst[q];
+                        double* dst = a.peer_buf[2 * dd.x + int((sc.step + 1) & 1)];
+#pragma unroll
+                        for (int d = 0; d < 3; ++d) st_vec<2>(dst + (int64_t(dd.y) * 3 + d) * n_s + s0, w[d]);
+                    }
+                    if (__ldg(a.fwd_ptr + i) < f1) __threadfence_system();
+                }
+#pragma unroll
+                for (int v = 0; v < 2; ++v)
+                    if (emax[v] == 0x7ff00000u) {
+                        const unsigned long long code = (unsigned long long)(sc.step) << 24 |
+                                                        (unsigned long long)(a.s_global0 + s0 + v);
+                        atomicMin(a.flag, code);
+                    }
             }
         };
         int32_t uu = wid - ubase % CW;
@@ -1540,13 +1561,14 @@ static constexpr int kMfsSmemMax = 227 * 1024;
 
 // Default plan per N_s (measured on B200, DESIGN.md §5 F3): at N_s = 64 a node row is 1.5 KB
 // and the per-copy cost of the TMA engine dominates, so strips of <= 16 consecutive RCM rows
-// (few long runs) win, 11 consumer warps x 3 stages; at N_s >= 128 the rows are 3 KB+ and the
-// byte volume dominates, so compact patches of <= 32 rows (fewer neighbour rows per own row)
-// win, 15 consumer warps x 3 stages.  ENS_MFS_SHAPE / ENS_MFS_TILING / ENS_MFS_MAXROWS override.
+// (few long runs) win; at N_s >= 128 the rows are 3 KB+ and the byte volume dominates, so
+// compact patches of <= 32 rows (fewer neighbour rows per own row) win.  11 consumer warps x
+// 3 stages for both (15 x 3: c4 0.735 vs 0.729 ms, c2 39.3 vs 38.3 us).  ENS_MFS_SHAPE /
+// ENS_MFS_TILING / ENS_MFS_MAXROWS override.
 MfsPlan mf_staged_plan(int32_t n_s) {
     MfsPlan p;
     const int env = mfs_env_shape();
-    p.shape = env >= 0 ? env : (n_s == 64 ? 0 : 3);     // 11x3 / 15x3 (kMfsShapes)
+    p.shape = env >= 0 ? env : 0;                       // 11x3 (kMfsShapes)
     const char* t = std::getenv("ENS_MFS_TILING");
     p.patches = t ? std::strcmp(t, "strip") != 0 : n_s != 64;
     const char* r = std::getenv("ENS_MFS_MAXROWS");

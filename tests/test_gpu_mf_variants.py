@@ -143,3 +143,26 @@ def test_variant_selection_and_rejection():
     ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, kernel="assembled_sym", mf_variant="staged")
     assert ens.info()["mf_variant"] == 0
     ens.close()
+
+
+def test_staged_divergence_detected():
+    """A step 3x above the stability limit blows up: the staged kernel's non-finite check
+    (all-ones exponent per realisation) raises ENS_E_DIVERGED and latches the context."""
+    from paper_2101_09059_b200._ffi import ENS_E_DIVERGED, ENS_E_STATE
+    m = meshmod.cylinder(12, 23)
+    E, h = _mats(m, 64, 51)
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, kernel="matrix_free",
+                          mf_variant="staged")
+    dt = 3.0 * ens.info()["dt"] / 0.9 * 1.3
+    ens.close()
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, kernel="matrix_free",
+                          mf_variant="staged", dt=dt)
+    ens.set_traction(loads.steady(m.xyz, m.tris).F)
+    ens.step(3000)
+    with pytest.raises(EnsError) as ei:
+        ens.sync()
+    assert ei.value.code == ENS_E_DIVERGED
+    with pytest.raises(EnsError) as ei:
+        ens.step(1)
+    assert ei.value.code == ENS_E_STATE
+    ens.close()
