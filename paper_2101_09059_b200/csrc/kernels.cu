@@ -1053,14 +1053,6 @@ k_step_mf_staged(const StepArgs a) {
             const double2 k01 = K2[3 * c], k23 = K2[3 * c + 1], k45 = K2[3 * c + 2];
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
-#ifdef ENS_MF_SPLIT
-                double tp = k01.x * pv[0].v[v], tn = k23.y * nx[0].v[v];
-                tp = fma(k01.y, pv[1].v[v], tp);
-                tn = fma(k45.x, nx[1].v[v], tn);
-                tp = fma(k23.x, pv[2].v[v], tp);
-                tn = fma(k45.y, nx[2].v[v], tn);
-                y[c][v] = fma(al.v[v], tp + tn, y[c][v]);
-#else
                 double t = k01.x * pv[0].v[v];
                 t = fma(k01.y, pv[1].v[v], t);
                 t = fma(k23.x, pv[2].v[v], t);
@@ -1068,7 +1060,6 @@ k_step_mf_staged(const StepArgs a) {
                 t = fma(k45.x, nx[1].v[v], t);
                 t = fma(k45.y, nx[2].v[v], t);
                 y[c][v] = fma(al.v[v], t, y[c][v]);
-#endif
             }
         }
     };
@@ -1155,6 +1146,7 @@ k_step_mf_staged(const StepArgs a) {
                 // the F_k rows are 32-B aligned in the stage
                 const unsigned char* fk = st + hdr.w + wr * 32;
                 double f[3] = {0.0, 0.0, 0.0};
+#pragma unroll 1
                 for (int q = 0; q < a.n_fields; ++q) {
                     const double2 f01 = *reinterpret_cast<const double2*>(fk + q * hdr.x * 32);
                     const double f2 = *reinterpret_cast<const double*>(fk + q * hdr.x * 32 + 16);
