@@ -73,6 +73,7 @@ struct Part {
     double** d_peer_buf = nullptr;                         // [2 n_out]
     unsigned long long** d_out_flag = nullptr;             // [n_out]: &flags_q[p] of neighbour q
     int32_t* d_in_q = nullptr;                             // [n_in] neighbours this part waits for
+    unsigned int* d_hdone = nullptr;                       // CTAs done in the publishing launch (hw_signal)
     int32_t n_out = 0, n_in = 0;
     std::vector<int32_t> out_q;                            // neighbour rank of each slot
     std::vector<int64_t> out_rows;                         // its local row count (owned + ghosts)
@@ -455,22 +456,60 @@ int launch_interior(ens_ctx* c, int64_t k, cudaStream_t st) {
 // the interior rows run on the step stream.  Neighbours only ever write ghost rows of the
 // buffer this part is not reading, and only after it published the step before, so two
 // buffers suffice (no acknowledgement needed).
+// The step kernels a1, a1s and F3 wait for the neighbours' flags and publish their own inside
+// the boundary-row launches (StepArgs::hw_*): 3 launches per part per step instead of 5
+// (ENS_HALO_FUSED=0 restores the separate k_halo_wait / k_halo_signal launches).
+bool halo_fused(const ens_ctx* c) {
+    static const bool on = [] {
+        const char* e = std::getenv("ENS_HALO_FUSED");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return on && (c->kernel != ENS_KERNEL_MATRIX_FREE || c->mf_variant == ENS_MF_STAGED);
+}
+
 int enqueue_step_p2p(ens_ctx* c, int64_t step0, int64_t k, cudaStream_t st) {
     const int64_t step = step0 + k;
     const bool fork = !reassembly_due(c, step);
     cudaStream_t hs;
     RC_TRY(fork_halo(c, st, fork, &hs));
     for (Part& p : c->parts) {
-        CUDA_TRY(c, ens::launch_halo_wait(p.n_in, p.d_in_q, p.d_hflags, c->d_step, k, c->d_herr, hs));
-        RC_TRY(reassemble_if_due(c, p, step, hs));
         ens::StepArgs a = part_args(c, p);
         a.step_off = k;
         a.fwd_ptr = p.d_fwd_ptr;
         a.fwd_dst = p.d_fwd_dst;
         a.peer_buf = p.d_peer_buf;
-        CUDA_TRY(c, launch_rows(c, p, a, 0, p.plan.b_lo, hs));
-        CUDA_TRY(c, launch_rows(c, p, a, p.n_own - p.plan.b_hi, p.plan.b_hi, hs));
-        CUDA_TRY(c, ens::launch_halo_signal(p.n_out, p.d_out_flag, c->d_step, k, hs));
+        const bool fused = halo_fused(c) && fork && (p.plan.b_lo > 0 || p.plan.b_hi > 0);
+        if (!fused) {
+            CUDA_TRY(c, ens::launch_halo_wait(p.n_in, p.d_in_q, p.d_hflags, c->d_step, k, c->d_herr, hs));
+            RC_TRY(reassemble_if_due(c, p, step, hs));
+            CUDA_TRY(c, launch_rows(c, p, a, 0, p.plan.b_lo, hs));
+            CUDA_TRY(c, launch_rows(c, p, a, p.n_own - p.plan.b_hi, p.plan.b_hi, hs));
+            CUDA_TRY(c, ens::launch_halo_signal(p.n_out, p.d_out_flag, c->d_step, k, hs));
+            continue;
+        }
+        // the first boundary launch waits, the last one publishes
+        ens::StepArgs w = a, g = a;
+        w.hw_wait = p.n_in > 0;
+        w.hw_flags = p.d_hflags;
+        w.hw_in_q = p.d_in_q;
+        w.hw_n_in = p.n_in;
+        w.hw_err = c->d_herr;
+        g.hw_signal = p.n_out > 0;
+        g.hw_out = p.d_out_flag;
+        g.hw_n_out = p.n_out;
+        g.hw_done = p.d_hdone;
+        if (p.plan.b_lo > 0 && p.plan.b_hi > 0) {
+            CUDA_TRY(c, launch_rows(c, p, w, 0, p.plan.b_lo, hs));
+            CUDA_TRY(c, launch_rows(c, p, g, p.n_own - p.plan.b_hi, p.plan.b_hi, hs));
+        } else {
+            ens::StepArgs b = w;
+            b.hw_signal = g.hw_signal;
+            b.hw_out = g.hw_out;
+            b.hw_n_out = g.hw_n_out;
+            b.hw_done = g.hw_done;
+            if (p.plan.b_lo > 0) CUDA_TRY(c, launch_rows(c, p, b, 0, p.plan.b_lo, hs));
+            else CUDA_TRY(c, launch_rows(c, p, b, p.n_own - p.plan.b_hi, p.plan.b_hi, hs));
+        }
     }
     RC_TRY(launch_interior(c, k, st));
     return join_halo(c, st, fork);
@@ -1141,6 +1180,8 @@ int build_p2p(ens_ctx* c, Part& P, const std::vector<ens::PartPlan>& plans) {
     RC_TRY(upload(c, &P.d_fwd_ptr, fptr.data(), fptr.size()));
     RC_TRY(upload(c, &P.d_fwd_dst, fdst.data(), fdst.size()));
     RC_TRY(upload(c, &P.d_in_q, in_q.data(), in_q.size()));
+    RC_TRY(dalloc(c, &P.d_hdone, 1));
+    CUDA_TRY(c, cudaMemsetAsync(P.d_hdone, 0, sizeof(unsigned int), c->stream));
     RC_TRY(dalloc(c, &P.d_peer_buf, size_t(2 * P.n_out)));
     RC_TRY(dalloc(c, &P.d_out_flag, size_t(P.n_out)));
     const size_t nf = size_t(c->world);
@@ -2011,6 +2052,8 @@ int ens_query(const ens_ctx* c, ens_info* info) {
         halo += int64_t(p.plan.send_rows.size());
         for (const auto& pe : p.plan.peers) halo += pe.recv_n;
         if (!c->has_halo()) launches += 1;
+        else if (c->p2p() && halo_fused(c) && (p.plan.b_lo > 0 || p.plan.b_hi > 0))
+            launches += 1 + (p.plan.b_lo > 0) + (p.plan.b_hi > 0);
         else if (c->p2p()) launches += 1 + (p.n_in > 0) + (p.plan.b_lo > 0) + (p.plan.b_hi > 0) + (p.n_out > 0);
         else launches += 1 + (p.plan.b_lo > 0) + (p.plan.b_hi > 0) + !p.plan.send_rows.empty();
     }

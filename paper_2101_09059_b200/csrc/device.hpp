@@ -108,6 +108,19 @@ struct StepArgs {
     const int32_t* fwd_ptr = nullptr;   // [rows + 1]
     const int2* fwd_dst = nullptr;
     double* const* peer_buf = nullptr;
+    // P2P halo flags inside the step kernels (a1, a1s and F3): hw_wait =>
+    // before any ghost row is read, every CTA waits until flags[in_q[k]] >= step for each of
+    // the n_in neighbours (ld.acquire.sys, 10 s timeout -> *hw_err); hw_signal => the last CTA
+    // of this launch to finish (counter *hw_done) publishes step + 1 to the n_out neighbours
+    // (fence.sc.sys; st.release.sys).  Set on a part's first / last boundary-row launch, which
+    // replace the separate k_halo_wait / k_halo_signal launches.
+    int32_t hw_wait = 0, hw_signal = 0;
+    const unsigned long long* hw_flags = nullptr;
+    const int32_t* hw_in_q = nullptr;
+    int32_t hw_n_in = 0, hw_n_out = 0;
+    unsigned long long* const* hw_out = nullptr;
+    unsigned int* hw_done = nullptr;
+    unsigned long long* hw_err = nullptr;
 };
 
 // P2P halo: publish "ghost data of u_{step+1} stored" to every neighbour

@@ -183,6 +183,44 @@ __device__ __forceinline__ const double* step_coef(const StepArgs& a, const Step
     return a.coef_buf + (sc.step & 1) * kMaxFields;
 }
 
+// P2P halo flags inside a step kernel (StepArgs::hw_*).  halo_wait_cta: thread 0 of the CTA
+// spins (acquire, system scope) until every neighbour has published step >= sc.step, then
+// the CTA proceeds; a wait longer than 10 s records (step, neighbour) in *hw_err and gives
+// up, so a dead peer cannot hang the device.  halo_signal_last: after the CTA's stores (and
+// forwarding stores) the last CTA of the launch publishes step + 1 to every neighbour.
+__device__ __forceinline__ void halo_wait_one(const StepArgs& a, int64_t step) {
+    for (int k = 0; k < a.hw_n_in; ++k) {
+        const int32_t q = __ldg(a.hw_in_q + k);
+        const unsigned long long* f = a.hw_flags + q;
+        unsigned long long t0, now, v;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+            if ((long long)v >= step) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (now - t0 > 10000000000ull) {
+                atomicMin(a.hw_err, (unsigned long long)step << 16 | (unsigned long long)q);
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+}
+
+__device__ __forceinline__ void halo_signal_last(const StepArgs& a, int64_t step) {
+    // called by thread 0 of each CTA after a __syncthreads that follows every store of the CTA
+    __threadfence();
+    const unsigned int old = atomicAdd(a.hw_done, 1u);
+    if (old == gridDim.x * gridDim.y - 1) {
+        *a.hw_done = 0u;
+        __threadfence();
+        const unsigned long long v = (unsigned long long)(step + 1);
+        asm volatile("fence.sc.sys;" ::: "memory");
+        for (int k = 0; k < a.hw_n_out; ++k)
+            asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(a.hw_out[k]), "l"(v) : "memory");
+    }
+}
+
 // S2 + S4: r = f - y; u_{n+1} = c1 r + c2 u_n - c3 u_{n-1}; Dirichlet; non-finite flag.
 // The operands of the update do not depend on the product, so they are loaded (upd_load)
 // before the gather loop and their latency hides behind it; upd_store finishes the step.
@@ -323,14 +361,7 @@ __device__ __forceinline__ void store_y(const StepArgs& a, int64_t i, int s0, co
 
 // ---- F1: fused step on the assembled per-realisation block values ----------------------
 template <int VEC, bool APPLY>
-__global__ void __launch_bounds__(kThreads)
-k_step_assembled(const StepArgs a) {
-    const StepCtx sc = step_ctx(a);
-    const double* s_coef = APPLY ? nullptr : step_coef(a, sc);
-
-    const int P = a.n_s / VEC;                       // realisation groups per row
-    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= a.V * P) return;
+__device__ __forceinline__ void a1_row(const StepArgs& a, const StepCtx& sc, const double* s_coef, int64_t tid, int P) {
     const int64_t i = a.row0 + tid / P;
     const int s0 = int(tid % P) * VEC;
     const int n_s = a.n_s;
@@ -372,6 +403,26 @@ k_step_assembled(const StepArgs a) {
     }
 }
 
+
+template <int VEC, bool APPLY>
+__global__ void __launch_bounds__(kThreads)
+k_step_assembled(const StepArgs a) {
+    const StepCtx sc = step_ctx(a);
+    const double* s_coef = APPLY ? nullptr : step_coef(a, sc);
+
+    const int P = a.n_s / VEC;                       // realisation groups per row
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a.hw_wait) {                                 // P2P halo: the neighbours' ghost rows of u_n
+        if (threadIdx.x == 0) halo_wait_one(a, sc.step);
+        __syncthreads();
+    }
+    if (tid < a.V * P) a1_row<VEC, APPLY>(a, sc, s_coef, tid, P);
+    if (a.hw_signal) {
+        __syncthreads();
+        if (threadIdx.x == 0) halo_signal_last(a, sc.step);
+    }
+}
+
 // ---- F1s: fused step on symmetric (half) block storage ----------------------------------
 // K_s is symmetric (Eq. 10: B^T C B), so only the blocks (i, j >= i) are stored; row i takes
 // its blocks (i, j < i) as the transposes of blocks stored with row j (within the RCM
@@ -384,14 +435,8 @@ k_step_assembled(const StepArgs a) {
 // an L2 evict_last policy and row j's later own read an evict_first one (HINT 3, default).
 // Without the policies the second reads mostly miss L2.
 template <int VEC, bool APPLY, int HINT>
-__global__ void __launch_bounds__(kThreads)
-k_step_assembled_sym(const StepArgs a) {
-    const StepCtx sc = step_ctx(a);
-    const double* s_coef = APPLY ? nullptr : step_coef(a, sc);
-
-    const int P = a.n_s / VEC;
-    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (tid >= a.V * P) return;
+__device__ __forceinline__ void a1s_row(const StepArgs& a, const StepCtx& sc, const double* s_coef, int64_t tid,
+                                        int P) {
     const int64_t i = a.row0 + tid / P;
     const int s0 = int(tid % P) * VEC;
     const int n_s = a.n_s;
@@ -458,6 +503,24 @@ k_step_assembled_sym(const StepArgs a) {
     } else {
         upd_load<VEC>(a, sc, s_coef, i, s0, upd, true);
         upd_store<VEC>(a, sc, i, s0, y, upd);
+    }
+}
+
+template <int VEC, bool APPLY, int HINT>
+__global__ void __launch_bounds__(kThreads)
+k_step_assembled_sym(const StepArgs a) {
+    const StepCtx sc = step_ctx(a);
+    const double* s_coef = APPLY ? nullptr : step_coef(a, sc);
+    const int P = a.n_s / VEC;
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a.hw_wait) {                                 // P2P halo: the neighbours' ghost rows of u_n
+        if (threadIdx.x == 0) halo_wait_one(a, sc.step);
+        __syncthreads();
+    }
+    if (tid < a.V * P) a1s_row<VEC, APPLY, HINT>(a, sc, s_coef, tid, P);
+    if (a.hw_signal) {
+        __syncthreads();
+        if (threadIdx.x == 0) halo_signal_last(a, sc.step);
     }
 }
 
@@ -961,8 +1024,9 @@ k_step_mf_staged(const StepArgs a) {
             mbar_init(bar0 + 8u * (S + s), CW);
         }
     }
-    __syncthreads();
     const StepCtx sc = step_ctx(a);
+    if (a.hw_wait && threadIdx.x == 0) halo_wait_one(a, sc.step);   // P2P halo: ghost rows of u_n
+    __syncthreads();
     const int n_s = NS ? NS : a.n_s;
     const int32_t nt = a.mfs_ntiles;
     // tiles round-robin over the CTAs (tile t = blockIdx.x + it * gridDim.x): all CTAs sweep
@@ -1030,8 +1094,7 @@ k_step_mf_staged(const StepArgs a) {
                                  a.Fk + (int64_t(k) * a.fk_rows + x.y) * 4, uint32_t(x.z) * 32u, full);
             }
         }
-        return;
-    }
+    } else {
 
     // ---- consumer warps.  Units = (row, 64-realisation slice) pairs, H = N_s / 64 per row,
     // numbered consecutively over this CTA's tiles; warp wid takes units wid, wid + CW, ...
@@ -1201,7 +1264,12 @@ k_step_mf_staged(const StepArgs a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 8u * (S + s));
     }
+    }                                  // consumer warps
     if (!APPLY) step_coef(a, sc);      // block 0 thread 0: the next step's load coefficients
+    if (a.hw_signal) {                 // P2P halo: the last CTA publishes step + 1
+        __syncthreads();
+        if (threadIdx.x == 0) halo_signal_last(a, sc.step);
+    }
 }
 
 __global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
