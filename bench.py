@@ -463,7 +463,27 @@ def main(argv=None):
     else:
         # headline: node partition of the whole config (strong scaling), halo every step
         halo = "nccl" if backend == "nccl" else "p2p"
-        head = Run(base, args.kernel, world, rank, local, dist_mode="node", halo=halo, mf_variant=args.mf_variant)
+        try:
+            head = Run(base, args.kernel, world, rank, local, dist_mode="node", halo=halo, mf_variant=args.mf_variant)
+        except Exception as e:           # never lose the whole line: fall back to the ensemble shard
+            print(f"node partition failed ({e!r}); ensemble shard as the headline", file=sys.stderr, flush=True)
+            head = None
+    if world > 1 and head is None:
+        shard = configs.make(args.config, n_s=n_s, s_begin=rank * n_s)
+        head = Run(shard, args.kernel, world, rank, local, dist_mode="ensemble")
+        clk = ClockSampler(local)
+        head.time(K, args.warmup, stream, barrier, clocks=clk)
+        units = world * n_s * 3 * m.n_nodes * K
+        item = _line_item(head, K, units, peak)
+        item.update(rows_rank=head.info["n_owned"], halo="none", halo_bytes_per_step_rank=0,
+                    launches_per_step=head.info["launches_per_step"])
+        scaling, parallelism = "weak", f"ensemble shard x{world} (node partition failed)"
+        e2e_el, e2e_meta = _e2e(head, args.e2e_windows, args.obs_every, world, barrier)
+        e2e_units = world * n_s * 3 * m.n_nodes * args.obs_every * args.e2e_windows
+        launches = _launch_count(K, head.info.get("graph_steps", 0))
+        head_info = head.info
+        head.close()
+    elif world > 1:
         if head.info.get("comm_nranks", -1) > 0:
             comm = {"backend": "nccl", "rank": head.info["comm_rank"], "nranks": head.info["comm_nranks"],
                     "source": "ncclCommUserRank / ncclCommCount of the halo's communicator"}
@@ -504,6 +524,22 @@ def main(argv=None):
                 r.close()
             except Exception as e:
                 alts["ensemble_shard"] = {"error": repr(e)[:300]}
+            if n_s % world == 0 and n_s // world >= 1:
+                # the same N_s realisations split across the ranks (strong scaling): the
+                # communication-free counterpart of the node partition (BASELINE config c5:
+                # "node-partitioned vs ensemble-sharded")
+                try:
+                    per = n_s // world
+                    shard = configs.make(args.config, n_s=per, s_begin=rank * per)
+                    r = Run(shard, args.kernel, world, rank, local, dist_mode="ensemble")
+                    r.time(K, args.warmup, stream, barrier)
+                    it = _line_item(r, K, n_s * 3 * m.n_nodes * K, peak)
+                    it["scaling"] = "strong"
+                    it["n_s_per_gpu"] = per
+                    alts["ensemble_shard_strong"] = it
+                    r.close()
+                except Exception as e:
+                    alts["ensemble_shard_strong"] = {"error": repr(e)[:300]}
 
     read_gbs = _read_stream_gbs() if rank == 0 else None
     try:                         # FP64 FMA probe: the ALU roofline

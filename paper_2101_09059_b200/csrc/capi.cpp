@@ -1643,7 +1643,19 @@ int ens_step(ens_ctx* c, int64_t n) {
         c->graph_dirty = false;
         for (; left >= c->graph_steps; left -= c->graph_steps) {
             const int par = int(c->step & 1);
-            if (!c->graph[par]) RC_TRY(build_graph(c, par));
+            if (!c->graph[par]) {
+                const int rc = build_graph(c, par);
+                if (rc && c->nccl_comm) {
+                    // an NCCL build that cannot capture its send/recv: every rank runs the same
+                    // code and fails the same way, so all fall back to direct launches together
+                    (void)cudaGetLastError();
+                    drop_graph(c);
+                    c->graph_dirty = false;
+                    c->graph_steps = 0;
+                    break;
+                }
+                RC_TRY(rc);
+            }
             CUDA_TRY(c, cudaGraphLaunch(c->graph[par], c->stream));
             c->step += c->graph_steps;
         }
