@@ -69,3 +69,5 @@ def test_bench_n2_node_partition_headline():
     assert d["cpu_baseline"] is None                          # rank 0 at N = 1 only
     assert d["alternatives"]["ensemble_shard"]["scaling"] == "weak"
     assert d["alternatives"]["ensemble_shard"]["n_s_total"] == 2 * 4
+    strong = d["alternatives"]["ensemble_shard_strong"]            # the 4 realisations split 2 + 2
+    assert strong["scaling"] == "strong" and strong["n_s_per_gpu"] == 2 and strong["value"] > 0
