@@ -1622,7 +1622,8 @@ static constexpr int kMfsSmemMax = 227 * 1024;
 // Default plan per N_s (measured on B200, DESIGN.md §5 F3): at N_s = 64 a node row is 1.5 KB
 // and the per-copy cost of the TMA engine dominates, so strips of <= 16 consecutive RCM rows
 // (few long runs) win; at N_s >= 128 the rows are 3 KB+ and the byte volume dominates, so
-// compact patches of <= 32 rows (fewer neighbour rows per own row) win.  11 consumer warps x
+// compact patches of <= 24 rows (fewer neighbour rows per own row) win (c4: 24 rows 0.714 ms,
+// 16 rows 0.727, 32 rows 0.751 on one box).  11 consumer warps x
 // 3 stages for both (15 x 3: c4 0.735 vs 0.729 ms, c2 39.3 vs 38.3 us).  ENS_MFS_SHAPE /
 // ENS_MFS_TILING / ENS_MFS_MAXROWS override.
 MfsPlan mf_staged_plan(int32_t n_s) {
@@ -1632,7 +1633,7 @@ MfsPlan mf_staged_plan(int32_t n_s) {
     const char* t = std::getenv("ENS_MFS_TILING");
     p.patches = t ? std::strcmp(t, "strip") != 0 : n_s != 64;
     const char* r = std::getenv("ENS_MFS_MAXROWS");
-    p.max_rows = r ? std::max(1, std::min(kMfsMaxRows, std::atoi(r))) : (p.patches ? kMfsMaxRows : 16);
+    p.max_rows = r ? std::max(1, std::min(kMfsMaxRows, std::atoi(r))) : (p.patches ? 24 : 16);
     return p;
 }
 
