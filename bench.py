@@ -550,9 +550,11 @@ def main(argv=None):
         for a in alts.values():
             if "achieved_fp64_TFLOPs" in a:
                 a["fp64_frac"] = a["achieved_fp64_TFLOPs"] / fp64_peak
-    cpu = None
+    cpu = cpu_c2 = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = _cpu_baseline(base)
+        if args.config != "c2" and not args.no_alternatives:     # c2 and c4
+            cpu_c2 = _cpu_baseline(configs.make("c2"))
 
     if rank == 0:
         kfn = item["kernel_fn"]
@@ -570,6 +572,7 @@ def main(argv=None):
                          "frac": item["frac"], "traffic": _traffic(args.config, kfn, n_s) if world == 1 else None,
                          "peak_source": peak_src, "kernel": kfn,
                          "algorithmic_bytes_per_launch": head_info["bytes_per_step"],
+                         "frac_of_nominal_8TBs": item["achieved_GBs"] / 8000.0,
                          "read_stream_GBs": read_gbs,
                          "frac_of_read_stream": item["achieved_GBs"] / read_gbs if read_gbs else None,
                          "fp64": {"achieved_TFLOPs": item["achieved_fp64_TFLOPs"], "peak_TFLOPs": fp64_peak,
@@ -577,6 +580,7 @@ def main(argv=None):
                                   "frac": item["achieved_fp64_TFLOPs"] / fp64_peak if fp64_peak else None}},
             "cpu_baseline": cpu,
             "alternatives": alts,
+            "cpu_baseline_c2": cpu_c2,
             "e2e": {"value": e2e_units / e2e_el, "unit": "DOF-updates/s", **e2e_meta},
             "gpu_launches": launches,
             "clocks": clk.summary(),
