@@ -132,6 +132,12 @@ typedef struct {
                                TILES.  Asking for a path that does not apply to the context
                                (STAGED: N_s % 64 != 0; WARP: N_s % 64 != 0 or damping == IDENTITY)
                                returns ENS_E_UNSUPPORTED.  Ignored by the assembled kernels. */
+    int32_t persistent;     /* dist == NODE, halo == P2P, kernel ASSEMBLED or ASSEMBLED_SYM, no
+                               re-assembly: 1 = ens_step(n) advances every part held here by n
+                               steps in ONE persistent cooperative kernel (grid-wide barrier per
+                               step, the neighbours' step flags waited for and published inside:
+                               SURVEY.md §8(f) N2) instead of CUDA graphs of per-step launches.
+                               Other combinations: ENS_E_UNSUPPORTED. */
 } ens_options;
 
 /* Matrix-free data paths (ens_options.mf_variant, ens_info.mf_variant).  All three compute

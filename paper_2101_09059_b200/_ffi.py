@@ -37,7 +37,8 @@ class EnsOptions(C.Structure):
                 ("rank", C.c_int32), ("world", C.c_int32), ("nccl_comm", C.c_void_p),
                 ("stream", C.c_void_p), ("dev_alloc", DEV_ALLOC), ("dev_free", DEV_FREE),
                 ("alloc_user", C.c_void_p), ("device", C.c_int32), ("reassemble_every", C.c_int32),
-                ("halo", C.c_int32), ("p2p_procs", C.c_int32), ("mf_variant", C.c_int32)]
+                ("halo", C.c_int32), ("p2p_procs", C.c_int32), ("mf_variant", C.c_int32),
+                ("persistent", C.c_int32)]
 
 
 class EnsInfo(C.Structure):

@@ -145,6 +145,10 @@ struct ens_ctx {
     double* d_G = nullptr;                  // [F][45]
     int32_t* d_etri = nullptr;              // [F][3] RCM ids
 
+    bool persistent = false;                // N2: one persistent kernel per ens_step (ens_options.persistent)
+    ens::StepArgs* d_pparts = nullptr;      // its per-part arguments (rebuilt when the graphs would be)
+    int64_t* d_pitems = nullptr;            // [parts + 1] prefix of (row, group) items
+    unsigned int* d_pbar = nullptr;         // grid-barrier state [2]
     int32_t graph_steps = 64;               // CUDA graph of this many steps (single part, no halo)
     // one graph per parity of the step it starts at: the NCCL / device-copy halos receive
     // into buffer (step + 1) & 1, fixed in the captured nodes (the kernels read the step
@@ -290,6 +294,10 @@ int check_opts(const ens_options* opt) {
                     "reassemble_every needs an assembled kernel (per-realisation geometry breaks the shared K^_e)");
     if (opt->halo < 0 || opt->halo > 1) return fail(nullptr, ENS_E_ARG, "opt->halo must be 0 (NCCL) or 1 (P2P)");
     if (opt->mf_variant < 0 || opt->mf_variant > 3) return fail(nullptr, ENS_E_ARG, "opt->mf_variant must be 0..3 (ENS_MF_*)");
+    if (opt->persistent && (opt->dist != ENS_DIST_NODE || opt->halo != ENS_HALO_P2P ||
+                            opt->kernel == ENS_KERNEL_MATRIX_FREE || opt->reassemble_every > 0))
+        return fail(nullptr, ENS_E_UNSUPPORTED,
+                    "opt->persistent needs dist = NODE, halo = P2P, an assembled kernel and no re-assembly");
     if (opt->p2p_procs && (opt->halo != ENS_HALO_P2P || opt->dist != ENS_DIST_NODE))
         return fail(nullptr, ENS_E_ARG, "opt->p2p_procs needs dist = NODE and halo = P2P");
     if (opt->halo == ENS_HALO_P2P && opt->nccl_comm)
@@ -320,6 +328,7 @@ int init_ctx(ens_ctx* c, const ens_options* opt) {
     c->rank = opt->rank;
     c->world = opt->world > 0 ? opt->world : 1;
     c->reassemble_every = opt->reassemble_every;
+    c->persistent = opt->persistent != 0;
     c->nccl_comm = opt->dist == ENS_DIST_NODE ? opt->nccl_comm : nullptr;
     c->halo = opt->dist == ENS_DIST_NODE ? opt->halo : ENS_HALO_NCCL;
     c->multi = c->nccl_comm != nullptr || (c->halo == ENS_HALO_P2P && opt->p2p_procs != 0 && c->world > 1);
@@ -1628,6 +1637,46 @@ int ens_observe_wait(ens_ctx* c, int64_t* step) {
     return ENS_OK;
 }
 
+// N2 (ens_options.persistent): the per-part arguments of the persistent kernel, rebuilt after
+// any change that would rebuild the CUDA graphs (traction shape, load table, state)
+static int step_persistent(ens_ctx* c, int64_t n) {
+    if (!c->d_pparts || c->graph_dirty) {
+        std::vector<ens::StepArgs> args;
+        std::vector<int64_t> items(1, 0);
+        for (Part& p : c->parts) {
+            ens::StepArgs a = part_args(c, p);
+            a.row0 = 0;
+            a.V = p.n_own;
+            a.fwd_ptr = p.d_fwd_ptr;
+            a.fwd_dst = p.d_fwd_dst;
+            a.peer_buf = p.d_peer_buf;
+            a.hw_flags = p.d_hflags;          // one part per process: its neighbours' flags
+            a.hw_in_q = p.d_in_q;
+            a.hw_n_in = p.n_in;
+            a.hw_out = p.d_out_flag;
+            a.hw_n_out = p.n_out;
+            a.hw_err = c->d_herr;
+            args.push_back(a);
+            items.push_back(items.back() + p.n_own * (c->n_s / ens::pick_vec(c->n_s)));
+        }
+        dfree(c, c->d_pparts);
+        dfree(c, c->d_pitems);
+        RC_TRY(upload(c, &c->d_pparts, args.data(), args.size()));
+        RC_TRY(upload(c, &c->d_pitems, items.data(), items.size()));
+        if (!c->d_pbar) {
+            RC_TRY(dalloc(c, &c->d_pbar, 2));
+            CUDA_TRY(c, cudaMemsetAsync(c->d_pbar, 0, 2 * sizeof(unsigned int), c->stream));
+        }
+        c->graph_dirty = false;
+    }
+    CUDA_TRY(c, ens::launch_steps_persistent(c->d_pparts, c->d_pitems, int32_t(c->parts.size()), c->n_s,
+                                             c->kernel == ENS_KERNEL_ASSEMBLED_SYM, n, c->d_pbar, c->multi ? 1 : 0,
+                                             c->stream));
+    CUDA_TRY(c, ens::launch_advance(c->d_step, n, c->stream));
+    c->step += n;
+    return ENS_OK;
+}
+
 int ens_step(ens_ctx* c, int64_t n) {
     if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
     if (n < 0) return fail(c, ENS_E_ARG, "n must be >= 0");
@@ -1637,6 +1686,7 @@ int ens_step(ens_ctx* c, int64_t n) {
         CUDA_TRY(c, ens::launch_seed_coeffs(part_args(c, c->parts[0]), c->stream));
         c->coef_dirty = false;
     }
+    if (c->persistent && n > 0) return step_persistent(c, n);
     int64_t left = n;
     if (c->use_graphs() && n >= c->graph_steps) {
         if (c->graph_dirty) drop_graph(c);
@@ -2043,7 +2093,7 @@ int ens_query(const ens_ctx* c, ens_info* info) {
     info->step = c->step;
     info->device_bytes = c->device_bytes;
     info->rcm_bandwidth = c->bandwidth;
-    info->graph_steps = c->use_graphs() ? c->graph_steps : 0;
+    info->graph_steps = (c->use_graphs() && !c->persistent) ? c->graph_steps : 0;
     info->reassemble_every = c->reassemble_every;
     info->halo = c->halo;
     info->mf_variant = c->kernel == ENS_KERNEL_MATRIX_FREE ? c->mf_variant : 0;
@@ -2064,6 +2114,7 @@ int ens_query(const ens_ctx* c, ens_info* info) {
         halo += int64_t(p.plan.send_rows.size());
         for (const auto& pe : p.plan.peers) halo += pe.recv_n;
         if (!c->has_halo()) launches += 1;
+        else if (c->persistent) launches = 1;             // one launch per ens_step call
         else if (c->p2p() && halo_fused(c) && (p.plan.b_lo > 0 || p.plan.b_hi > 0))
             launches += 1 + (p.plan.b_lo > 0) + (p.plan.b_hi > 0);
         else if (c->p2p()) launches += 1 + (p.n_in > 0) + (p.plan.b_lo > 0) + (p.plan.b_hi > 0) + (p.n_out > 0);

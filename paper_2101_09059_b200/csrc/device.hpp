@@ -157,6 +157,12 @@ int mf_inc_bytes();        // matrix-free: shared-memory bytes per incidence (K^
 cudaError_t launch_seed_coeffs(const StepArgs& a, cudaStream_t st);
 // FP64 FMA throughput of this device (TFLOP/s, best of 5 timed launches)
 cudaError_t measure_fp64_fma(double* tflops);
+// N2: n steps of every part in `parts` (device array of P StepArgs, items[P + 1] prefix of
+// their (row, realisation group) counts) as one cooperative persistent launch of the a1
+// (sym = false) or a1s kernel rows; flags != 0: one part per process, neighbour step flags
+// waited for / published inside (parts[0].hw_*).  bar: [2] zeroed grid-barrier state.
+cudaError_t launch_steps_persistent(const StepArgs* parts, const int64_t* items, int32_t P, int32_t n_s, bool sym,
+                                    int64_t n, unsigned int* bar, int32_t flags, cudaStream_t st);
 // *step_base += n (after n steps were enqueued)
 cudaError_t launch_advance(int64_t* step_base, int64_t n, cudaStream_t st);
 

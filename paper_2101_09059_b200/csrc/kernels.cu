@@ -1272,6 +1272,74 @@ k_step_mf_staged(const StepArgs a) {
     }
 }
 
+// ---- N2: the P2P-partitioned step loop as one persistent kernel --------------------------
+// Every part of the context (all of them in the one-GPU emulation, the process's own part
+// with CUDA IPC) is advanced n steps by ONE cooperative launch: per step the threads walk the
+// (row, realisation group) items of all parts (a1 / a1s rows, u_{n+1} of send rows forwarded
+// into the neighbours' ghost rows), block 0 evaluates the next step's load coefficients, and a
+// grid-wide barrier ends the step.  With one part per process the neighbours' step flags are
+// waited for at the start of a step and published after the barrier (the same release /
+// acquire protocol as k_halo_*), inside the kernel.  No per-step launch at all.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int gen;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            bar[0] = 0u;
+            __threadfence();
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(bar + 1) : "memory");
+        } else {
+            unsigned int g2 = gen;
+            while (g2 == gen) {
+                __nanosleep(32);
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g2) : "l"(bar + 1) : "memory");
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int VEC, bool SYM>
+__global__ void __launch_bounds__(kThreads)
+k_steps_persistent(const StepArgs* __restrict__ parts, const int64_t* __restrict__ items, int32_t P, int64_t n_steps,
+                   unsigned int* bar, int32_t flags) {
+    const int64_t total = items[P];
+    const int G = parts[0].n_s / VEC;
+    const int64_t step0 = *parts[0].step_base;
+    for (int64_t k = 0; k < n_steps; ++k) {
+        const int64_t step = step0 + k;
+        if (flags) {                                  // one part per process: the neighbours' ghosts
+            if (threadIdx.x == 0) halo_wait_one(parts[0], step);
+            __syncthreads();
+        }
+        int p = 0;
+        for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < total;
+             g += int64_t(gridDim.x) * blockDim.x) {
+            while (g >= items[p + 1]) ++p;
+            const StepArgs& a = parts[p];
+            StepCtx sc;
+            sc.step = step;
+            sc.un = (step & 1) ? a.ubuf1 : a.ubuf0;
+            sc.uo = (step & 1) ? a.ubuf0 : a.ubuf1;
+            const double* coef = a.coef_buf + (step & 1) * kMaxFields;
+            if constexpr (SYM) a1s_row<VEC, false, 3>(a, sc, coef, g - items[p], G);
+            else a1_row<VEC, false>(a, sc, coef, g - items[p], G);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0)      // the next step's load coefficients
+            load_coeffs(parts[0], double(step + 1) * parts[0].dt, parts[0].coef_buf + ((step + 1) & 1) * kMaxFields);
+        grid_barrier(bar);
+        if (flags && blockIdx.x == 0 && threadIdx.x == 0) {
+            const unsigned long long v = (unsigned long long)(step + 1);
+            asm volatile("fence.sc.sys;" ::: "memory");
+            for (int q = 0; q < parts[0].hw_n_out; ++q)
+                asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(parts[0].hw_out[q]), "l"(v) : "memory");
+        }
+    }
+}
+
 __global__ void k_advance(int64_t* step_base, int64_t n) { *step_base += n; }
 
 // FP64 FMA throughput probe (the ALU roofline of the matrix-free step):
@@ -1721,6 +1789,30 @@ cudaError_t measure_fp64_fma(double* tflops) {
     if (e != cudaSuccess) return e;
     *tflops = 2.0 * 8.0 * iters * double(blocks) * 256.0 / (double(best) * 1e-3) / 1e12;
     return cudaSuccess;
+}
+
+template <int VEC, bool SYM>
+static cudaError_t launch_persistent_t(const StepArgs* parts, const int64_t* items, int32_t P, int64_t n,
+                                       unsigned int* bar, int32_t flags, cudaStream_t st) {
+    int dev = 0, sms = 148, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_steps_persistent<VEC, SYM>, kThreads, 0);
+    if (e != cudaSuccess) return e;
+    dim3 grid(unsigned(std::max(1, per_sm) * sms)), block(kThreads);
+    void* args[] = {(void*)&parts, (void*)&items, (void*)&P, (void*)&n, (void*)&bar, (void*)&flags};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_steps_persistent<VEC, SYM>), grid, block, args,
+                                       0, st);
+}
+
+cudaError_t launch_steps_persistent(const StepArgs* parts, const int64_t* items, int32_t P, int32_t n_s, bool sym,
+                                    int64_t n, unsigned int* bar, int32_t flags, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    if (pick_vec(n_s) == 2)
+        return sym ? launch_persistent_t<2, true>(parts, items, P, n, bar, flags, st)
+                   : launch_persistent_t<2, false>(parts, items, P, n, bar, flags, st);
+    return sym ? launch_persistent_t<1, true>(parts, items, P, n, bar, flags, st)
+               : launch_persistent_t<1, false>(parts, items, P, n, bar, flags, st);
 }
 
 cudaError_t launch_seed_coeffs(const StepArgs& a, cudaStream_t st) {

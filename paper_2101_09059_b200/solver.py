@@ -64,13 +64,15 @@ class Ensemble:
                  cfl_safety=0.9, c_d=0.0, damping="none", kernel="assembled", dist="single",
                  s_begin=0, rank=0, world=1, nccl_comm=None, device=None, stream=None,
                  torch_alloc=True, reassemble_every=0, halo="nccl", p2p_procs=False, group=None,
-                 mf_variant="auto", _ctx=None):
+                 mf_variant="auto", persistent=False, _ctx=None):
         """dist="node" splits the RCM rows into `world` parts.  halo="nccl": NCCL
         send/recv with nccl_comm (one part per process) or, without it, device copies
         between all parts held here.  halo="p2p": device-initiated stores into the
         neighbours' ghost rows; p2p_procs=True => one part per process, connected to the
         other ranks of `group` (torch.distributed, default group) through CUDA IPC.
-        mf_variant ("auto", "tiles", "warp", "staged"): the matrix-free data path (ens.h)."""
+        mf_variant ("auto", "tiles", "warp", "staged"): the matrix-free data path (ens.h).
+        persistent=True (node partition, P2P halo, assembled kernels): one persistent kernel per
+        ens_step call instead of per-step launches (ens.h ens_options.persistent)."""
         self._ctx = None
         self._alloc = None
         self._p2p_group, self._p2p_multi = None, False
@@ -91,6 +93,7 @@ class Ensemble:
         opt.halo = HALO[halo]
         opt.p2p_procs = int(bool(p2p_procs))
         opt.mf_variant = MF_VARIANT[mf_variant]
+        opt.persistent = int(bool(persistent))
         ctx = C.c_void_p()
         check(lib().ens_create(C.byref(mesh), C.byref(mat), C.byref(opt), C.byref(ctx)))
         self._ctx = ctx

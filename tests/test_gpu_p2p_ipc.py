@@ -25,7 +25,7 @@ def _problem():
     return m, E, h, tr, kw
 
 
-def _rank_main(rank, world, port, outdir):
+def _rank_main(rank, world, port, outdir, persistent=False, steps=STEPS):
     import torch
     import torch.distributed as dist
     from paper_2101_09059_b200 import solver
@@ -33,9 +33,9 @@ def _rank_main(rank, world, port, outdir):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     m, E, h, tr, kw = _problem()
     ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, dist="node", world=world, rank=rank, halo="p2p",
-                          p2p_procs=True, **kw)
+                          p2p_procs=True, persistent=persistent, **kw)
     ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
-    ens.step(STEPS)
+    ens.step(steps)
     u, um, _, st = ens.get_state()
     np.savez(os.path.join(outdir, f"r{rank}.npz"), u=u, um=um, ids=ens.owned(), step=st,
              launches=ens.info()["launches_per_step"])
@@ -45,24 +45,29 @@ def _rank_main(rank, world, port, outdir):
 
 
 @pytest.mark.timeout(600)
-def test_p2p_two_processes_bitexact(tmp_path):
+@pytest.mark.parametrize("persistent", [False, True])
+def test_p2p_two_processes_bitexact(tmp_path, persistent):
+    """persistent=True: each rank advances its part in ONE cooperative kernel per ens_step
+    (N2), waiting for / publishing the step flags inside it; the two kernels share the one
+    GPU by time slicing here (a few steps only), across NVLink on a multi-GPU box."""
     import torch.multiprocessing as mp
     from paper_2101_09059_b200 import solver
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     world = 2
-    mp.start_processes(_rank_main, args=(world, port, str(tmp_path)), nprocs=world, join=True,
+    steps = 12 if persistent else STEPS
+    mp.start_processes(_rank_main, args=(world, port, str(tmp_path), persistent, steps), nprocs=world, join=True,
                        start_method="spawn")
     m, E, h, tr, kw = _problem()
     ref = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, **kw)
     ref.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
-    ref.step(STEPS)
+    ref.step(steps)
     u, um, _, st = ref.get_state()
     seen = np.zeros(m.n_nodes, bool)
     for r in range(world):
         d = np.load(tmp_path / f"r{r}.npz")
-        assert int(d["step"]) == st == STEPS
+        assert int(d["step"]) == st == steps
         ids = d["ids"]
         assert np.array_equal(d["u"], u[:, ids]) and np.array_equal(d["um"], um[:, ids])
         seen[ids] = True

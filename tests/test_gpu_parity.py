@@ -287,6 +287,46 @@ def test_node_partition_bitexact(kernel, P, halo):
     ref.close(); par.close()
 
 
+@pytest.mark.parametrize("kernel", ["assembled", "assembled_sym"])
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_node_partition_persistent_bitexact(kernel, P):
+    """N2 (ens_options.persistent): all P parts advanced by one persistent cooperative kernel
+    per ens_step (grid-wide barrier per step, u_{n+1} of send rows stored into the neighbours'
+    ghost rows): bit-identical to the unpartitioned run, across calls, a checkpoint restart
+    and a traction change."""
+    m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(24, 60), 0.01, 3), 2)
+    E, h = _mats(m, 6, 61)
+    tr = loads.pulsatile(m.xyz, m.tris, period=0.01, systole=0.004, ramp_T=0.003)
+    kw = dict(rho=RHO, nu=NU, k_shear=KS, kernel=kernel, dt=5e-5, damping="identity", c_d=0.3)
+    ref = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, **kw)
+    par = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, dist="node", world=P, halo="p2p", persistent=True, **kw)
+    assert par.info()["launches_per_step"] == 1 and par.info()["graph_steps"] == 0
+    for e in (ref, par):
+        e.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+        e.step(257)
+        e.step(3)
+    u0, p0, _, s0 = ref.get_state()
+    u1, p1, _, s1 = par.get_state()
+    assert s0 == s1 == 260 and np.array_equal(u0, u1) and np.array_equal(p0, p1)
+    par.set_state(u0, p0, s0)
+    F2 = np.concatenate([tr.F, 0.5 * tr.F])
+    for e in (ref, par):
+        e.set_traction(F2, tr.tab_t, np.concatenate([tr.tab_g, tr.tab_g[::-1]]), tr.period, tr.ramp_T)
+        e.step(50)
+    assert np.array_equal(ref.get_state()[0], par.get_state()[0])
+    ref.close(); par.close()
+
+
+def test_persistent_rejected_elsewhere():
+    m = meshmod.cylinder(12, 23)
+    E, h = _mats(m, 4, 3)
+    for kw in (dict(dist="node", world=2, halo="nccl"), dict(dist="node", world=2, halo="p2p", kernel="matrix_free"),
+               dict(dist="single")):
+        with pytest.raises(EnsError) as ei:
+            solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, persistent=True, **kw)
+        assert ei.value.code == -8                      # ENS_E_UNSUPPORTED
+
+
 def test_symmetric_storage_bitexact_vs_full():
     """ASSEMBLED_SYM stores only blocks (i, j >= i) and reads (j, i)^T for j < i, in the
     full row's column order: bit-identical to ASSEMBLED, with fewer value bytes."""
