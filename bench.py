@@ -416,12 +416,14 @@ def main(argv=None):
         head.close()
         if args.emulate_partition > 1:
             node_emul = {"emulated_parts": args.emulate_partition}
-            for halo in ("nccl", "p2p"):
+            variants = ["nccl", "p2p"] + (["p2p_persistent"] if args.kernel != "matrix_free" else [])
+            for halo in variants:
                 try:
                     ens = solver.Ensemble(m.xyz, m.tris, m.fixed, base.E, base.h, rho=base.rho, nu=base.nu,
                                           k_shear=base.k_shear, damping=base.damping, c_d=base.c_d,
                                           kernel=args.kernel, dist="node", world=args.emulate_partition,
-                                          halo=halo, device=local)
+                                          halo=halo.split("_")[0], persistent=halo.endswith("persistent"),
+                                          device=local)
                     r = Run.__new__(Run)
                     r.cfg, r.kernel, r.ens = base, args.kernel, ens
                     tr = base.traction
