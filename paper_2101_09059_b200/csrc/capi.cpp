@@ -58,6 +58,7 @@ struct Part {
     double *d_Krow = nullptr, *d_alpha = nullptr;
     int32_t mf_rows = 1, mf_groups = 1, mf_smem_inc = 0;
     std::vector<MfTileSet> mfs;                            // matrix-free F3 tiles, per launched row range
+    int64_t n_alpha = 0;                                   // alpha rows (elements touching the owned rows)
     int32_t *d_sym_lptr = nullptr, *d_sym_lidx = nullptr, *d_sym_lcol = nullptr, *d_sym_scol = nullptr;
     int2* d_sym_urange = nullptr;
     int64_t n_stored = 0;                                  // value blocks held (assembled kernels)
@@ -408,6 +409,8 @@ cudaError_t launch_rows(const ens_ctx* c, const Part& p, ens::StepArgs a, int64_
         a.mfs_ntiles = ts->ntiles;
         a.mfs_stage_bytes = ts->stage_bytes;
         a.mfs_shape = c->mfs_plan.shape;
+        a.mfs_slices = c->mfs_plan.sliced ? c->n_s / 64 : 1;
+        a.mfs_alpha_rows = p.n_alpha;
     }
     switch (c->kernel) {
         case ENS_KERNEL_MATRIX_FREE: return ens::launch_step_matrix_free(a, st);
@@ -757,7 +760,8 @@ int build_mf_tiles(ens_ctx* c, const std::vector<int32_t>& ip, const std::vector
                    const std::vector<double>& k18, const std::vector<uint8_t>& fx,
                    std::vector<std::vector<int32_t>> patches, int64_t row0, int64_t rows, MfTileSet& out) {
     const ens::MfsShape sh = ens::mf_staged_shape(c->mfs_plan.shape);
-    const size_t US = size_t(c->n_s) * 24, AS = size_t(c->n_s) * 8;
+    const size_t W = c->mfs_plan.sliced ? 64 : size_t(c->n_s);       // realisations per stage row
+    const size_t US = W * 24, AS = W * 8;
     std::vector<ens::MfTile> tiles;
     std::vector<int4> entries;
     std::vector<unsigned char> blob;
@@ -1074,7 +1078,8 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
         std::vector<std::vector<std::vector<int32_t>>> patches;     // F3: per launched range
         if (c->mf_variant == ENS_MF_STAGED) {
             const ens::MfsShape sh = ens::mf_staged_shape(c->mfs_plan.shape);
-            const size_t US = size_t(n_s) * 24, AS = size_t(n_s) * 8;
+            const size_t W = c->mfs_plan.sliced ? 64 : size_t(n_s);
+            const size_t US = W * 24, AS = W * 8;
             for (const auto& tl : tilings)
                 patches.push_back(tl.second > tl.first
                                       ? mf_patches(ip, rec, n_loc, tl.first, tl.second - tl.first, US, AS, size_t(sh.stage_bytes), c->mfs_plan)
@@ -1142,6 +1147,7 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
             RC_TRY(upload(c, &P.d_Krow, fans.Krow.data() + size_t(k0) * 28, size_t(k1 - k0) * 28));
         }
         RC_TRY(upload(c, &P.d_alpha, al.data(), al.size()));
+        P.n_alpha = Fl;
     }
     const size_t ns = size_t(n_loc) * 3 * size_t(n_s);
     if (c->multi && c->p2p()) {      // exported to the neighbours: plain cudaMalloc (IPC)
@@ -1312,7 +1318,8 @@ int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, cons
             // records, F_k): at large N_s a high-degree node may not; AUTO then falls back to
             // TILES, an explicit STAGED request fails
             const ens::MfsShape sh = ens::mf_staged_shape(c->mfs_plan.shape);
-            const size_t US = size_t(c->n_s) * 24, AS = size_t(c->n_s) * 8;
+            const size_t W = c->mfs_plan.sliced ? 64 : size_t(c->n_s);
+            const size_t US = W * 24, AS = W * 8;
             size_t worst = 0;
             std::vector<int32_t> nb;
             for (int64_t i = 0; i < V; ++i) {

@@ -1008,10 +1008,21 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
 }
 
-// NS: N_s at compile time (64) or 0 (runtime); C23: per-row c2, c3 arrays (identity damping)
-template <bool APPLY, int CW, int S, int NS, bool C23>
+// Sliced stages (SL, N_s >= 256): a stage holds one 64-realisation slice of a tile's rows
+// ([3][64] per node, like N_s = 64), the work items are (tile, slice) pairs, and the u_n and
+// alpha runs move as 2-D tensor copies (cp.async.bulk.tensor.2d) of [3 x count][64] and
+// [count][64] boxes out of the row-major arrays: boxes of 2^k rows (k = 0..5), a run of any
+// length being issued as its binary decomposition.
+struct MfsMaps {
+    CUtensorMap u[2][6];      // u buffer b viewed as [rows * 3][N_s], box [3 * 2^k][64]
+    CUtensorMap al[6];        // alpha [F][N_s], box [2^k][64]
+};
+
+// NS: N_s at compile time (64) or 0 (runtime); C23: per-row c2, c3 arrays (identity damping);
+// SL: sliced stages (above)
+template <bool APPLY, int CW, int S, int NS, bool C23, bool SL>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
-k_step_mf_staged(const StepArgs a) {
+k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t SB = uint32_t(a.mfs_stage_bytes);
     const uint32_t smem_s = uint32_t(__cvta_generic_to_shared(smem));
@@ -1033,8 +1044,10 @@ k_step_mf_staged(const StepArgs a) {
     // one front of ~gridDim.x consecutive tiles, so a node row loaded by one tile is still in
     // L2 when the tiles one ring later need it (contiguous per-CTA chunks spread the front
     // over the whole mesh: c4 moved 1.43x its algorithmic DRAM bytes that way)
-    const int32_t ta = int32_t(blockIdx.x), tb = nt, tstep = int32_t(gridDim.x);
-    const uint32_t US = uint32_t(n_s) * 24u, AS = uint32_t(n_s) * 8u;
+    // work items: tiles, or (tile, slice) pairs with SL (item = tile * HS + slice)
+    const int HS = SL ? (n_s >> 6) : 1;
+    const int32_t ta = int32_t(blockIdx.x), tb = nt * HS, tstep = int32_t(gridDim.x);
+    const uint32_t US = SL ? 1536u : uint32_t(n_s) * 24u, AS = SL ? 512u : uint32_t(n_s) * 8u;   // stage rows
 
     if (wid == CW) {                                          // ---- producer warp
         // Each lane issues copy entries lane, lane + 32, lane + 64 of the tile.  The entries
@@ -1053,12 +1066,13 @@ k_step_mf_staged(const StepArgs a) {
                                                      : make_int4(-1, 0, 0, 0);
         };
         if (ta < tb) {
-            dn = a.mfs_tiles[ta];
+            dn = a.mfs_tiles[ta / HS];
             load_entries();
         }
-        if (ta + tstep < tb) dn2 = a.mfs_tiles[ta + tstep];
+        if (ta + tstep < tb) dn2 = a.mfs_tiles[(ta + tstep) / HS];
         for (int32_t t = ta; t < tb; t += tstep) {
             const int it = int((t - ta) / tstep), s = it % S;
+            const int sl = SL ? t % HS : 0;                   // realisation slice of the item
             const uint32_t full = bar0 + 8u * s, stage = smem_s + uint32_t(s) * SB;
             const MfTile d = dn;
             int4 e[EPL];
@@ -1067,7 +1081,7 @@ k_step_mf_staged(const StepArgs a) {
             if (t + tstep < tb) {
                 dn = dn2;
                 load_entries();
-                if (t + 2 * tstep < tb) dn2 = a.mfs_tiles[t + 2 * tstep];
+                if (t + 2 * tstep < tb) dn2 = a.mfs_tiles[(t + 2 * tstep) / HS];
             }
             if (it >= S) mbar_wait(bar0 + 8u * (S + s), uint32_t(it / S - 1) & 1u);
             if (lane == 0) mbar_expect_tx(full, uint32_t(d.stage_bytes) + uint32_t(nf * d.nrows) * 32u);
@@ -1078,6 +1092,24 @@ k_step_mf_staged(const StepArgs a) {
             for (int q = 0; q < EPL; ++q) {
                 const int4 x = e[q];
                 if (x.x < 0 || x.x == kMfsF) continue;
+                if (SL && x.x != kMfsBlob) {                  // 2-D boxes of 2^k rows, slice sl
+                    const bool isu = x.x == kMfsU;
+                    const int b = int(sc.step & 1);
+                    int32_t first = x.y, cnt = x.z;
+                    uint32_t dst = stage + uint32_t(x.w);
+                    while (cnt > 0) {
+                        const int k = min(5, 31 - __clz(cnt));
+                        const CUtensorMap* m = isu ? &maps.u[b][k] : &maps.al[k];
+                        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                                     " [%0], [%1, {%2, %3}], [%4];"
+                                     :: "r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(sl * 64),
+                                        "r"(isu ? first * 3 : first), "r"(full) : "memory");
+                        first += 1 << k;
+                        cnt -= 1 << k;
+                        dst += (isu ? US : AS) << k;
+                    }
+                    continue;
+                }
                 const unsigned char* src =
                     x.x == kMfsU ? reinterpret_cast<const unsigned char*>(sc.un) + int64_t(x.y) * US
                     : x.x == kMfsA ? reinterpret_cast<const unsigned char*>(a.alpha) + int64_t(x.y) * AS
@@ -1098,7 +1130,7 @@ k_step_mf_staged(const StepArgs a) {
 
     // ---- consumer warps.  Units = (row, 64-realisation slice) pairs, H = N_s / 64 per row,
     // numbered consecutively over this CTA's tiles; warp wid takes units wid, wid + CW, ...
-    const int H = n_s >> 6;
+    const int H = SL ? 1 : (n_s >> 6);                       // units per row
     auto ld2 = [&](const unsigned char* p) {
         const double2 v = *reinterpret_cast<const double2*>(p);
         Vec<2> r;
@@ -1133,6 +1165,7 @@ k_step_mf_staged(const StepArgs a) {
     int32_t ubase = 0;                                        // units of the tiles before this one
     for (int32_t t = ta; t < tb; t += tstep) {
         const int it = int((t - ta) / tstep), s = it % S;
+        const int sl = SL ? t % HS : 0;
         const unsigned char* st = smem + size_t(s) * SB;
         mbar_wait(bar0 + 8u * s, uint32_t(it / S) & 1u);
         const int4 hdr = *reinterpret_cast<const int4*>(st);  // {nrows, u image, row offsets, F_k}
@@ -1145,8 +1178,8 @@ k_step_mf_staged(const StepArgs a) {
             int wr = uu, h = 0;                               // uu = wr * H + h
             if (H > 1) { wr = uu / H; h = uu - wr * H; }
             const int64_t i = rowid[wr];
-            const int s0 = h * 64 + 2 * lane;                 // this lane's realisations s0, s0 + 1
-            const uint32_t lofs = uint32_t(s0) * 8u;
+            const int s0 = (sl + h) * 64 + 2 * lane;          // this lane's realisations s0, s0 + 1
+            const uint32_t lofs = uint32_t(h * 64 + 2 * lane) * 8u;   // their offset in a stage row
             const int32_t* roff = reinterpret_cast<const int32_t*>(st + hdr.z);
             const int32_t ro = roff[wr];                      // incidence offset | fixed bits << 24
             const int32_t kb = ro & 0xffffff, ke = roff[wr + 1] & 0xffffff;
@@ -1696,10 +1729,12 @@ static constexpr int kMfsSmemMax = 227 * 1024;
 // ENS_MFS_TILING / ENS_MFS_MAXROWS override.
 MfsPlan mf_staged_plan(int32_t n_s) {
     MfsPlan p;
+    const char* sv = std::getenv("ENS_MFS_SLICED");
+    p.sliced = sv ? std::atoi(sv) != 0 && n_s > 64 : n_s >= 256;   // N_s >= 256: a node row (6 KB+) is too big
     const int env = mfs_env_shape();
     p.shape = env >= 0 ? env : 0;                       // 11x3 (kMfsShapes)
     const char* t = std::getenv("ENS_MFS_TILING");
-    p.patches = t ? std::strcmp(t, "strip") != 0 : n_s != 64;
+    p.patches = t ? std::strcmp(t, "strip") != 0 : (n_s != 64 && !p.sliced);   // 64-wide stage rows: strips
     const char* r = std::getenv("ENS_MFS_MAXROWS");
     p.max_rows = r ? std::max(1, std::min(kMfsMaxRows, std::atoi(r))) : (p.patches ? 24 : 16);
     return p;
@@ -1713,7 +1748,47 @@ MfsShape mf_staged_shape(int shape) {
 
 bool mf_staged_applies(int32_t n_s) { return n_s % 64 == 0; }
 
-template <bool APPLY, int CW, int S, int NS, bool C23>
+// 2-D tensor map of a row-major fp64 array [rows][cols] with a [box_rows][64] box, encoded
+// through the driver entry point (no -lcuda) and cached per (base, rows, cols, box_rows)
+static cudaError_t mfs_map(const double* base, int64_t rows, int64_t cols, int box_rows, CUtensorMap* out) {
+    struct Entry {
+        const double* base;
+        int64_t rows, cols;
+        int box;
+        CUtensorMap map;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Entry& e : cache)
+        if (e.base == base && e.rows == rows && e.cols == cols && e.box == box_rows) {
+            *out = e.map;
+            return cudaSuccess;
+        }
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    Entry en{base, rows, cols, box_rows, {}};
+    const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    const cuuint64_t strides[1] = {cuuint64_t(cols) * sizeof(double)};
+    const cuuint32_t box[2] = {64u, cuuint32_t(box_rows)};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = encode(&en.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    if (cache.size() >= 512) cache.erase(cache.begin());
+    cache.push_back(en);
+    *out = en.map;
+    return cudaSuccess;
+}
+
+template <bool APPLY, int CW, int S, int NS, bool C23, bool SL>
 static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
     if (a.mfs_ntiles == 0) return cudaSuccess;
     const size_t smem = size_t(S) * size_t(a.mfs_stage_bytes) + size_t(2 * S) * 8;
@@ -1723,24 +1798,42 @@ static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
     cudaGetDevice(&dev);
     const uint64_t bit = uint64_t(1) << (dev & 63);
     if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(k_step_mf_staged<APPLY, CW, S, NS, C23>,
+        cudaError_t e = cudaFuncSetAttribute(k_step_mf_staged<APPLY, CW, S, NS, C23, SL>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kMfsSmemMax - 256);
         if (e != cudaSuccess) return e;
         cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
         attr_set.fetch_or(bit, std::memory_order_release);
     }
-    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(sms[dev & 63], a.mfs_ntiles)));
-    k_step_mf_staged<APPLY, CW, S, NS, C23><<<grid, (CW + 1) * 32, smem, st>>>(a);
+    MfsMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    int64_t items = a.mfs_ntiles;
+    if constexpr (SL) {
+        items *= a.n_s / 64;
+        for (int k = 0; k < 6; ++k) {
+            cudaError_t e = mfs_map(a.ubuf0, a.u_rows * 3, a.n_s, 3 << k, &maps.u[0][k]);
+            if (e == cudaSuccess) e = mfs_map(a.ubuf1, a.u_rows * 3, a.n_s, 3 << k, &maps.u[1][k]);
+            if (e == cudaSuccess) e = mfs_map(a.alpha, a.mfs_alpha_rows, a.n_s, 1 << k, &maps.al[k]);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(sms[dev & 63], items)));
+    k_step_mf_staged<APPLY, CW, S, NS, C23, SL><<<grid, (CW + 1) * 32, smem, st>>>(a, maps);
     return cudaGetLastError();
 }
 
-// the hot instance (N_s = 64, scalar c2 / c3) gets N_s at compile time; the others run generic
+// the hot instance (N_s = 64, scalar c2 / c3) gets N_s at compile time; the others run generic;
+// sliced stages (N_s >= 256) are their own instances
 template <int CW, int S>
 static cudaError_t launch_mf_staged_shape(const StepArgs& a, cudaStream_t st) {
-    if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false>(a, st);
-    if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true>(a, st);
-    if (a.n_s == 64) return launch_mf_staged_t<false, CW, S, 64, false>(a, st);
-    return launch_mf_staged_t<false, CW, S, 0, false>(a, st);
+    if (a.mfs_slices > 1) {
+        if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, true>(a, st);
+        if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, true>(a, st);
+        return launch_mf_staged_t<false, CW, S, 0, false, true>(a, st);
+    }
+    if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, false>(a, st);
+    if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, false>(a, st);
+    if (a.n_s == 64) return launch_mf_staged_t<false, CW, S, 64, false, false>(a, st);
+    return launch_mf_staged_t<false, CW, S, 0, false, false>(a, st);
 }
 
 static cudaError_t launch_mf_staged(const StepArgs& a, cudaStream_t st) {

@@ -44,8 +44,9 @@ def _run(m, E, h, variant, damping="mass", c_d=120.0, steps=400, **kw):
     return u, p, y
 
 
-@pytest.mark.parametrize("n_s", [64, 128, 192])
+@pytest.mark.parametrize("n_s", [64, 128, 192, 256, 320])
 def test_variants_bitexact_and_oracle_spmm(n_s):
+    """N_s >= 256 takes STAGED's sliced stages (2-D tensor copies of 64-realisation slices)."""
     """States after 400 pulsatile steps (two load fields: ramp + table) and one product
     y = K x through TILES, WARP and STAGED: bit for bit; STAGED's product against the oracle."""
     m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(24, 60), 0.01, 3), 2)
@@ -86,15 +87,17 @@ def test_staged_nonmanifold_vs_oracle():
     ens.close()
 
 
+@pytest.mark.parametrize("sliced", ["0", "1"])
 @pytest.mark.parametrize("tiling", ["strip", "patch"])
 @pytest.mark.parametrize("n_s", [64, 128])
-def test_staged_tilings_bitexact(n_s, tiling, monkeypatch):
+def test_staged_tilings_bitexact(n_s, tiling, sliced, monkeypatch):
     """Strips of consecutive rows and compact patches (ENS_MFS_TILING, read at create) only
     change which rows share a stage: bit-identical results."""
     m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(24, 60), 0.01, 3), 6)
     E, h = _mats(m, n_s, 9)
     ref = _run(m, E, h, "tiles", steps=150)
     monkeypatch.setenv("ENS_MFS_TILING", tiling)
+    monkeypatch.setenv("ENS_MFS_SLICED", sliced)        # N_s = 128 in 64-realisation slices too
     got = _run(m, E, h, "staged", steps=150)
     for k in range(3):
         assert np.array_equal(ref[k], got[k]), k
@@ -102,7 +105,7 @@ def test_staged_tilings_bitexact(n_s, tiling, monkeypatch):
 
 @pytest.mark.parametrize("halo", ["nccl", "p2p"])
 @pytest.mark.parametrize("P", [2, 3, 8])
-@pytest.mark.parametrize("n_s", [64, 128])
+@pytest.mark.parametrize("n_s", [64, 128, 256])
 def test_staged_node_partition_bitexact(n_s, P, halo):
     """Boundary / interior launches each with their own tile set, ghost rows in the stages,
     P2P forwarding from the update: bit-identical to the single-part run."""
