@@ -409,7 +409,7 @@ cudaError_t launch_rows(const ens_ctx* c, const Part& p, ens::StepArgs a, int64_
         a.mfs_ntiles = ts->ntiles;
         a.mfs_stage_bytes = ts->stage_bytes;
         a.mfs_shape = c->mfs_plan.shape;
-        a.mfs_slices = c->mfs_plan.sliced ? c->n_s / 64 : 1;
+        a.mfs_slices = c->mfs_plan.sliced ? c->n_s / ens::mfs_stage_w(c->mfs_plan, c->n_s) : 1;
         a.mfs_alpha_rows = p.n_alpha;
     }
     switch (c->kernel) {
@@ -760,7 +760,7 @@ int build_mf_tiles(ens_ctx* c, const std::vector<int32_t>& ip, const std::vector
                    const std::vector<double>& k18, const std::vector<uint8_t>& fx,
                    std::vector<std::vector<int32_t>> patches, int64_t row0, int64_t rows, MfTileSet& out) {
     const ens::MfsShape sh = ens::mf_staged_shape(c->mfs_plan.shape);
-    const size_t W = c->mfs_plan.sliced ? 64 : size_t(c->n_s);       // realisations per stage row
+    const size_t W = size_t(ens::mfs_stage_w(c->mfs_plan, c->n_s));   // realisations per stage row
     const size_t US = W * 24, AS = W * 8;
     std::vector<ens::MfTile> tiles;
     std::vector<int4> entries;
@@ -1078,7 +1078,7 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
         std::vector<std::vector<std::vector<int32_t>>> patches;     // F3: per launched range
         if (c->mf_variant == ENS_MF_STAGED) {
             const ens::MfsShape sh = ens::mf_staged_shape(c->mfs_plan.shape);
-            const size_t W = c->mfs_plan.sliced ? 64 : size_t(n_s);
+            const size_t W = size_t(ens::mfs_stage_w(c->mfs_plan, n_s));
             const size_t US = W * 24, AS = W * 8;
             for (const auto& tl : tilings)
                 patches.push_back(tl.second > tl.first
@@ -1318,7 +1318,7 @@ int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, cons
             // records, F_k): at large N_s a high-degree node may not; AUTO then falls back to
             // TILES, an explicit STAGED request fails
             const ens::MfsShape sh = ens::mf_staged_shape(c->mfs_plan.shape);
-            const size_t W = c->mfs_plan.sliced ? 64 : size_t(c->n_s);
+            const size_t W = size_t(ens::mfs_stage_w(c->mfs_plan, c->n_s));
             const size_t US = W * 24, AS = W * 8;
             size_t worst = 0;
             std::vector<int32_t> nb;

@@ -78,7 +78,7 @@ struct StepArgs {
     int32_t mfs_ntiles = 0;
     int32_t mfs_stage_bytes = 0;        // bytes per stage (shared memory = stages * this + barriers)
     int32_t mfs_shape = 0;              // consumer warps x stages (kernels.cu kMfsShapes)
-    int32_t mfs_slices = 1;             // > 1: sliced stages (64 realisations per stage row), N_s / 64
+    int32_t mfs_slices = 1;             // > 1: sliced stages (64 * WS realisations per stage row), N_s / (64 WS)
     int64_t mfs_alpha_rows = 0;         // rows of alpha (the part's elements; tensor maps)
     // update coefficients
     const double* c1 = nullptr;
@@ -151,7 +151,10 @@ bool mf_staged_applies(int32_t n_s);
 struct MfsShape { int consumers, stages, stage_bytes; };
 MfsShape mf_staged_shape(int shape);
 // per-context plan: shape index, tiling (patches or strips of consecutive rows), rows per tile
-struct MfsPlan { int shape = 0; bool patches = false; int max_rows = 16; bool sliced = false; };
+// sliced: a stage row holds one slice of 64 * ws realisations (ws = the shape's slices per unit)
+struct MfsPlan { int shape = 0; bool patches = false; int max_rows = 16; bool sliced = false; int ws = 1; };
+// realisations per stage row: the slice width when sliced, else N_s
+inline int mfs_stage_w(const MfsPlan& p, int32_t n_s) { return p.sliced ? 64 * p.ws : int(n_s); }
 MfsPlan mf_staged_plan(int32_t n_s);
 bool mf_diff();            // matrix-free: neighbours relative to u_i, (prev, next) K^ columns only (ENS_MF_DIFF, default 1)
 int mf_inc_bytes();        // matrix-free: shared-memory bytes per incidence (K^ image + fan record)

@@ -1014,13 +1014,13 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // [count][64] boxes out of the row-major arrays: boxes of 2^k rows (k = 0..5), a run of any
 // length being issued as its binary decomposition.
 struct MfsMaps {
-    CUtensorMap u[2][6];      // u buffer b viewed as [rows * 3][N_s], box [3 * 2^k][64]
-    CUtensorMap al[6];        // alpha [F][N_s], box [2^k][64]
+    CUtensorMap u[2][6];      // u buffer b viewed as [rows * 3][N_s], box [3 * 2^k][64 WS]
+    CUtensorMap al[6];        // alpha [F][N_s], box [2^k][64 WS]
 };
 
 // NS: N_s at compile time (64) or 0 (runtime); C23: per-row c2, c3 arrays (identity damping);
 // SL: sliced stages (above)
-template <bool APPLY, int CW, int S, int NS, bool C23, bool SL>
+template <bool APPLY, int CW, int S, int NS, bool C23, bool SL, int WS>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
 k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1045,9 +1045,9 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
     // L2 when the tiles one ring later need it (contiguous per-CTA chunks spread the front
     // over the whole mesh: c4 moved 1.43x its algorithmic DRAM bytes that way)
     // work items: tiles, or (tile, slice) pairs with SL (item = tile * HS + slice)
-    const int HS = SL ? (n_s >> 6) : 1;
+    const int HS = SL ? (n_s >> 6) / WS : 1;                  // slices of 64 WS realisations
     const int32_t ta = int32_t(blockIdx.x), tb = nt * HS, tstep = int32_t(gridDim.x);
-    const uint32_t US = SL ? 1536u : uint32_t(n_s) * 24u, AS = SL ? 512u : uint32_t(n_s) * 8u;   // stage rows
+    const uint32_t US = SL ? 1536u * WS : uint32_t(n_s) * 24u, AS = SL ? 512u * WS : uint32_t(n_s) * 8u;   // stage rows
 
     if (wid == CW) {                                          // ---- producer warp
         // Each lane issues copy entries lane, lane + 32, lane + 64 of the tile.  The entries
@@ -1102,7 +1102,7 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                         const CUtensorMap* m = isu ? &maps.u[b][k] : &maps.al[k];
                         asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
                                      " [%0], [%1, {%2, %3}], [%4];"
-                                     :: "r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(sl * 64),
+                                     :: "r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(sl * 64 * WS),
                                         "r"(isu ? first * 3 : first), "r"(full) : "memory");
                         first += 1 << k;
                         cnt -= 1 << k;
@@ -1128,9 +1128,13 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
         }
     } else {
 
-    // ---- consumer warps.  Units = (row, 64-realisation slice) pairs, H = N_s / 64 per row,
-    // numbered consecutively over this CTA's tiles; warp wid takes units wid, wid + CW, ...
-    const int H = SL ? 1 : (n_s >> 6);                       // units per row
+    // ---- consumer warps.  Units = (row, WS consecutive 64-realisation slices), H = N_s / (64 WS)
+    // per row, numbered consecutively over this CTA's tiles; warp wid takes units wid, wid + CW, ...
+    // WS = 2 (N_s % 128 == 0): a lane owns realisation pairs 2 lane and 64 + 2 lane of the unit, so
+    // the K^ coefficients, the records and the loop overhead of an incidence serve both slices and
+    // the lane carries 12 independent accumulation chains; the arithmetic of each realisation is
+    // unchanged (bit-identical to WS = 1).
+    const int H = SL ? 1 : (n_s >> 6) / WS;                  // units per row
     auto ld2 = [&](const unsigned char* p) {
         const double2 v = *reinterpret_cast<const double2*>(p);
         Vec<2> r;
@@ -1139,22 +1143,24 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
     };
     // one incidence: y[c] += alpha * (K^[c, prev] . prev + K^[c, next] . next), prev / next
     // relative to u_i, one chain per (c, v) in the order prev_0..2, next_0..2
-    auto incidence = [&](double (&y)[3][2], const Vec<2> (&pv)[3], const Vec<2> (&nx)[3], const Vec<2>& al,
-                         const unsigned char* rp) {
+    auto incidence = [&](double (&y)[WS][3][2], const Vec<2> (&pv)[WS][3], const Vec<2> (&nx)[WS][3],
+                         const Vec<2> (&al)[WS], const unsigned char* rp) {
         const double2* K2 = reinterpret_cast<const double2*>(rp + 16);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             // K[6c .. 6c + 5] = (prev_0, prev_1, prev_2, next_0, next_1, next_2): 16-B aligned pairs
             const double2 k01 = K2[3 * c], k23 = K2[3 * c + 1], k45 = K2[3 * c + 2];
 #pragma unroll
+            for (int j = 0; j < WS; ++j)
+#pragma unroll
             for (int v = 0; v < 2; ++v) {
-                double t = k01.x * pv[0].v[v];
-                t = fma(k01.y, pv[1].v[v], t);
-                t = fma(k23.x, pv[2].v[v], t);
-                t = fma(k23.y, nx[0].v[v], t);
-                t = fma(k45.x, nx[1].v[v], t);
-                t = fma(k45.y, nx[2].v[v], t);
-                y[c][v] = fma(al.v[v], t, y[c][v]);
+                double t = k01.x * pv[j][0].v[v];
+                t = fma(k01.y, pv[j][1].v[v], t);
+                t = fma(k23.x, pv[j][2].v[v], t);
+                t = fma(k23.y, nx[j][0].v[v], t);
+                t = fma(k45.x, nx[j][1].v[v], t);
+                t = fma(k45.y, nx[j][2].v[v], t);
+                y[j][c][v] = fma(al[j].v[v], t, y[j][c][v]);
             }
         }
     };
@@ -1178,41 +1184,54 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
             int wr = uu, h = 0;                               // uu = wr * H + h
             if (H > 1) { wr = uu / H; h = uu - wr * H; }
             const int64_t i = rowid[wr];
-            const int s0 = (sl + h) * 64 + 2 * lane;          // this lane's realisations s0, s0 + 1
-            const uint32_t lofs = uint32_t(h * 64 + 2 * lane) * 8u;   // their offset in a stage row
+            const int s0 = (sl + h) * WS * 64 + 2 * lane;     // this lane's realisations s0 + 64 j + {0, 1}
+            const uint32_t lofs = uint32_t(h * WS * 64 + 2 * lane) * 8u;   // their offset in a stage row
             const int32_t* roff = reinterpret_cast<const int32_t*>(st + hdr.z);
             const int32_t ro = roff[wr];                      // incidence offset | fixed bits << 24
             const int32_t kb = ro & 0xffffff, ke = roff[wr + 1] & 0xffffff;
             const unsigned char* rec0 = st + kMfsHdrBytes;
             // update operands from global memory first: their latency hides behind the gather
             // (registers: a shared-memory slot per lane costs stage space, measured slower)
-            Vec<2> c1v, c2v, c3v, uold[3];
+            Vec<2> c1v[WS], c2v[WS], c3v[WS], uold[WS][3];
             const int64_t ic = i * n_s + s0;
             const double* po = sc.uo + 3 * ic - 2 * s0;       // (i * 3 + d) * n_s + s0
             if (!APPLY) {
-                c1v = ld_ro<2>(a.c1 + ic);
-                if constexpr (C23) {
-                    c2v = ld_ro<2>(a.c2a + ic);
-                    c3v = ld_ro<2>(a.c3a + ic);
-                }
 #pragma unroll
-                for (int d = 0; d < 3; ++d) uold[d] = ld_rw<2>(po + d * n_s);
+                for (int j = 0; j < WS; ++j) {
+                    c1v[j] = ld_ro<2>(a.c1 + ic + 64 * j);
+                    if constexpr (C23) {
+                        c2v[j] = ld_ro<2>(a.c2a + ic + 64 * j);
+                        c3v[j] = ld_ro<2>(a.c3a + ic + 64 * j);
+                    }
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) uold[j][d] = ld_rw<2>(po + d * n_s + 64 * j);
+                }
             }
             const unsigned char* own = st + hdr.y + size_t(wr) * US + lofs;   // own row = slot wr
-            Vec<2> uo[3], pa[3], pb[3];
+            Vec<2> uo[WS][3], pa[WS][3], pb[WS][3], al[WS];
 #pragma unroll
-            for (int d = 0; d < 3; ++d) uo[d] = ld2(own + d * AS);
-            auto rel = [&](Vec<2> (&w)[3], int32_t off) {    // w = u[node at off] - u_i
+            for (int j = 0; j < WS; ++j)
+#pragma unroll
+                for (int d = 0; d < 3; ++d) uo[j][d] = ld2(own + d * AS + 512 * j);
+            auto rel = [&](Vec<2> (&w)[WS][3], int32_t off) {   // w = u[node at off] - u_i
+#pragma unroll
+                for (int j = 0; j < WS; ++j)
 #pragma unroll
                 for (int d = 0; d < 3; ++d) {
-                    w[d] = ld2(st + off + lofs + d * AS);
-                    w[d].v[0] -= uo[d].v[0];
-                    w[d].v[1] -= uo[d].v[1];
+                    w[j][d] = ld2(st + off + lofs + d * AS + 512 * j);
+                    w[j][d].v[0] -= uo[j][d].v[0];
+                    w[j][d].v[1] -= uo[j][d].v[1];
                 }
             };
-            double y[3][2];
+            auto ldal = [&](int32_t off) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) y[c][0] = y[c][1] = 0.0;
+                for (int j = 0; j < WS; ++j) al[j] = ld2(st + off + lofs + 512 * j);
+            };
+            double y[WS][3][2];
+#pragma unroll
+            for (int j = 0; j < WS; ++j)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) y[j][c][0] = y[j][c][1] = 0.0;
             int32_t k = kb;
             if (k < ke) rel(pa, reinterpret_cast<const int4*>(rec0 + size_t(k) * kMfsRecBytes)->z);
             // pairs of incidences: the first takes prev = pa, next = pb, the second prev = pb,
@@ -1223,20 +1242,24 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                 const int4 r2 = *reinterpret_cast<const int4*>(rp + kMfsRecBytes);
                 if (r.w && k != kb) rel(pa, r.z);           // a further chain starts (rare)
                 rel(pb, r.y);
-                incidence(y, pa, pb, ld2(st + r.x + lofs), rp);
+                ldal(r.x);
+                incidence(y, pa, pb, al, rp);
                 if (r2.w) rel(pb, r2.z);
                 rel(pa, r2.y);
-                incidence(y, pb, pa, ld2(st + r2.x + lofs), rp + kMfsRecBytes);
+                ldal(r2.x);
+                incidence(y, pb, pa, al, rp + kMfsRecBytes);
             }
             if (k < ke) {
                 const unsigned char* rp = rec0 + size_t(k) * kMfsRecBytes;
                 const int4 r = *reinterpret_cast<const int4*>(rp);
                 if (r.w && k != kb) rel(pa, r.z);
                 rel(pb, r.y);
-                incidence(y, pa, pb, ld2(st + r.x + lofs), rp);
+                ldal(r.x);
+                incidence(y, pa, pb, al, rp);
             }
             if constexpr (APPLY) {
-                store_y<2>(a, i, s0, y);
+#pragma unroll
+                for (int j = 0; j < WS; ++j) store_y<2>(a, i, s0 + 64 * j, y[j]);
             } else {
                 // f = sum_k coef_k F_k(i): a runtime loop over the fields in use (usually one);
                 // the F_k rows are 32-B aligned in the stage
@@ -1255,21 +1278,25 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                 // u_{n+1} = fma(c1, r, fma(c2, u_n, -(c3 u_{n-1}))), Dirichlet bits, stored over
                 // u_{n-1}; a non-finite value is an all-ones exponent: one max per realisation
                 const uint32_t fxb = uint32_t(ro) >> 24;
-                uint32_t emax[2] = {0u, 0u};
-                Vec<2> w[3];
+                uint32_t emax[WS][2];
+                Vec<2> w[WS][3];
 #pragma unroll
-                for (int d = 0; d < 3; ++d) {
+                for (int j = 0; j < WS; ++j) {
+                    emax[j][0] = emax[j][1] = 0u;
 #pragma unroll
-                    for (int v = 0; v < 2; ++v) {
-                        const double c2v_ = C23 ? c2v.v[v] : a.c2, c3v_ = C23 ? c3v.v[v] : a.c3;
-                        const double r = f[d] - y[d][v];
-                        const double tt = fma(c2v_, uo[d].v[v], -(c3v_ * uold[d].v[v]));
-                        double x = fma(c1v.v[v], r, tt);
-                        if ((fxb >> d) & 1u) x = 0.0;
-                        emax[v] = max(emax[v], uint32_t(__double2hiint(x)) & 0x7ff00000u);
-                        w[d].v[v] = x;
+                    for (int d = 0; d < 3; ++d) {
+#pragma unroll
+                        for (int v = 0; v < 2; ++v) {
+                            const double c2v_ = C23 ? c2v[j].v[v] : a.c2, c3v_ = C23 ? c3v[j].v[v] : a.c3;
+                            const double r = f[d] - y[j][d][v];
+                            const double tt = fma(c2v_, uo[j][d].v[v], -(c3v_ * uold[j][d].v[v]));
+                            double x = fma(c1v[j].v[v], r, tt);
+                            if ((fxb >> d) & 1u) x = 0.0;
+                            emax[j][v] = max(emax[j][v], uint32_t(__double2hiint(x)) & 0x7ff00000u);
+                            w[j][d].v[v] = x;
+                        }
+                        st_vec<2>(const_cast<double*>(po) + d * n_s + 64 * j, w[j][d]);
                     }
-                    st_vec<2>(const_cast<double*>(po) + d * n_s, w[d]);
                 }
                 if (a.fwd_ptr) {          // P2P halo: the same values into the neighbours' ghost rows
                     const int32_t f1 = __ldg(a.fwd_ptr + i + 1);
@@ -1277,15 +1304,20 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                         const int2 dd = a.fwd_dst[q];
                         double* dst = a.peer_buf[2 * dd.x + int((sc.step + 1) & 1)];
 #pragma unroll
-                        for (int d = 0; d < 3; ++d) st_vec<2>(dst + (int64_t(dd.y) * 3 + d) * n_s + s0, w[d]);
+                        for (int j = 0; j < WS; ++j)
+#pragma unroll
+                            for (int d = 0; d < 3; ++d)
+                                st_vec<2>(dst + (int64_t(dd.y) * 3 + d) * n_s + s0 + 64 * j, w[j][d]);
                     }
                     if (__ldg(a.fwd_ptr + i) < f1) __threadfence_system();
                 }
 #pragma unroll
+                for (int j = 0; j < WS; ++j)
+#pragma unroll
                 for (int v = 0; v < 2; ++v)
-                    if (emax[v] == 0x7ff00000u) {
+                    if (emax[j][v] == 0x7ff00000u) {
                         const unsigned long long code = (unsigned long long)(sc.step) << 24 |
-                                                        (unsigned long long)(a.s_global0 + s0 + v);
+                                                        (unsigned long long)(a.s_global0 + s0 + 64 * j + v);
                         atomicMin(a.flag, code);
                     }
             }
@@ -1703,19 +1735,19 @@ static cudaError_t launch_mf_warp(const StepArgs& a, cudaStream_t st) {
 // F3 shapes: consumer warps x stages (+ the producer warp; register allocation rounds a CTA
 // to multiples of 4 warps, so 11 + 1 warps leave 168 registers per thread, 15 + 1 only 128).
 // ENS_MFS_SHAPE = "CWxS" picks one of the built ones.
-struct MfsShapeDef { const char* name; int cw, s; };
-static constexpr MfsShapeDef kMfsShapes[] = {{"11x3", 11, 3}, {"11x2", 11, 2}, {"11x4", 11, 4}, {"15x3", 15, 3},
-                                             {"15x2", 15, 2}};
+// "w" shapes: two 64-realisation slices per consumer unit (WS = 2, N_s % 128 == 0; sliced
+// stages then hold 128-realisation slices); 7 + 1 warps leave 255 registers per thread.
+struct MfsShapeDef { const char* name; int cw, s, ws; };
+static constexpr MfsShapeDef kMfsShapes[] = {{"11x3", 11, 3, 1}, {"15x3", 15, 3, 1}, {"7x3w", 7, 3, 2},
+                                             {"11x3w", 11, 3, 2}};
+static constexpr int kMfsWide = 2;        // the default shape where N_s % 128 == 0
 // the context's shape (StepArgs::mfs_shape, chosen at create: ens_mf_staged_plan)
-static int mfs_env_shape() {
-    static const int id = [] {
-        const char* e = std::getenv("ENS_MFS_SHAPE");
-        if (e)
-            for (int k = 0; k < int(sizeof(kMfsShapes) / sizeof(kMfsShapes[0])); ++k)
-                if (!std::strcmp(e, kMfsShapes[k].name)) return k;
-        return -1;
-    }();
-    return id;
+static int mfs_env_shape() {          // read at each create (tests switch it per context)
+    const char* e = std::getenv("ENS_MFS_SHAPE");
+    if (e)
+        for (int k = 0; k < int(sizeof(kMfsShapes) / sizeof(kMfsShapes[0])); ++k)
+            if (!std::strcmp(e, kMfsShapes[k].name)) return k;
+    return -1;
 }
 
 static constexpr int kMfsSmemMax = 227 * 1024;
@@ -1724,17 +1756,23 @@ static constexpr int kMfsSmemMax = 227 * 1024;
 // and the per-copy cost of the TMA engine dominates, so strips of <= 16 consecutive RCM rows
 // (few long runs) win; at N_s >= 128 the rows are 3 KB+ and the byte volume dominates, so
 // compact patches of <= 24 rows (fewer neighbour rows per own row) win (c4: 24 rows 0.714 ms,
-// 16 rows 0.727, 32 rows 0.751 on one box).  11 consumer warps x
-// 3 stages for both (15 x 3: c4 0.735 vs 0.729 ms, c2 39.3 vs 38.3 us).  ENS_MFS_SHAPE /
+// 16 rows 0.727, 32 rows 0.751 on one box).  3 stages; 11 consumer warps of one 64-realisation
+// slice each at N_s = 64 (15 x 3: c4 0.735 vs 0.729 ms, c2 39.3 vs 38.3 us), 7 warps of two
+// slices each where N_s % 128 == 0 (c4: 0.676-0.683 vs 0.744-0.750 ms for 11 x 3 on one box;
+// 11 x 3w 0.757-0.762 ms: spills at 168 registers; 7 x 4w 0.737-0.770).  ENS_MFS_SHAPE /
 // ENS_MFS_TILING / ENS_MFS_MAXROWS override.
 MfsPlan mf_staged_plan(int32_t n_s) {
     MfsPlan p;
     const char* sv = std::getenv("ENS_MFS_SLICED");
     p.sliced = sv ? std::atoi(sv) != 0 && n_s > 64 : n_s >= 256;   // N_s >= 256: a node row (6 KB+) is too big
     const int env = mfs_env_shape();
-    p.shape = env >= 0 ? env : 0;                       // 11x3 (kMfsShapes)
+    // 7x3w (two slices per unit) where N_s % 128 == 0, else 11x3; a wide shape asked for where
+    // N_s % 128 != 0 falls back to 11x3
+    const bool wide_ok = n_s % 128 == 0;
+    p.shape = env >= 0 && (kMfsShapes[env].ws == 1 || wide_ok) ? env : (wide_ok ? kMfsWide : 0);
+    p.ws = kMfsShapes[p.shape].ws;
     const char* t = std::getenv("ENS_MFS_TILING");
-    p.patches = t ? std::strcmp(t, "strip") != 0 : (n_s != 64 && !p.sliced);   // 64-wide stage rows: strips
+    p.patches = t ? std::strcmp(t, "strip") != 0 : mfs_stage_w(p, n_s) != 64;   // 64-wide stage rows: strips
     const char* r = std::getenv("ENS_MFS_MAXROWS");
     p.max_rows = r ? std::max(1, std::min(kMfsMaxRows, std::atoi(r))) : (p.patches ? 24 : 16);
     return p;
@@ -1750,11 +1788,12 @@ bool mf_staged_applies(int32_t n_s) { return n_s % 64 == 0; }
 
 // 2-D tensor map of a row-major fp64 array [rows][cols] with a [box_rows][64] box, encoded
 // through the driver entry point (no -lcuda) and cached per (base, rows, cols, box_rows)
-static cudaError_t mfs_map(const double* base, int64_t rows, int64_t cols, int box_rows, CUtensorMap* out) {
+static cudaError_t mfs_map(const double* base, int64_t rows, int64_t cols, int box_rows, int box_cols,
+                           CUtensorMap* out) {
     struct Entry {
         const double* base;
         int64_t rows, cols;
-        int box;
+        int box, bcols;
         CUtensorMap map;
     };
     static std::mutex mu;
@@ -1762,7 +1801,7 @@ static cudaError_t mfs_map(const double* base, int64_t rows, int64_t cols, int b
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     std::lock_guard<std::mutex> lock(mu);
     for (const Entry& e : cache)
-        if (e.base == base && e.rows == rows && e.cols == cols && e.box == box_rows) {
+        if (e.base == base && e.rows == rows && e.cols == cols && e.box == box_rows && e.bcols == box_cols) {
             *out = e.map;
             return cudaSuccess;
         }
@@ -1773,10 +1812,10 @@ static cudaError_t mfs_map(const double* base, int64_t rows, int64_t cols, int b
         if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
-    Entry en{base, rows, cols, box_rows, {}};
+    Entry en{base, rows, cols, box_rows, box_cols, {}};
     const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
     const cuuint64_t strides[1] = {cuuint64_t(cols) * sizeof(double)};
-    const cuuint32_t box[2] = {64u, cuuint32_t(box_rows)};
+    const cuuint32_t box[2] = {cuuint32_t(box_cols), cuuint32_t(box_rows)};
     const cuuint32_t estr[2] = {1u, 1u};
     const CUresult r = encode(&en.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1788,7 +1827,7 @@ static cudaError_t mfs_map(const double* base, int64_t rows, int64_t cols, int b
     return cudaSuccess;
 }
 
-template <bool APPLY, int CW, int S, int NS, bool C23, bool SL>
+template <bool APPLY, int CW, int S, int NS, bool C23, bool SL, int WS = 1>
 static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
     if (a.mfs_ntiles == 0) return cudaSuccess;
     const size_t smem = size_t(S) * size_t(a.mfs_stage_bytes) + size_t(2 * S) * 8;
@@ -1798,7 +1837,7 @@ static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
     cudaGetDevice(&dev);
     const uint64_t bit = uint64_t(1) << (dev & 63);
     if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(k_step_mf_staged<APPLY, CW, S, NS, C23, SL>,
+        cudaError_t e = cudaFuncSetAttribute(k_step_mf_staged<APPLY, CW, S, NS, C23, SL, WS>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kMfsSmemMax - 256);
         if (e != cudaSuccess) return e;
         cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
@@ -1808,16 +1847,16 @@ static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
     std::memset(&maps, 0, sizeof(maps));
     int64_t items = a.mfs_ntiles;
     if constexpr (SL) {
-        items *= a.n_s / 64;
+        items *= a.n_s / (64 * WS);
         for (int k = 0; k < 6; ++k) {
-            cudaError_t e = mfs_map(a.ubuf0, a.u_rows * 3, a.n_s, 3 << k, &maps.u[0][k]);
-            if (e == cudaSuccess) e = mfs_map(a.ubuf1, a.u_rows * 3, a.n_s, 3 << k, &maps.u[1][k]);
-            if (e == cudaSuccess) e = mfs_map(a.alpha, a.mfs_alpha_rows, a.n_s, 1 << k, &maps.al[k]);
+            cudaError_t e = mfs_map(a.ubuf0, a.u_rows * 3, a.n_s, 3 << k, 64 * WS, &maps.u[0][k]);
+            if (e == cudaSuccess) e = mfs_map(a.ubuf1, a.u_rows * 3, a.n_s, 3 << k, 64 * WS, &maps.u[1][k]);
+            if (e == cudaSuccess) e = mfs_map(a.alpha, a.mfs_alpha_rows, a.n_s, 1 << k, 64 * WS, &maps.al[k]);
             if (e != cudaSuccess) return e;
         }
     }
     const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(sms[dev & 63], items)));
-    k_step_mf_staged<APPLY, CW, S, NS, C23, SL><<<grid, (CW + 1) * 32, smem, st>>>(a, maps);
+    k_step_mf_staged<APPLY, CW, S, NS, C23, SL, WS><<<grid, (CW + 1) * 32, smem, st>>>(a, maps);
     return cudaGetLastError();
 }
 
@@ -1836,12 +1875,25 @@ static cudaError_t launch_mf_staged_shape(const StepArgs& a, cudaStream_t st) {
     return launch_mf_staged_t<false, CW, S, 0, false, false>(a, st);
 }
 
+// two slices per unit (the plan picks these only where N_s % 128 == 0)
+template <int CW, int S>
+static cudaError_t launch_mf_staged_wide(const StepArgs& a, cudaStream_t st) {
+    if (a.n_s % 128 != 0) return cudaErrorInvalidValue;
+    if (a.mfs_slices > 1) {
+        if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, true, 2>(a, st);
+        if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, true, 2>(a, st);
+        return launch_mf_staged_t<false, CW, S, 0, false, true, 2>(a, st);
+    }
+    if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, false, 2>(a, st);
+    if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, false, 2>(a, st);
+    return launch_mf_staged_t<false, CW, S, 0, false, false, 2>(a, st);
+}
+
 static cudaError_t launch_mf_staged(const StepArgs& a, cudaStream_t st) {
     switch (a.mfs_shape) {
-        case 1: return launch_mf_staged_shape<11, 2>(a, st);
-        case 2: return launch_mf_staged_shape<11, 4>(a, st);
-        case 3: return launch_mf_staged_shape<15, 3>(a, st);
-        case 4: return launch_mf_staged_shape<15, 2>(a, st);
+        case 1: return launch_mf_staged_shape<15, 3>(a, st);
+        case 2: return launch_mf_staged_wide<7, 3>(a, st);
+        case 3: return launch_mf_staged_wide<11, 3>(a, st);
         default: return launch_mf_staged_shape<11, 3>(a, st);
     }
 }

@@ -127,6 +127,24 @@ def test_staged_node_partition_bitexact(n_s, P, halo):
     ref.close(); par.close()
 
 
+@pytest.mark.parametrize("damping", ["mass", "identity"])
+@pytest.mark.parametrize("n_s", [128, 256])
+def test_staged_shapes_bitexact(n_s, damping, monkeypatch):
+    """Consumer shapes (ENS_MFS_SHAPE, read at create): one 64-realisation slice per unit
+    (11x3, 15x3) or two (7x3w, the default at N_s % 128 == 0; 11x3w) change only which warp
+    computes a realisation, not its operations: bit-identical states and products (N_s = 256
+    takes the sliced stages: 64-realisation slices for 11x3 / 15x3, 128 for the wide shapes)."""
+    m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(24, 60), 0.01, 3), 8)
+    E, h = _mats(m, n_s, 21)
+    c_d = 120.0 if damping == "mass" else 0.3
+    ref = _run(m, E, h, "tiles", damping=damping, c_d=c_d, steps=200)
+    for shape in ("11x3", "15x3", "7x3w", "11x3w"):
+        monkeypatch.setenv("ENS_MFS_SHAPE", shape)
+        got = _run(m, E, h, "staged", damping=damping, c_d=c_d, steps=200)
+        for k in range(3):
+            assert np.array_equal(ref[k], got[k]), (shape, k)
+
+
 def test_variant_selection_and_rejection():
     """AUTO takes STAGED where it applies (N_s % 64 == 0) and TILES elsewhere; asking for a
     path that does not apply is ENS_E_UNSUPPORTED."""
@@ -148,12 +166,14 @@ def test_variant_selection_and_rejection():
     ens.close()
 
 
-def test_staged_divergence_detected():
+@pytest.mark.parametrize("n_s", [64, 128])
+def test_staged_divergence_detected(n_s):
     """A step 3x above the stability limit blows up: the staged kernel's non-finite check
-    (all-ones exponent per realisation) raises ENS_E_DIVERGED and latches the context."""
+    (all-ones exponent per realisation; at N_s = 128 in the two-slice units) raises
+    ENS_E_DIVERGED and latches the context."""
     from paper_2101_09059_b200._ffi import ENS_E_DIVERGED, ENS_E_STATE
     m = meshmod.cylinder(12, 23)
-    E, h = _mats(m, 64, 51)
+    E, h = _mats(m, n_s, 51)
     ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, k_shear=KS, kernel="matrix_free",
                           mf_variant="staged")
     dt = 3.0 * ens.info()["dt"] / 0.9 * 1.3
