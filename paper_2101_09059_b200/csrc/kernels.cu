@@ -1070,8 +1070,11 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
             load_entries();
         }
         if (ta + tstep < tb) dn2 = a.mfs_tiles[(ta + tstep) / HS];
-        for (int32_t t = ta; t < tb; t += tstep) {
-            const int it = int((t - ta) / tstep), s = it % S;
+        // stage s of item it = it mod S and its use count it / S, kept incrementally (a division
+        // by the runtime grid size per item cost ~6% of the issue slots on c4)
+        int s = 0, it = 0;
+        uint32_t round = 0;
+        for (int32_t t = ta; t < tb; t += tstep, ++it, s = s + 1 == S ? 0 : s + 1, round += s == 0) {
             const int sl = SL ? t % HS : 0;                   // realisation slice of the item
             const uint32_t full = bar0 + 8u * s, stage = smem_s + uint32_t(s) * SB;
             const MfTile d = dn;
@@ -1083,7 +1086,7 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                 load_entries();
                 if (t + 2 * tstep < tb) dn2 = a.mfs_tiles[(t + 2 * tstep) / HS];
             }
-            if (it >= S) mbar_wait(bar0 + 8u * (S + s), uint32_t(it / S - 1) & 1u);
+            if (it >= S) mbar_wait(bar0 + 8u * (S + s), (round - 1u) & 1u);
             if (lane == 0) mbar_expect_tx(full, uint32_t(d.stage_bytes) + uint32_t(nf * d.nrows) * 32u);
             __syncwarp();
             // one bulk-copy call site per entry slot (a lane-varying copy compiles to a loop over
@@ -1146,34 +1149,54 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
     auto incidence = [&](double (&y)[WS][3][2], const Vec<2> (&pv)[WS][3], const Vec<2> (&nx)[WS][3],
                          const Vec<2> (&al)[WS], const unsigned char* rp) {
         const double2* K2 = reinterpret_cast<const double2*>(rp + 16);
+        // K[6c .. 6c + 5] = (prev_0, prev_1, prev_2, next_0, next_1, next_2): 16-B aligned pairs.
+        // Written term-major: each of the 6 terms is issued for all 6 WS chains (c, j, v) before
+        // the next, so dependent FMAs of a chain sit 6 WS independent ones apart (component-major
+        // source let the scheduler place them 2-4 apart: fixed-latency stalls).  Same operations
+        // in the same order per chain as before.
+        double t[3][WS][2];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            // K[6c .. 6c + 5] = (prev_0, prev_1, prev_2, next_0, next_1, next_2): 16-B aligned pairs
-            const double2 k01 = K2[3 * c], k23 = K2[3 * c + 1], k45 = K2[3 * c + 2];
+        for (int q = 0; q < 3; ++q) {                       // terms 2q, 2q + 1
+            double2 kk[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) kk[c] = K2[3 * c + q];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int j = 0; j < WS; ++j)
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) {
+                        const double x0 = q == 0 ? pv[j][0].v[v] : q == 1 ? pv[j][2].v[v] : nx[j][1].v[v];
+                        t[c][j][v] = q == 0 ? kk[c].x * x0 : fma(kk[c].x, x0, t[c][j][v]);
+                    }
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int j = 0; j < WS; ++j)
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) {
+                        const double x1 = q == 0 ? pv[j][1].v[v] : q == 1 ? nx[j][0].v[v] : nx[j][2].v[v];
+                        t[c][j][v] = fma(kk[c].y, x1, t[c][j][v]);
+                    }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
 #pragma unroll
             for (int j = 0; j < WS; ++j)
 #pragma unroll
-            for (int v = 0; v < 2; ++v) {
-                double t = k01.x * pv[j][0].v[v];
-                t = fma(k01.y, pv[j][1].v[v], t);
-                t = fma(k23.x, pv[j][2].v[v], t);
-                t = fma(k23.y, nx[j][0].v[v], t);
-                t = fma(k45.x, nx[j][1].v[v], t);
-                t = fma(k45.y, nx[j][2].v[v], t);
-                y[j][c][v] = fma(al[j].v[v], t, y[j][c][v]);
-            }
-        }
+                for (int v = 0; v < 2; ++v) y[j][c][v] = fma(al[j].v[v], t[c][j][v], y[j][c][v]);
     };
     __shared__ double s_coef[kMaxFields];
     if (!APPLY && wid == 0 && lane < kMaxFields)
         s_coef[lane] = lane < a.n_fields ? a.coef_buf[(sc.step & 1) * kMaxFields + lane] : 0.0;
     asm volatile("bar.sync 1, %0;" :: "r"(CW * 32) : "memory");   // consumers only
     int32_t ubase = 0;                                        // units of the tiles before this one
-    for (int32_t t = ta; t < tb; t += tstep) {
-        const int it = int((t - ta) / tstep), s = it % S;
+    int s = 0;
+    uint32_t round = 0;
+    for (int32_t t = ta; t < tb; t += tstep, s = s + 1 == S ? 0 : s + 1, round += s == 0) {
         const int sl = SL ? t % HS : 0;
         const unsigned char* st = smem + size_t(s) * SB;
-        mbar_wait(bar0 + 8u * s, uint32_t(it / S) & 1u);
+        mbar_wait(bar0 + 8u * s, round & 1u);
         const int4 hdr = *reinterpret_cast<const int4*>(st);  // {nrows, u image, row offsets, F_k}
         const int32_t* rowid = reinterpret_cast<const int32_t*>(st + *reinterpret_cast<const int32_t*>(st + 16));
         const int32_t nunits = hdr.x * H;
