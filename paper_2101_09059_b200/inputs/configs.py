@@ -5,8 +5,8 @@ c2  ideal cylinder ~50k tri (96x262), N_s = 64, steady, mode-1 damping 250 1/s (
 c3  as c2, pulsatile traction over 3 cardiac cycles, undamped
 c4  synthetic branched aorta ~500k tri (mesh.aorta), N_s = 128, pulsatile, E 7e6 +- 7e5,
     zeta 0.2 +- 0.02 cm; every realisation an independent GMRF draw
-c5  the same generator at ~2M tri, N_s = 512, realisations from a 32-field GMRF basis
-    (fields.sample_materials: ~1,000 independent solves on 1M nodes would take minutes)
+c5  the same generator at ~2M tri, N_s = 512, independent draws too (~1,000 solves on 1M
+    nodes in 4-column groups on a thread pool)
 
 Material statistics: E 7.0e6 +- 7.0e5 Ba, zeta 0.4 +- 0.04 cm, rho_corr 3.7 cm
 (PAPER.md:436); density 1.06 g/cm^3; nu = 0.5, k = 5/6
@@ -65,12 +65,11 @@ def make_aorta(name: str, n_s: int | None = None, s_begin: int = 0, target_tris:
     tt, ns_def = _AORTA[name]
     m = meshmod.aorta(target_tris or tt)
     ns = n_s or ns_def
-    # c4: every realisation an independent GMRF draw (2 x 127 sparse-LU
-    # solves, ~20 s); c5 (512 realisations on 1M nodes, ~1,000 solves) keeps the 32-field
-    # basis, whose realisations are correlated
+    # every realisation an independent GMRF draw: one sparse LU, then
+    # 2 x (N_s - 1) solves in 4-column groups on a thread pool (c4 ~10 s, c5 ~1.5 min)
     E, h, _ = fields.sample_materials(m.xyz, m.tris, ns, E_mean=E_MEAN, E_std=E_STD,
                                       h_mean=0.2, h_std=0.02, rho_corr=RHO_CORR,
-                                      seed=seed, s_begin=s_begin, basis=32 if name == "c5" else None)
+                                      seed=seed, s_begin=s_begin)
     tr = loads.pulsatile(m.xyz, m.tris)
     return Config(name, m, E, h, tr, damping=DAMP_NONE, c_d=0.0, steps=2000, s_begin=s_begin)
 

@@ -21,6 +21,9 @@ Paper: nodal vectors E ~ N(E_bar, Q_alpha^-1) and zeta ~ N(zeta_bar, Q_alpha^-1)
 """
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 import scipy.sparse as sp
 import scipy.sparse.linalg as spla
@@ -55,8 +58,16 @@ def _z(seed: int, field_id: int, s: int, V: int) -> np.ndarray:
     return np.random.Generator(np.random.Philox(key=key)).standard_normal(V)
 
 
+GROUP = 4          # realisations solved together: s in [4g, 4g + 4) always as one 4-column solve
+
+
 class MaternSampler:
-    """Factor A = kappa^2 C~ + G once; draw any realisation index on demand."""
+    """Factor A = kappa^2 C~ + G once; draw any realisation index on demand.
+
+    Realisations are solved in aligned groups of GROUP columns (the whole group even when
+    only part of it is asked for), so the value of realisation s never depends on which
+    other realisations are drawn with it (N_s, shard s_begin); the groups run on a thread
+    pool (SuperLU's solve releases the GIL)."""
 
     def __init__(self, xyz: np.ndarray, tris: np.ndarray, rho_corr: float):
         self.V = xyz.shape[0]
@@ -68,10 +79,21 @@ class MaternSampler:
         self.sigma_spde = np.sqrt(1.0 / (4.0 * np.pi * self.kappa ** 2))
 
     def standard(self, seed: int, field_id: int, s_list) -> np.ndarray:
-        """Unit-variance GMRF draws, one column per realisation index in s_list."""
-        Z = np.stack([_z(seed, field_id, s, self.V) * self.sqrtC for s in s_list], axis=1)
-        X = self.lu.solve(Z)
-        return (X / self.sigma_spde).T                # [len(s_list)][V]
+        """Unit-variance GMRF draws, one row per realisation index in s_list: [len][V]."""
+        s_list = [int(s) for s in s_list]
+        groups = sorted({s // GROUP for s in s_list})
+
+        def solve(g):
+            Z = np.stack([_z(seed, field_id, s, self.V) * self.sqrtC for s in range(g * GROUP, (g + 1) * GROUP)],
+                         axis=1)
+            return g, self.lu.solve(Z)
+
+        with ThreadPoolExecutor(max(1, min(len(groups), os.cpu_count() or 1))) as ex:
+            sol = dict(ex.map(solve, groups))
+        out = np.empty((len(s_list), self.V))
+        for k, s in enumerate(s_list):
+            out[k] = sol[s // GROUP][:, s % GROUP]
+        return out / self.sigma_spde
 
 
 def standard_normals(seed: int, field_id: int, s_list, V: int) -> np.ndarray:
@@ -79,47 +101,20 @@ def standard_normals(seed: int, field_id: int, s_list, V: int) -> np.ndarray:
     return np.stack([_z(seed, field_id, s, V) for s in s_list])
 
 
-def _basis_weights(seed: int, field_id: int, s_list, K: int) -> np.ndarray:
-    """Unit vectors w_s in R^K, one per realisation index, counter-based (seed, field, s)."""
-    W = np.stack([_z(seed + 7919, field_id, s, K) for s in s_list])
-    return W / np.linalg.norm(W, axis=1, keepdims=True)
-
-
 def sample_materials(xyz: np.ndarray, tris: np.ndarray, n_s: int, *, E_mean: float,
                      E_std: float, h_mean: float, h_std: float, rho_corr: float,
-                     seed: int, s_begin: int = 0, homogeneous_first: bool = True,
-                     basis: int | None = None, device: bool = False):
-    """Return (E[n_s][V], h[n_s][V], n_clipped) for realisations s_begin .. s_begin+n_s-1.
-
-    basis = K (large configs c4/c5): draw K independent GMRF fields z_1..z_K per field type
-    and give realisation s the field sum_k w_{s,k} z_k with w_s a unit vector keyed by
-    (seed, field, s) — each realisation still has exactly the GMRF covariance Q^-1, at the
-    cost of correlation between realisations (stated in DESIGN.md "Inputs").
-    device = True solves on the GPU (ens_matern_fields) with the same z."""
+                     seed: int, s_begin: int = 0, homogeneous_first: bool = True):
+    """Return (E[n_s][V], h[n_s][V], n_clipped) for realisations s_begin .. s_begin+n_s-1,
+    every realisation an independent GMRF draw."""
     V = xyz.shape[0]
     E = np.empty((n_s, V))
     h = np.empty((n_s, V))
     s_idx = list(range(s_begin, s_begin + n_s))
     rand = [s for s in s_idx if not (homogeneous_first and s == 0)]
     if rand:
-        smp = None if device else MaternSampler(xyz, tris, rho_corr)
-        if device:                                    # GPU Jacobi-PCG (ens_matern_fields), same z
-            from .. import solver
-            def draw(fid, idx):
-                return solver.matern_fields(xyz, tris, rho_corr, standard_normals(seed, fid, idx, V))[0]
-            if basis:
-                xe = _basis_weights(seed, FIELD_E, rand, basis) @ draw(FIELD_E, range(basis))
-                xh = _basis_weights(seed, FIELD_H, rand, basis) @ draw(FIELD_H, range(basis))
-            else:
-                xe, xh = draw(FIELD_E, rand), draw(FIELD_H, rand)
-        elif basis:
-            be = smp.standard(seed, FIELD_E, range(basis))
-            bh = smp.standard(seed, FIELD_H, range(basis))
-            xe = _basis_weights(seed, FIELD_E, rand, basis) @ be
-            xh = _basis_weights(seed, FIELD_H, rand, basis) @ bh
-        else:
-            xe = smp.standard(seed, FIELD_E, rand)
-            xh = smp.standard(seed, FIELD_H, rand)
+        smp = MaternSampler(xyz, tris, rho_corr)
+        xe = smp.standard(seed, FIELD_E, rand)
+        xh = smp.standard(seed, FIELD_H, rand)
     k = 0
     for row, s in enumerate(s_idx):
         if homogeneous_first and s == 0:
