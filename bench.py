@@ -71,7 +71,7 @@ class ClockSampler:
              "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
              "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
-    def __init__(self, device_index: int, period_s: float = 0.02):
+    def __init__(self, device_index: int, period_s: float = 0.005):
         self.samples, self.reasons = [], set()
         self.period = period_s
         self._stop = threading.Event()
