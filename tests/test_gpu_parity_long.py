@@ -4,7 +4,8 @@
   both damping forms (mode 1 C~ = c_d M~, mode 2 C~ = c_d I: PAPER.md:343 and DESIGN.md
   reading 4), N_s = 4 and 64: relative L2 of u_n and u_{n-1} <= 1e-9 against the oracle
   (BASELINE.json north_star), for the assembled half storage (a1s) and
-  every matrix-free data path that applies (TILES, WARP, STAGED).
+  every matrix-free data path that applies (TILES, WARP, STAGED); STAGED also at N_s = 128
+  and 256 (two-slice units, whole rows / 128-wide sliced stages).
 * c2 at full size (96 x 262 rings, N_s = 64) in the bench's launch configuration, every
   kernel: sampled realisations recomputed one by one by the oracle, <= 1e-9 after 10^3 steps.
 * A node-partitioned run (P = 3, NCCL-style and P2P halos) compared directly with the oracle,
@@ -74,6 +75,29 @@ def test_1e4_steps_every_kernel(kernel, variant, n_s, damping):
                           damping=damping, c_d=C_D[damping], kernel=kernel, mf_variant=variant)
     if kernel == "matrix_free":
         assert ens.info()["mf_variant"] == solver.MF_VARIANT[variant if variant != "auto" else "staged"]
+    ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    done = 0
+    for step in sorted(snaps):
+        ens.step(step - done)
+        done = step
+        u, up, _, s = ens.get_state()
+        assert s == step
+        ref_u, ref_up = snaps[step]
+        for a, b in ((u, ref_u), (up, ref_up)):
+            assert np.linalg.norm(a - b) <= 1e-9 * np.linalg.norm(b), (step, np.linalg.norm(a - b) / np.linalg.norm(b))
+    ens.close()
+
+
+@pytest.mark.parametrize("n_s,damping", [(128, "mass"), (128, "identity"), (256, "mass")])
+def test_1e4_steps_staged_wide(n_s, damping):
+    """The matrix-free default at N_s % 128 == 0: two 64-realisation slices per consumer unit
+    (shape 7x3w), whole rows at 128 and 128-wide sliced stages at 256, 10^4 steps against the
+    oracle (the same bar as above)."""
+    cfg, dt, tr, snaps = _c1_case(n_s, damping)
+    m = cfg.mesh
+    ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS, dt=dt,
+                          damping=damping, c_d=C_D[damping], kernel="matrix_free")
+    assert ens.info()["mf_variant"] == solver.MF_VARIANT["staged"]
     ens.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
     done = 0
     for step in sorted(snaps):
