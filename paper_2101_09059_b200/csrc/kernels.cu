@@ -11,6 +11,7 @@
 // accumulates its realisations sequentially in CSR block order then d = 0,1,2 with explicit
 // fma(): the per-realisation arithmetic is identical whatever N_s, VEC or the launch
 // geometry, which makes ensemble runs bit-identical to single-realisation runs.
+#include <cstdio>
 #include <algorithm>
 #include <array>
 #include <atomic>
@@ -1013,6 +1014,23 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // alpha runs move as 2-D tensor copies (cp.async.bulk.tensor.2d) of [3 x count][64] and
 // [count][64] boxes out of the row-major arrays: boxes of 2^k rows (k = 0..5), a run of any
 // length being issued as its binary decomposition.
+// Opt-in device-side bounds checks of the staged path (build with ENS_NVCC_EXTRA=-DENS_CHECKS):
+// every copy lands inside its stage, every shared-memory read of a unit stays inside the
+// stage, rows and incidence ranges are consistent.  A violation prints and latches the
+// context's error flag (ENS_E_DIVERGED at step 0); the pool has no compute-sanitizer.
+#ifdef ENS_CHECKS
+#define MFS_CHECK(cond, what, v0, v1)                                                              \
+    do {                                                                                           \
+        if (!(cond)) {                                                                             \
+            printf("F3 check failed: %s (%lld, %lld) block %d thread %d\n", what, (long long)(v0),    \
+                   (long long)(v1), int(blockIdx.x), int(threadIdx.x));                            \
+            atomicMin(a.flag, 0ull);  /* reported as a divergence at step 0 */                    \
+        }                                                                                          \
+    } while (0)
+#else
+#define MFS_CHECK(cond, what, v0, v1) do {} while (0)
+#endif
+
 struct MfsMaps {
     CUtensorMap u[2][6];      // u buffer b viewed as [rows * 3][N_s], box [3 * 2^k][64 WS]
     CUtensorMap al[6];        // alpha [F][N_s], box [2^k][64 WS]
@@ -1100,6 +1118,8 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                     const int b = int(sc.step & 1);
                     int32_t first = x.y, cnt = x.z;
                     uint32_t dst = stage + uint32_t(x.w);
+                    MFS_CHECK(x.w >= 0 && uint32_t(x.w) + uint32_t(cnt) * (isu ? US : AS) <= SB, "2-D run past the stage",
+                              x.w, cnt);
                     while (cnt > 0) {
                         const int k = min(5, 31 - __clz(cnt));
                         const CUtensorMap* m = isu ? &maps.u[b][k] : &maps.al[k];
@@ -1118,12 +1138,15 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                     : x.x == kMfsA ? reinterpret_cast<const unsigned char*>(a.alpha) + int64_t(x.y) * AS
                                    : a.mfs_blob + int64_t(x.y) * 16;
                 const uint32_t bytes = x.x == kMfsU ? uint32_t(x.z) * US : x.x == kMfsA ? uint32_t(x.z) * AS : uint32_t(x.z);
+                MFS_CHECK(x.w >= 0 && uint32_t(x.w) + bytes <= SB && (bytes & 15u) == 0, "copy past the stage", x.w, bytes);
+                MFS_CHECK(x.x != kMfsU || int64_t(x.y) + x.z <= a.u_rows, "u run past the state", x.y, x.z);
                 tma_bulk_g2s(stage + uint32_t(x.w), src, bytes, full);
             }
 #pragma unroll
             for (int q = 0; q < EPL; ++q) {                  // own-row load fields (nf copies each)
                 const int4 x = e[q];
                 if (x.x != kMfsF) continue;
+                MFS_CHECK(uint32_t(x.w) + uint32_t(nf * d.nrows) * 32u <= SB, "F_k rows past the stage", x.w, d.nrows);
                 for (int k = 0; k < nf; ++k)
                     tma_bulk_g2s(stage + uint32_t(x.w) + uint32_t(k * d.nrows) * 32u,
                                  a.Fk + (int64_t(k) * a.fk_rows + x.y) * 4, uint32_t(x.z) * 32u, full);
@@ -1200,6 +1223,8 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
         const int4 hdr = *reinterpret_cast<const int4*>(st);  // {nrows, u image, row offsets, F_k}
         const int32_t* rowid = reinterpret_cast<const int32_t*>(st + *reinterpret_cast<const int32_t*>(st + 16));
         const int32_t nunits = hdr.x * H;
+        MFS_CHECK(hdr.x >= 1 && hdr.x <= kMfsMaxRows && hdr.y > 0 && uint32_t(hdr.y) + uint32_t(hdr.x) * US <= SB,
+                  "tile header", hdr.x, hdr.y);
         // Units go round-robin to the CW consumer warps.  (Weighting the warps of the SMSP that
         // also holds the producer less was measured slower: the most loaded warp releases each
         // stage last, which holds the producer back.)
@@ -1213,6 +1238,8 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
             const int32_t ro = roff[wr];                      // incidence offset | fixed bits << 24
             const int32_t kb = ro & 0xffffff, ke = roff[wr + 1] & 0xffffff;
             const unsigned char* rec0 = st + kMfsHdrBytes;
+            MFS_CHECK(kb <= ke && uint32_t(kMfsHdrBytes) + uint32_t(ke) * kMfsRecBytes <= SB, "incidence range", kb, ke);
+            MFS_CHECK(i >= 0 && i < a.u_rows, "row id", i, wr);
             // update operands from global memory first: their latency hides behind the gather
             // (registers: a shared-memory slot per lane costs stage space, measured slower)
             Vec<2> c1v[WS], c2v[WS], c3v[WS], uold[WS][3];
@@ -1237,6 +1264,7 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
 #pragma unroll
                 for (int d = 0; d < 3; ++d) uo[j][d] = ld2(own + d * AS + 512 * j);
             auto rel = [&](Vec<2> (&w)[WS][3], int32_t off) {   // w = u[node at off] - u_i
+                MFS_CHECK(off >= 0 && uint32_t(off) + US <= SB, "u read past the stage", off, US);
 #pragma unroll
                 for (int j = 0; j < WS; ++j)
 #pragma unroll
@@ -1247,6 +1275,7 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                 }
             };
             auto ldal = [&](int32_t off) {
+                MFS_CHECK(off >= 0 && uint32_t(off) + AS <= SB, "alpha read past the stage", off, AS);
 #pragma unroll
                 for (int j = 0; j < WS; ++j) al[j] = ld2(st + off + lofs + 512 * j);
             };
