@@ -268,6 +268,7 @@ class Run:
 
     def time(self, steps, warmup, stream, barrier, clocks=None):
         import torch
+        self.ens.prepare()              # step-loop graphs built as setup (ens_prepare), not timed
         self.ens.step(max(3, warmup))
         self.ens.sync()
         barrier()

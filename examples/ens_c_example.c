@@ -92,6 +92,7 @@ int main(void) {
     int rc = ens_create(&mesh, &mat, &opt, &ctx);
     if (rc) return die("ens_create", rc);
     if ((rc = ens_set_traction(ctx, 1, force, 0, NULL, NULL, 0.0, 0.0))) return die("ens_set_traction", rc);
+    if ((rc = ens_prepare(ctx))) return die("ens_prepare", rc);   /* step-loop graphs, no step run */
     if ((rc = ens_step(ctx, 12000))) return die("ens_step", rc);
     double t = 0.0;
     int64_t step = 0;

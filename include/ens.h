@@ -204,6 +204,16 @@ int ens_set_traction(ens_ctx* ctx, int32_t n_fields, const double* F, int32_t n_
  * ENS_E_STATE until ens_set_state. */
 int ens_step(ens_ctx* ctx, int64_t n);
 
+/* Build now what the first ens_step(n >= graph_steps) would otherwise build: the CUDA graphs
+ * of the step loop for both parities of the starting step (capture + instantiate; no step is
+ * executed and the state is untouched).  Setup work, so that a timed step loop does not pay
+ * for it.  No-op without graphs (graph_steps == 0, persistent kernel,
+ * re-assembly).  Collective with NCCL (the capture records the halo send/recv; a
+ * communicator that cannot be captured makes every rank fall back to direct launches, as in
+ * ens_step).  Errors: ENS_E_ARG (ctx NULL), ENS_E_STATE (P2P halo not connected),
+ * ENS_E_CUDA. */
+int ens_prepare(ens_ctx* ctx);
+
 /* Wait for the enqueued work; report a pending divergence. */
 int ens_sync(ens_ctx* ctx);
 

@@ -54,7 +54,7 @@ class EnsInfo(C.Structure):
 
 
 EXPORTS = [
-    "ens_create", "ens_set_traction", "ens_step", "ens_sync", "ens_get_state", "ens_set_state",
+    "ens_create", "ens_set_traction", "ens_step", "ens_prepare", "ens_sync", "ens_get_state", "ens_set_state",
     "ens_apply_stiffness", "ens_query", "ens_destroy", "ens_last_error", "ens_host_validate",
     "ens_host_pattern", "ens_host_partition", "ens_host_ghosts", "ens_host_element_stiffness",
     "ens_host_materials", "ens_create_csr", "ens_get_owned", "ens_host_halo_plan", "ens_stress",
@@ -89,6 +89,7 @@ def lib():
         "ens_create": (C.c_int, [P(EnsMesh), P(EnsMaterials), P(EnsOptions), P(vp)]),
         "ens_set_traction": (C.c_int, [vp, i32, vp, i32, vp, vp, f64, f64]),
         "ens_step": (C.c_int, [vp, i64]),
+        "ens_prepare": (C.c_int, [vp]),
         "ens_sync": (C.c_int, [vp]),
         "ens_get_state": (C.c_int, [vp, vp, vp, P(f64), P(i64)]),
         "ens_set_state": (C.c_int, [vp, vp, vp, f64, i64]),

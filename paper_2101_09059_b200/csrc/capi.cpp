@@ -1723,6 +1723,26 @@ int ens_step(ens_ctx* c, int64_t n) {
     return ENS_OK;
 }
 
+int ens_prepare(ens_ctx* c) {
+    if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
+    if (!c->p2p_connected) return fail(c, ENS_E_STATE, "P2P halo: call ens_p2p_connect before ens_prepare");
+    if (!c->use_graphs() || c->persistent) return ENS_OK;
+    if (c->graph_dirty) drop_graph(c);
+    c->graph_dirty = false;
+    for (int par = 0; par < 2; ++par) {
+        if (c->graph[par]) continue;
+        const int rc = build_graph(c, par);
+        if (rc && c->nccl_comm) {          // the same fallback as ens_step (every rank alike)
+            (void)cudaGetLastError();
+            drop_graph(c);
+            c->graph_steps = 0;
+            return ENS_OK;
+        }
+        RC_TRY(rc);
+    }
+    return ENS_OK;
+}
+
 int ens_sync(ens_ctx* c) {
     if (!c) return fail(nullptr, ENS_E_ARG, "ctx is NULL");
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));

@@ -158,6 +158,10 @@ class Ensemble:
     def step(self, n: int = 1):
         check(lib().ens_step(self._ctx, int(n)), self._ctx)
 
+    def prepare(self):
+        """Build the step-loop CUDA graphs now (setup; ens_prepare), not in the first ens_step."""
+        check(lib().ens_prepare(self._ctx), self._ctx)
+
     def sync(self):
         check(lib().ens_sync(self._ctx), self._ctx)
 

@@ -267,6 +267,8 @@ def test_node_partition_bitexact(kernel, P, halo):
     assert inf["halo"] == solver.HALO[halo] and inf["graph_steps"] > 0     # both halos captured in graphs
     for e in (ref, par):
         e.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    par.prepare()                   # both parities' graphs (with the halo) built ahead of ens_step
+    for e in (ref, par):
         e.step(257)
     u0, p0, _, s0 = ref.get_state()
     u1, p1, _, s1 = par.get_state()
@@ -285,6 +287,37 @@ def test_node_partition_bitexact(kernel, P, halo):
         e.step(40)
     assert np.array_equal(ref.get_state()[0], par.get_state()[0])
     ref.close(); par.close()
+
+
+@pytest.mark.parametrize("kernel", ["assembled_sym", "matrix_free"])
+def test_prepare_builds_graphs_without_stepping(kernel):
+    """ens_prepare captures the step-loop graphs of both parities and executes nothing: the
+    state and step are unchanged, and the run afterwards (graph replays from both parities,
+    a traction change that drops the graphs, prepare again) is bit-identical to one without."""
+    m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(20, 40), 0.01, 3), 5)
+    E, h = _mats(m, 64, 17)
+    tr = loads.pulsatile(m.xyz, m.tris, period=0.01, systole=0.004, ramp_T=0.003)
+    kw = dict(rho=RHO, nu=NU, k_shear=KS, kernel=kernel, dt=5e-5, damping="mass", c_d=100.0)
+    a = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, **kw)
+    b = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, **kw)
+    for e in (a, b):
+        e.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+    b.prepare()
+    u, p, t, s = b.get_state()
+    assert s == 0 and not u.any() and not p.any()
+    for e in (a, b):
+        e.step(1)
+    b.prepare()
+    for e in (a, b):
+        e.step(200)
+        e.set_traction(tr.F, tr.tab_t, tr.tab_g, 2 * tr.period, tr.ramp_T)   # new period: graphs dropped
+    b.prepare()
+    for e in (a, b):
+        e.step(129)
+    ua, pa, _, sa = a.get_state()
+    ub, pb, _, sb = b.get_state()
+    assert sa == sb == 330 and np.array_equal(ua, ub) and np.array_equal(pa, pb)
+    a.close(); b.close()
 
 
 @pytest.mark.parametrize("kernel", ["assembled", "assembled_sym"])
