@@ -31,21 +31,27 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+LIB_CHECKS = os.path.join(HERE, "libens_checks.so")   # -DENS_CHECKS: F3 device-side bounds checks
+
+
+def build(force: bool = False, verbose: bool = False, checks: bool = False) -> str:
+    """libens.so; with checks=True the bounds-checked libens_checks.so (load it with
+    ENS_LIB_PATH)."""
+    lib = LIB_CHECKS if checks else LIB
+    if not checks and not force and not stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc"),
-           *os.environ.get("ENS_NVCC_EXTRA", "").split(), *sources(), "-o", tmp]
+           *(["-DENS_CHECKS"] if checks else []), *os.environ.get("ENS_NVCC_EXTRA", "").split(), *sources(),
+           "-o", tmp]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
     import sys
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force=True, verbose="-v" in sys.argv, checks="--checks" in sys.argv))
