@@ -1750,16 +1750,15 @@ template <bool APPLY, int WARPS, int B>
 static cudaError_t launch_mf_warp_t(const StepArgs& a, cudaStream_t st) {
     if (a.V == 0) return cudaSuccess;
     const size_t smem = size_t(WARPS) * 2 * B * (kMfwSlotBytes + sizeof(int4) + sizeof(uint64_t));
-    static std::atomic<uint64_t> attr_set{0};
-    static int sms[64] = {0};
-    int dev = 0;
+    static std::atomic<uint64_t> attr_set{0};   // the attribute call is idempotent: a race only repeats it
+    int dev = 0, n_sm = 0;
     cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);   // host-cached, no shared state
     const uint64_t bit = uint64_t(1) << (dev & 63);
     if (!(attr_set.load(std::memory_order_acquire) & bit)) {
         cudaError_t e = cudaFuncSetAttribute(k_step_mf_warp<APPLY, WARPS, B>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
-        cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
         attr_set.fetch_or(bit, std::memory_order_release);
     }
     MfwMaps maps;
@@ -1771,7 +1770,7 @@ static cudaError_t launch_mf_warp_t(const StepArgs& a, cudaStream_t st) {
     }
     // one CTA per SM (persistent); fewer when the rows would leave warps empty
     const int64_t max_ctas = (a.V + WARPS - 1) / WARPS;
-    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(sms[dev & 63], max_ctas)));
+    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(n_sm, max_ctas)));
     k_step_mf_warp<APPLY, WARPS, B><<<grid, WARPS * 32, smem, st>>>(a, maps);
     return cudaGetLastError();
 }
@@ -1883,16 +1882,15 @@ template <bool APPLY, int CW, int S, int NS, bool C23, bool SL, int WS = 1>
 static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
     if (a.mfs_ntiles == 0) return cudaSuccess;
     const size_t smem = size_t(S) * size_t(a.mfs_stage_bytes) + size_t(2 * S) * 8;
-    static std::atomic<uint64_t> attr_set{0};
-    static int sms[64] = {0};
-    int dev = 0;
+    static std::atomic<uint64_t> attr_set{0};   // the attribute call is idempotent: a race only repeats it
+    int dev = 0, n_sm = 0;
     cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);   // host-cached, no shared state
     const uint64_t bit = uint64_t(1) << (dev & 63);
     if (!(attr_set.load(std::memory_order_acquire) & bit)) {
         cudaError_t e = cudaFuncSetAttribute(k_step_mf_staged<APPLY, CW, S, NS, C23, SL, WS>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kMfsSmemMax - 256);
         if (e != cudaSuccess) return e;
-        cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
         attr_set.fetch_or(bit, std::memory_order_release);
     }
     MfsMaps maps;
@@ -1907,7 +1905,7 @@ static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
             if (e != cudaSuccess) return e;
         }
     }
-    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(sms[dev & 63], items)));
+    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(n_sm, items)));
     k_step_mf_staged<APPLY, CW, S, NS, C23, SL, WS><<<grid, (CW + 1) * 32, smem, st>>>(a, maps);
     return cudaGetLastError();
 }
