@@ -1228,7 +1228,15 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
         // Units go round-robin to the CW consumer warps.  (Weighting the warps of the SMSP that
         // also holds the producer less was measured slower: the most loaded warp releases each
         // stage last, which holds the producer back.)
-        auto unit = [&](int32_t uu) {
+        // A warp arrives on the stage's EMPTY barrier right after its last read of the stage
+        // (the last unit's F_k rows), before that unit's update arithmetic and stores, so the
+        // producer can start the refill while they run.
+        const uint32_t empty_bar = bar0 + 8u * (S + s);
+        auto release = [&]() {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty_bar);
+        };
+        auto unit = [&](int32_t uu, bool last) {
             int wr = uu, h = 0;                               // uu = wr * H + h
             if (H > 1) { wr = uu / H; h = uu - wr * H; }
             const int64_t i = rowid[wr];
@@ -1310,6 +1318,7 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                 incidence(y, pa, pb, al, rp);
             }
             if constexpr (APPLY) {
+                if (last) release();
 #pragma unroll
                 for (int j = 0; j < WS; ++j) store_y<2>(a, i, s0 + 64 * j, y[j]);
             } else {
@@ -1326,6 +1335,7 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                     f[1] = fma(cq, f01.y, f[1]);
                     f[2] = fma(cq, f2, f[2]);
                 }
+                if (last) release();                      // no stage read below
                 // S2 + S4 (Eq. 22), the same operations as upd_store: r = f - y,
                 // u_{n+1} = fma(c1, r, fma(c2, u_n, -(c3 u_{n-1}))), Dirichlet bits, stored over
                 // u_{n-1}; a non-finite value is an all-ones exponent: one max per realisation
@@ -1376,10 +1386,9 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
         };
         int32_t uu = wid - ubase % CW;
         if (uu < 0) uu += CW;
-        for (; uu < nunits; uu += CW) unit(uu);
+        if (uu >= nunits) release();                      // no unit of this warp in the tile
+        for (; uu < nunits; uu += CW) unit(uu, uu + CW >= nunits);
         ubase += nunits;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar0 + 8u * (S + s));
     }
     }                                  // consumer warps
     if (!APPLY) step_coef(a, sc);      // block 0 thread 0: the next step's load coefficients
