@@ -1373,15 +1373,22 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                     }
                     if (__ldg(a.fwd_ptr + i) < f1) __threadfence_system();
                 }
+                uint32_t bad = 0;                          // one branch for the common case
 #pragma unroll
                 for (int j = 0; j < WS; ++j)
 #pragma unroll
-                for (int v = 0; v < 2; ++v)
-                    if (emax[j][v] == 0x7ff00000u) {
-                        const unsigned long long code = (unsigned long long)(sc.step) << 24 |
-                                                        (unsigned long long)(a.s_global0 + s0 + 64 * j + v);
-                        atomicMin(a.flag, code);
-                    }
+                    for (int v = 0; v < 2; ++v) bad |= uint32_t(emax[j][v] == 0x7ff00000u) << (2 * j + v);
+                if (bad) {
+#pragma unroll
+                    for (int j = 0; j < WS; ++j)
+#pragma unroll
+                        for (int v = 0; v < 2; ++v)
+                            if ((bad >> (2 * j + v)) & 1u) {
+                                const unsigned long long code = (unsigned long long)(sc.step) << 24 |
+                                                                (unsigned long long)(a.s_global0 + s0 + 64 * j + v);
+                                atomicMin(a.flag, code);
+                            }
+                }
             }
         };
         int32_t uu = wid - ubase % CW;
