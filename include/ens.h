@@ -128,9 +128,9 @@ typedef struct {
                                other ranks with ens_p2p_export / ens_p2p_connect before ens_step. */
     int32_t p2p_procs;      /* halo == P2P: 1 = one part per process (CUDA IPC), 0 = all parts here */
     int32_t mf_variant;     /* kernel == MATRIX_FREE: the device data path of the same arithmetic
-                               (ENS_MF_*).  AUTO (0): STAGED where it applies (N_s % 64 == 0), else
+                               (ENS_MF_*).  AUTO (0): STAGED where it applies (even N_s >= 64), else
                                TILES.  Asking for a path that does not apply to the context
-                               (STAGED: N_s % 64 != 0; WARP: N_s % 64 != 0 or damping == IDENTITY)
+                               (STAGED: N_s odd or < 64; WARP: N_s % 64 != 0 or damping == IDENTITY)
                                returns ENS_E_UNSUPPORTED.  Ignored by the assembled kernels. */
     int32_t persistent;     /* dist == NODE, halo == P2P, kernel ASSEMBLED or ASSEMBLED_SYM, no
                                re-assembly: 1 = ens_step(n) advances every part held here by n

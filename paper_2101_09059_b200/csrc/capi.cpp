@@ -409,7 +409,8 @@ cudaError_t launch_rows(const ens_ctx* c, const Part& p, ens::StepArgs a, int64_
         a.mfs_ntiles = ts->ntiles;
         a.mfs_stage_bytes = ts->stage_bytes;
         a.mfs_shape = c->mfs_plan.shape;
-        a.mfs_slices = c->mfs_plan.sliced ? c->n_s / ens::mfs_stage_w(c->mfs_plan, c->n_s) : 1;
+        a.mfs_slices = c->mfs_plan.sliced ? (c->n_s + ens::mfs_stage_w(c->mfs_plan, c->n_s) - 1) /
+                                                 ens::mfs_stage_w(c->mfs_plan, c->n_s) : 1;
         a.mfs_alpha_rows = p.n_alpha;
     }
     switch (c->kernel) {
@@ -755,6 +756,16 @@ static std::vector<std::vector<int32_t>> mf_patches(const std::vector<int32_t>& 
     return tiles;
 }
 
+// Bytes of a stage a tile image may fill.  With a ragged N_s in whole-row stages the lanes of
+// a row's last (partial) unit read up to 8 * pad bytes past the end of a node row (pad = the
+// realisations that round N_s up to whole units; kernels.cu k_step_mf_staged): that much
+// slack stays free at the end of every stage.
+static size_t mfs_budget(const ens_ctx* c, const ens::MfsShape& sh) {
+    const int64_t w = 64 * c->mfs_plan.ws;
+    const int64_t pad = c->mfs_plan.sliced ? 0 : (c->n_s + w - 1) / w * w - c->n_s;
+    return size_t(sh.stage_bytes) - size_t((8 * pad + 127) & ~int64_t(127));
+}
+
 // Upload the tile set of one launched row range: copy entries and blobs (final element ids).
 int build_mf_tiles(ens_ctx* c, const std::vector<int32_t>& ip, const std::vector<ens::FanRec>& rec,
                    const std::vector<double>& k18, const std::vector<uint8_t>& fx,
@@ -769,7 +780,7 @@ int build_mf_tiles(ens_ctx* c, const std::vector<int32_t>& ip, const std::vector
     for (size_t pi = 0; pi < patches.size(); ++pi) {
         mf_layout(ip, rec, patches[pi], US, AS, L);
         if (L.entries > ens::kMfsMaxEntries ||
-            L.bytes + size_t(ens::kMaxFields) * L.rows.size() * 32 > size_t(sh.stage_bytes)) {
+            L.bytes + size_t(ens::kMaxFields) * L.rows.size() * 32 > mfs_budget(c, sh)) {
             if (L.rows.size() == 1)
                 return fail(c, ENS_E_UNSUPPORTED, "matrix-free staged: the operands of row " +
                                                       std::to_string(L.rows[0]) + " exceed one shared-memory stage");
@@ -1082,7 +1093,7 @@ int build_part(ens_ctx* c, Part& P, const Global& G) {
             const size_t US = W * 24, AS = W * 8;
             for (const auto& tl : tilings)
                 patches.push_back(tl.second > tl.first
-                                      ? mf_patches(ip, rec, n_loc, tl.first, tl.second - tl.first, US, AS, size_t(sh.stage_bytes), c->mfs_plan)
+                                      ? mf_patches(ip, rec, n_loc, tl.first, tl.second - tl.first, US, AS, mfs_budget(c, sh), c->mfs_plan)
                                       : std::vector<std::vector<int32_t>>());
             // elements renumbered by first touch in the (whole-range) tile order: each tile's
             // alpha rows then move in few runs
@@ -1258,7 +1269,7 @@ int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, cons
         const bool warp_ok = diff && c->n_s % 64 == 0 && c->damping != ENS_DAMP_IDENTITY;
         if (req == ENS_MF_AUTO) c->mf_variant = staged_ok ? ENS_MF_STAGED : ENS_MF_TILES;
         else if (req == ENS_MF_STAGED && !staged_ok)
-            return fail(c, ENS_E_UNSUPPORTED, "mf_variant STAGED needs n_s % 64 == 0 (and the DIFF form)");
+            return fail(c, ENS_E_UNSUPPORTED, "mf_variant STAGED needs an even n_s >= 64 (and the DIFF form)");
         else if (req == ENS_MF_WARP && !warp_ok)
             return fail(c, ENS_E_UNSUPPORTED, "mf_variant WARP needs n_s % 64 == 0 and damping != IDENTITY");
         else c->mf_variant = req;
@@ -1334,7 +1345,7 @@ int create_impl(ens_ctx* c, const ens_mesh* mesh, const ens_materials* mat, cons
                 const size_t blob = (size_t(ens::kMfsHdrBytes) + ninc * ens::kMfsRecBytes + 12 + 127) & ~size_t(127);
                 worst = std::max(worst, blob + (1 + nn) * US + ninc * AS + size_t(ens::kMaxFields) * 32);
             }
-            if (worst > size_t(sh.stage_bytes)) {
+            if (worst > mfs_budget(c, sh)) {
                 if (!opt || opt->mf_variant == ENS_MF_AUTO) c->mf_variant = ENS_MF_TILES;
                 else return fail(c, ENS_E_UNSUPPORTED, "mf_variant STAGED: one row's operands (" + std::to_string(worst) +
                                                           " B) exceed a shared-memory stage at this N_s");

@@ -1038,7 +1038,7 @@ struct MfsMaps {
 
 // NS: N_s at compile time (64) or 0 (runtime); C23: per-row c2, c3 arrays (identity damping);
 // SL: sliced stages (above)
-template <bool APPLY, int CW, int S, int NS, bool C23, bool SL, int WS>
+template <bool APPLY, int CW, int S, int NS, bool C23, bool SL, int WS, bool RAG>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
 k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1063,7 +1063,7 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
     // L2 when the tiles one ring later need it (contiguous per-CTA chunks spread the front
     // over the whole mesh: c4 moved 1.43x its algorithmic DRAM bytes that way)
     // work items: tiles, or (tile, slice) pairs with SL (item = tile * HS + slice)
-    const int HS = SL ? (n_s >> 6) / WS : 1;                  // slices of 64 WS realisations
+    const int HS = SL ? (n_s + 64 * WS - 1) / (64 * WS) : 1; // slices of 64 WS realisations (last may be partial)
     const int32_t ta = int32_t(blockIdx.x), tb = nt * HS, tstep = int32_t(gridDim.x);
     const uint32_t US = SL ? 1536u * WS : uint32_t(n_s) * 24u, AS = SL ? 512u * WS : uint32_t(n_s) * 8u;   // stage rows
 
@@ -1160,7 +1160,9 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
     // the K^ coefficients, the records and the loop overhead of an incidence serve both slices and
     // the lane carries 12 independent accumulation chains; the arithmetic of each realisation is
     // unchanged (bit-identical to WS = 1).
-    const int H = SL ? 1 : (n_s >> 6) / WS;                  // units per row
+    // units per row; N_s need only be even: the last unit of a row may be partial (its lanes
+    // past N_s address realisation N_s - 2 instead and store nothing)
+    const int H = SL ? 1 : (n_s + 64 * WS - 1) / (64 * WS);
     auto ld2 = [&](const unsigned char* p) {
         const double2 v = *reinterpret_cast<const double2*>(p);
         Vec<2> r;
@@ -1242,6 +1244,18 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
             const int64_t i = rowid[wr];
             const int s0 = (sl + h) * WS * 64 + 2 * lane;     // this lane's realisations s0 + 64 j + {0, 1}
             const uint32_t lofs = uint32_t(h * WS * 64 + 2 * lane) * 8u;   // their offset in a stage row
+            // per pair j: valid (inside N_s) and the realisation its global loads and stores use
+            // (clamped to N_s - 2 past N_s; those lanes store nothing).  Shared-memory reads keep
+            // the plain offsets: past N_s they read zero-filled columns of a sliced row, or up to
+            // 64 WS - 2 realisations past the end of a whole row — the host keeps that much slack
+            // at the end of every stage image when N_s is ragged (capi.cpp mfs_budget)
+            bool vj[WS];
+            int sa[WS];
+#pragma unroll
+            for (int j = 0; j < WS; ++j) {
+                vj[j] = !RAG || s0 + 64 * j < n_s;            // RAG: N_s % (64 WS) != 0
+                sa[j] = vj[j] ? s0 + 64 * j : n_s - 2;
+            }
             const int32_t* roff = reinterpret_cast<const int32_t*>(st + hdr.z);
             const int32_t ro = roff[wr];                      // incidence offset | fixed bits << 24
             const int32_t kb = ro & 0xffffff, ke = roff[wr + 1] & 0xffffff;
@@ -1251,18 +1265,18 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
             // update operands from global memory first: their latency hides behind the gather
             // (registers: a shared-memory slot per lane costs stage space, measured slower)
             Vec<2> c1v[WS], c2v[WS], c3v[WS], uold[WS][3];
-            const int64_t ic = i * n_s + s0;
-            const double* po = sc.uo + 3 * ic - 2 * s0;       // (i * 3 + d) * n_s + s0
+            const int64_t ic = i * n_s;
+            double* po = sc.uo + 3 * ic;                      // row i of u_{n-1} / u_{n+1}: (i * 3 + d) * n_s
             if (!APPLY) {
 #pragma unroll
                 for (int j = 0; j < WS; ++j) {
-                    c1v[j] = ld_ro<2>(a.c1 + ic + 64 * j);
+                    c1v[j] = ld_ro<2>(a.c1 + ic + sa[j]);
                     if constexpr (C23) {
-                        c2v[j] = ld_ro<2>(a.c2a + ic + 64 * j);
-                        c3v[j] = ld_ro<2>(a.c3a + ic + 64 * j);
+                        c2v[j] = ld_ro<2>(a.c2a + ic + sa[j]);
+                        c3v[j] = ld_ro<2>(a.c3a + ic + sa[j]);
                     }
 #pragma unroll
-                    for (int d = 0; d < 3; ++d) uold[j][d] = ld_rw<2>(po + d * n_s + 64 * j);
+                    for (int d = 0; d < 3; ++d) uold[j][d] = ld_rw<2>(po + d * n_s + sa[j]);
                 }
             }
             const unsigned char* own = st + hdr.y + size_t(wr) * US + lofs;   // own row = slot wr
@@ -1320,7 +1334,8 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
             if constexpr (APPLY) {
                 if (last) release();
 #pragma unroll
-                for (int j = 0; j < WS; ++j) store_y<2>(a, i, s0 + 64 * j, y[j]);
+                for (int j = 0; j < WS; ++j)
+                    if (vj[j]) store_y<2>(a, i, sa[j], y[j]);
             } else {
                 // f = sum_k coef_k F_k(i): a runtime loop over the fields in use (usually one);
                 // the F_k rows are 32-B aligned in the stage
@@ -1357,8 +1372,9 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                             emax[j][v] = max(emax[j][v], uint32_t(__double2hiint(x)) & 0x7ff00000u);
                             w[j][d].v[v] = x;
                         }
-                        st_vec<2>(const_cast<double*>(po) + d * n_s + 64 * j, w[j][d]);
+                        if (vj[j]) st_vec<2>(po + d * n_s + sa[j], w[j][d]);
                     }
+                    if (!vj[j]) emax[j][0] = emax[j][1] = 0u;
                 }
                 if (a.fwd_ptr) {          // P2P halo: the same values into the neighbours' ghost rows
                     const int32_t f1 = __ldg(a.fwd_ptr + i + 1);
@@ -1369,7 +1385,7 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                         for (int j = 0; j < WS; ++j)
 #pragma unroll
                             for (int d = 0; d < 3; ++d)
-                                st_vec<2>(dst + (int64_t(dd.y) * 3 + d) * n_s + s0 + 64 * j, w[j][d]);
+                                if (vj[j]) st_vec<2>(dst + (int64_t(dd.y) * 3 + d) * n_s + sa[j], w[j][d]);
                     }
                     if (__ldg(a.fwd_ptr + i) < f1) __threadfence_system();
                 }
@@ -1385,7 +1401,7 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                         for (int v = 0; v < 2; ++v)
                             if ((bad >> (2 * j + v)) & 1u) {
                                 const unsigned long long code = (unsigned long long)(sc.step) << 24 |
-                                                                (unsigned long long)(a.s_global0 + s0 + 64 * j + v);
+                                                                (unsigned long long)(a.s_global0 + sa[j] + v);
                                 atomicMin(a.flag, code);
                             }
                 }
@@ -1833,10 +1849,15 @@ MfsPlan mf_staged_plan(int32_t n_s) {
     const char* sv = std::getenv("ENS_MFS_SLICED");
     p.sliced = sv ? std::atoi(sv) != 0 && n_s > 64 : n_s >= 256;   // N_s >= 256: a node row (6 KB+) is too big
     const int env = mfs_env_shape();
-    // 7x3w (two slices per unit) where N_s % 128 == 0, else 11x3; a wide shape asked for where
-    // N_s % 128 != 0 falls back to 11x3
-    const bool wide_ok = n_s % 128 == 0;
-    p.shape = env >= 0 && (kMfsShapes[env].ws == 1 || wide_ok) ? env : (wide_ok ? kMfsWide : 0);
+    // 7x3w (two slices per unit) unless that pads more realisations than one slice per unit
+    // does (N_s = 192: three units of 64 against two of 128 with 64 idle lanes), else 11x3; a
+    // wide shape asked for below N_s = 128 falls back to 11x3
+    auto pad = [&](int w) { return (n_s + w - 1) / w * w - n_s; };
+    const bool wide_ok = n_s >= 128 && pad(128) <= pad(64);
+    // shapes other than the defaults (11x3, 7x3w) have no instances for a ragged N_s
+    const bool env_ok = env >= 0 && (kMfsShapes[env].ws == 1 || n_s >= 128) &&
+                        (env == 0 || env == kMfsWide || n_s % (64 * kMfsShapes[env].ws) == 0);
+    p.shape = env_ok ? env : (wide_ok ? kMfsWide : 0);
     p.ws = kMfsShapes[p.shape].ws;
     const char* t = std::getenv("ENS_MFS_TILING");
     p.patches = t ? std::strcmp(t, "strip") != 0 : mfs_stage_w(p, n_s) != 64;   // 64-wide stage rows: strips
@@ -1851,7 +1872,8 @@ MfsShape mf_staged_shape(int shape) {
     return {d.cw, d.s, sb};
 }
 
-bool mf_staged_applies(int32_t n_s) { return n_s % 64 == 0; }
+// any even N_s >= 64 (the last unit or slice of a row may be partial)
+bool mf_staged_applies(int32_t n_s) { return n_s >= 64 && n_s % 2 == 0; }
 
 // 2-D tensor map of a row-major fp64 array [rows][cols] with a [box_rows][64] box, encoded
 // through the driver entry point (no -lcuda) and cached per (base, rows, cols, box_rows)
@@ -1894,7 +1916,7 @@ static cudaError_t mfs_map(const double* base, int64_t rows, int64_t cols, int b
     return cudaSuccess;
 }
 
-template <bool APPLY, int CW, int S, int NS, bool C23, bool SL, int WS = 1>
+template <bool APPLY, int CW, int S, int NS, bool C23, bool SL, int WS = 1, bool RAG = false>
 static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
     if (a.mfs_ntiles == 0) return cudaSuccess;
     const size_t smem = size_t(S) * size_t(a.mfs_stage_bytes) + size_t(2 * S) * 8;
@@ -1904,7 +1926,7 @@ static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);   // host-cached, no shared state
     const uint64_t bit = uint64_t(1) << (dev & 63);
     if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(k_step_mf_staged<APPLY, CW, S, NS, C23, SL, WS>,
+        cudaError_t e = cudaFuncSetAttribute(k_step_mf_staged<APPLY, CW, S, NS, C23, SL, WS, RAG>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kMfsSmemMax - 256);
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(bit, std::memory_order_release);
@@ -1913,7 +1935,7 @@ static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
     std::memset(&maps, 0, sizeof(maps));
     int64_t items = a.mfs_ntiles;
     if constexpr (SL) {
-        items *= a.n_s / (64 * WS);
+        items *= (a.n_s + 64 * WS - 1) / (64 * WS);
         for (int k = 0; k < 6; ++k) {
             cudaError_t e = mfs_map(a.ubuf0, a.u_rows * 3, a.n_s, 3 << k, 64 * WS, &maps.u[0][k]);
             if (e == cudaSuccess) e = mfs_map(a.ubuf1, a.u_rows * 3, a.n_s, 3 << k, 64 * WS, &maps.u[1][k]);
@@ -1922,45 +1944,46 @@ static cudaError_t launch_mf_staged_t(const StepArgs& a, cudaStream_t st) {
         }
     }
     const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(n_sm, items)));
-    k_step_mf_staged<APPLY, CW, S, NS, C23, SL, WS><<<grid, (CW + 1) * 32, smem, st>>>(a, maps);
+    k_step_mf_staged<APPLY, CW, S, NS, C23, SL, WS, RAG><<<grid, (CW + 1) * 32, smem, st>>>(a, maps);
     return cudaGetLastError();
 }
 
 // the hot instance (N_s = 64, scalar c2 / c3) gets N_s at compile time; the others run generic;
-// sliced stages (N_s >= 256) are their own instances
-template <int CW, int S>
+// sliced stages (N_s >= 256) are their own instances; RAG: N_s not a multiple of the unit
+// width (partial last units; only the default shapes have these instances)
+template <int CW, int S, bool RAG = false>
 static cudaError_t launch_mf_staged_shape(const StepArgs& a, cudaStream_t st) {
     if (a.mfs_slices > 1) {
-        if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, true>(a, st);
-        if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, true>(a, st);
-        return launch_mf_staged_t<false, CW, S, 0, false, true>(a, st);
+        if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, true, 1, RAG>(a, st);
+        if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, true, 1, RAG>(a, st);
+        return launch_mf_staged_t<false, CW, S, 0, false, true, 1, RAG>(a, st);
     }
-    if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, false>(a, st);
-    if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, false>(a, st);
-    if (a.n_s == 64) return launch_mf_staged_t<false, CW, S, 64, false, false>(a, st);
-    return launch_mf_staged_t<false, CW, S, 0, false, false>(a, st);
+    if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, false, 1, RAG>(a, st);
+    if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, false, 1, RAG>(a, st);
+    if (!RAG && a.n_s == 64) return launch_mf_staged_t<false, CW, S, 64, false, false>(a, st);
+    return launch_mf_staged_t<false, CW, S, 0, false, false, 1, RAG>(a, st);
 }
 
-// two slices per unit (the plan picks these only where N_s % 128 == 0)
-template <int CW, int S>
+// two slices per unit (the plan picks these only for N_s >= 128)
+template <int CW, int S, bool RAG = false>
 static cudaError_t launch_mf_staged_wide(const StepArgs& a, cudaStream_t st) {
-    if (a.n_s % 128 != 0) return cudaErrorInvalidValue;
+    if (a.n_s < 128) return cudaErrorInvalidValue;
     if (a.mfs_slices > 1) {
-        if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, true, 2>(a, st);
-        if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, true, 2>(a, st);
-        return launch_mf_staged_t<false, CW, S, 0, false, true, 2>(a, st);
+        if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, true, 2, RAG>(a, st);
+        if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, true, 2, RAG>(a, st);
+        return launch_mf_staged_t<false, CW, S, 0, false, true, 2, RAG>(a, st);
     }
-    if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, false, 2>(a, st);
-    if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, false, 2>(a, st);
-    return launch_mf_staged_t<false, CW, S, 0, false, false, 2>(a, st);
+    if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, false, 2, RAG>(a, st);
+    if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, false, 2, RAG>(a, st);
+    return launch_mf_staged_t<false, CW, S, 0, false, false, 2, RAG>(a, st);
 }
 
 static cudaError_t launch_mf_staged(const StepArgs& a, cudaStream_t st) {
     switch (a.mfs_shape) {
         case 1: return launch_mf_staged_shape<15, 3>(a, st);
-        case 2: return launch_mf_staged_wide<7, 3>(a, st);
+        case 2: return a.n_s % 128 ? launch_mf_staged_wide<7, 3, true>(a, st) : launch_mf_staged_wide<7, 3>(a, st);
         case 3: return launch_mf_staged_wide<11, 3>(a, st);
-        default: return launch_mf_staged_shape<11, 3>(a, st);
+        default: return a.n_s % 64 ? launch_mf_staged_shape<11, 3, true>(a, st) : launch_mf_staged_shape<11, 3>(a, st);
     }
 }
 

@@ -60,6 +60,49 @@ def test_variants_bitexact_and_oracle_spmm(n_s):
     ens.close()
 
 
+@pytest.mark.parametrize("n_s,damping", [(66, "mass"), (100, "identity"), (200, "mass"), (258, "mass"),
+                                         (500, "identity")])
+def test_staged_ragged_ensemble(n_s, damping):
+    """Any even N_s >= 64 takes STAGED: the last unit (or sliced stage) of a row is partial,
+    its lanes past N_s address realisation N_s - 2 and store nothing.  States and products
+    bit-identical to TILES (which handles any N_s), the product against the oracle.  N_s = 66:
+    one-slice units, the second of a row 2 wide; 100, 200: two-slice units (100 of 128, then
+    128 + 72); 258: sliced, 64-wide slices (5, the last 2 wide); 500: sliced, 128-wide (4, the
+    last 116 wide)."""
+    m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(24, 60), 0.01, 3), 9)
+    E, h = _mats(m, n_s, 31)
+    c_d = 120.0 if damping == "mass" else 0.3
+    ref = _run(m, E, h, "tiles", damping=damping, c_d=c_d, steps=200)
+    got = _run(m, E, h, "staged", damping=damping, c_d=c_d, steps=200)
+    for k in range(3):
+        assert np.array_equal(ref[k], got[k]), k
+    ens, om = _pair(m, E, h, kernel="matrix_free")
+    assert ens.info()["mf_variant"] == MFV["staged"]             # AUTO takes it
+    _check_spmm(ens, om, np.random.default_rng(n_s).uniform(-1, 1, (n_s, m.n_nodes, 3)))
+    ens.close()
+
+
+@pytest.mark.parametrize("halo", ["nccl", "p2p"])
+def test_staged_ragged_node_partition(halo):
+    """A ragged N_s (100: one two-slice unit per row with 100 of its 128 lanes' realisations
+    valid) in a node partition with P2P forwarding of the partial unit: bit-identical to one
+    part."""
+    m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(24, 60), 0.01, 3), 4)
+    E, h = _mats(m, 100, 62)
+    tr = loads.pulsatile(m.xyz, m.tris, period=0.01, systole=0.004, ramp_T=0.003)
+    kw = dict(rho=RHO, nu=NU, k_shear=KS, kernel="matrix_free", dt=5e-5, damping="mass", c_d=80.0,
+              mf_variant="staged")
+    ref = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, **kw)
+    par = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, dist="node", world=3, halo=halo, **kw)
+    for e in (ref, par):
+        e.set_traction(tr.F, tr.tab_t, tr.tab_g, tr.period, tr.ramp_T)
+        e.step(201)
+    u0, p0, _, s0 = ref.get_state()
+    u1, p1, _, s1 = par.get_state()
+    assert s0 == s1 and np.array_equal(u0, u1) and np.array_equal(p0, p1)
+    ref.close(); par.close()
+
+
 def test_staged_identity_damping_bitexact():
     """Per-row c2, c3 arrays (damping mode 2) in the staged kernel (the C23 instance)."""
     m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(20, 40), 0.01, 5), 3)
@@ -146,10 +189,11 @@ def test_staged_shapes_bitexact(n_s, damping, monkeypatch):
 
 
 def test_variant_selection_and_rejection():
-    """AUTO takes STAGED where it applies (N_s % 64 == 0) and TILES elsewhere; asking for a
+    """AUTO takes STAGED where it applies (even N_s >= 64) and TILES elsewhere; asking for a
     path that does not apply is ENS_E_UNSUPPORTED."""
     m = meshmod.cylinder(12, 23)
-    for n_s, want in ((64, "staged"), (128, "staged"), (48, "tiles"), (5, "tiles")):
+    for n_s, want in ((64, "staged"), (128, "staged"), (100, "staged"), (48, "tiles"), (5, "tiles"),
+                      (101, "tiles")):
         E, h = _mats(m, n_s, 3)
         ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, kernel="matrix_free")
         assert ens.info()["mf_variant"] == MFV[want]

@@ -88,11 +88,13 @@ def test_1e4_steps_every_kernel(kernel, variant, n_s, damping):
     ens.close()
 
 
-@pytest.mark.parametrize("n_s,damping", [(128, "mass"), (128, "identity"), (256, "mass")])
+@pytest.mark.parametrize("n_s,damping", [(128, "mass"), (128, "identity"), (256, "mass"), (100, "mass"),
+                                         (200, "identity")])
 def test_1e4_steps_staged_wide(n_s, damping):
     """The matrix-free default at N_s % 128 == 0: two 64-realisation slices per consumer unit
-    (shape 7x3w), whole rows at 128 and 128-wide sliced stages at 256, 10^4 steps against the
-    oracle (the same bar as above)."""
+    (shape 7x3w), whole rows at 128 and 128-wide sliced stages at 256; ragged N_s (100: one
+    two-slice unit per row, 100 of 128 realisations valid; 200: two units, the second 72 wide),
+    10^4 steps against the oracle (the same bar as above)."""
     cfg, dt, tr, snaps = _c1_case(n_s, damping)
     m = cfg.mesh
     ens = solver.Ensemble(m.xyz, m.tris, m.fixed, cfg.E, cfg.h, rho=RHO, nu=NU, k_shear=KS, dt=dt,
