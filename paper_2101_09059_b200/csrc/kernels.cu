@@ -1287,6 +1287,7 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
                 for (int d = 0; d < 3; ++d) uo[j][d] = ld2(own + d * AS + 512 * j);
             auto rel = [&](Vec<2> (&w)[WS][3], int32_t off) {   // w = u[node at off] - u_i
                 MFS_CHECK(off >= 0 && uint32_t(off) + US <= SB, "u read past the stage", off, US);
+                MFS_CHECK(uint32_t(off) + lofs + 2 * AS + 512 * (WS - 1) + 16 <= SB, "lane's u read past the stage", off, lofs);
 #pragma unroll
                 for (int j = 0; j < WS; ++j)
 #pragma unroll
@@ -1298,6 +1299,7 @@ k_step_mf_staged(const StepArgs a, const __grid_constant__ MfsMaps maps) {
             };
             auto ldal = [&](int32_t off) {
                 MFS_CHECK(off >= 0 && uint32_t(off) + AS <= SB, "alpha read past the stage", off, AS);
+                MFS_CHECK(uint32_t(off) + lofs + 512 * (WS - 1) + 16 <= SB, "lane's alpha read past the stage", off, lofs);
 #pragma unroll
                 for (int j = 0; j < WS; ++j) al[j] = ld2(st + off + lofs + 512 * j);
             };
