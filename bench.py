@@ -307,7 +307,10 @@ def _line_item(run, steps, units, peak):
     info = run.info
     per = run.el / steps
     ach = info["bytes_per_step"] / (run.el_local / steps) / 1e9     # this rank's kernel bytes / its time
-    return {"value": units / run.el, "unit": "DOF-updates/s", "ms_per_step": 1e3 * per,
+    extra = {}
+    if info.get("mfs_consumers"):
+        extra["staged_shape"] = {k: info[k] for k in ("mfs_consumers", "mfs_unit_width", "mfs_stage_width", "mfs_stages")}
+    return {**extra, "value": units / run.el, "unit": "DOF-updates/s", "ms_per_step": 1e3 * per,
             "achieved_GBs": ach, "frac": ach / peak, "algorithmic_bytes_per_launch": info["bytes_per_step"],
             "achieved_fp64_TFLOPs": info["flops_per_step"] / (run.el_local / steps) / 1e12,
             "algorithmic_flops_per_launch": info["flops_per_step"], "kernel_fn": _KERNEL_FN[run.kernel](info)}

@@ -173,6 +173,11 @@ typedef struct {
                                            STAGED); 0 for the assembled kernels */
     int32_t comm_rank, comm_nranks;     /* NODE with nccl_comm: ncclCommUserRank / ncclCommCount of the
                                            communicator the halo runs on; -1 otherwise */
+    int32_t mfs_consumers;              /* STAGED: consumer warps per CTA (0 otherwise) */
+    int32_t mfs_unit_width;             /* STAGED: realisations per consumer unit (64 or 128) */
+    int32_t mfs_stage_width;            /* STAGED: realisations per stage row (N_s, or the slice width
+                                           of sliced stages) */
+    int32_t mfs_stages;                 /* STAGED: shared-memory stages per CTA */
 } ens_info;
 
 /* Create a context: validate the mesh, build the RCM-ordered block-CSR pattern, the

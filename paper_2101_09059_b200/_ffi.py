@@ -50,7 +50,8 @@ class EnsInfo(C.Structure):
                 ("n_owned", C.c_int64), ("halo_bytes_per_step", C.c_int64),
                 ("launches_per_step", C.c_int32), ("reassemble_every", C.c_int32), ("graph_steps", C.c_int32),
                 ("halo", C.c_int32), ("mf_variant", C.c_int32), ("comm_rank", C.c_int32),
-                ("comm_nranks", C.c_int32)]
+                ("comm_nranks", C.c_int32), ("mfs_consumers", C.c_int32), ("mfs_unit_width", C.c_int32),
+                ("mfs_stage_width", C.c_int32), ("mfs_stages", C.c_int32)]
 
 
 EXPORTS = [

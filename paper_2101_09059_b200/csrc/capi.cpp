@@ -2135,6 +2135,14 @@ int ens_query(const ens_ctx* c, ens_info* info) {
     info->reassemble_every = c->reassemble_every;
     info->halo = c->halo;
     info->mf_variant = c->kernel == ENS_KERNEL_MATRIX_FREE ? c->mf_variant : 0;
+    info->mfs_consumers = info->mfs_unit_width = info->mfs_stage_width = info->mfs_stages = 0;
+    if (c->kernel == ENS_KERNEL_MATRIX_FREE && c->mf_variant == ENS_MF_STAGED) {
+        const ens::MfsShape sh = ens::mf_staged_shape(c->mfs_plan.shape);
+        info->mfs_consumers = sh.consumers;
+        info->mfs_unit_width = 64 * c->mfs_plan.ws;
+        info->mfs_stage_width = ens::mfs_stage_w(c->mfs_plan, c->n_s);
+        info->mfs_stages = sh.stages;
+    }
     info->comm_rank = info->comm_nranks = -1;
     if (c->nccl_comm && c->nccl && c->nccl->comm_count && c->nccl->comm_user_rank) {
         int r = -1, n = -1;

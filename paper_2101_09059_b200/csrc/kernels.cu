@@ -1852,13 +1852,12 @@ MfsPlan mf_staged_plan(int32_t n_s) {
     p.sliced = sv ? std::atoi(sv) != 0 && n_s > 64 : n_s >= 256;   // N_s >= 256: a node row (6 KB+) is too big
     const int env = mfs_env_shape();
     // 7x3w (two slices per unit) unless that pads more realisations than one slice per unit
-    // does (N_s = 192: three units of 64 against two of 128 with 64 idle lanes), else 11x3; a
-    // wide shape asked for below N_s = 128 falls back to 11x3
+    // does (N_s = 64: one unit of 64 against one of 128 with half the lanes idle; N_s = 192:
+    // three units of 64 against two of 128), else 11x3
     auto pad = [&](int w) { return (n_s + w - 1) / w * w - n_s; };
-    const bool wide_ok = n_s >= 128 && pad(128) <= pad(64);
+    const bool wide_ok = pad(128) <= pad(64);
     // shapes other than the defaults (11x3, 7x3w) have no instances for a ragged N_s
-    const bool env_ok = env >= 0 && (kMfsShapes[env].ws == 1 || n_s >= 128) &&
-                        (env == 0 || env == kMfsWide || n_s % (64 * kMfsShapes[env].ws) == 0);
+    const bool env_ok = env >= 0 && (env == 0 || env == kMfsWide || n_s % (64 * kMfsShapes[env].ws) == 0);
     p.shape = env_ok ? env : (wide_ok ? kMfsWide : 0);
     p.ws = kMfsShapes[p.shape].ws;
     const char* t = std::getenv("ENS_MFS_TILING");
@@ -1966,10 +1965,10 @@ static cudaError_t launch_mf_staged_shape(const StepArgs& a, cudaStream_t st) {
     return launch_mf_staged_t<false, CW, S, 0, false, false, 1, RAG>(a, st);
 }
 
-// two slices per unit (the plan picks these only for N_s >= 128)
+// two slices per unit
 template <int CW, int S, bool RAG = false>
 static cudaError_t launch_mf_staged_wide(const StepArgs& a, cudaStream_t st) {
-    if (a.n_s < 128) return cudaErrorInvalidValue;
+    if (a.n_s < 64) return cudaErrorInvalidValue;
     if (a.mfs_slices > 1) {
         if (a.y_out) return launch_mf_staged_t<true, CW, S, 0, false, true, 2, RAG>(a, st);
         if (a.c2a) return launch_mf_staged_t<false, CW, S, 0, true, true, 2, RAG>(a, st);

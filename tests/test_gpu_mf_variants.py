@@ -65,10 +65,9 @@ def test_variants_bitexact_and_oracle_spmm(n_s):
 def test_staged_ragged_ensemble(n_s, damping):
     """Any even N_s >= 64 takes STAGED: the last unit (or sliced stage) of a row is partial,
     its lanes past N_s address realisation N_s - 2 and store nothing.  States and products
-    bit-identical to TILES (which handles any N_s), the product against the oracle.  N_s = 66:
-    one-slice units, the second of a row 2 wide; 100, 200: two-slice units (100 of 128, then
-    128 + 72); 258: sliced, 64-wide slices (5, the last 2 wide); 500: sliced, 128-wide (4, the
-    last 116 wide)."""
+    bit-identical to TILES (which handles any N_s), the product against the oracle.  N_s = 66,
+    100, 200: two-slice units (66 or 100 of 128; 128 + 72); 258: sliced, 64-wide slices (5, the
+    last 2 wide); 500: sliced, 128-wide (4, the last 116 wide)."""
     m = meshmod.shuffle_nodes(meshmod.perturb(meshmod.cylinder(24, 60), 0.01, 3), 9)
     E, h = _mats(m, n_s, 31)
     c_d = 120.0 if damping == "mass" else 0.3
@@ -192,11 +191,20 @@ def test_variant_selection_and_rejection():
     """AUTO takes STAGED where it applies (even N_s >= 64) and TILES elsewhere; asking for a
     path that does not apply is ENS_E_UNSUPPORTED."""
     m = meshmod.cylinder(12, 23)
-    for n_s, want in ((64, "staged"), (128, "staged"), (100, "staged"), (48, "tiles"), (5, "tiles"),
-                      (101, "tiles")):
+    # the staged shape the plan picks (ens_info): consumers, unit width, stage-row width
+    shapes = {64: (11, 64, 64), 128: (7, 128, 128), 100: (7, 128, 100), 192: (11, 64, 192), 500: (7, 128, 128),
+              66: (7, 128, 66)}
+    for n_s, want in ((64, "staged"), (128, "staged"), (100, "staged"), (192, "staged"), (500, "staged"), (66, "staged"),
+                      (48, "tiles"), (5, "tiles"), (101, "tiles")):
         E, h = _mats(m, n_s, 3)
         ens = solver.Ensemble(m.xyz, m.tris, m.fixed, E, h, rho=RHO, nu=NU, kernel="matrix_free")
-        assert ens.info()["mf_variant"] == MFV[want]
+        inf = ens.info()
+        assert inf["mf_variant"] == MFV[want]
+        if want == "staged":
+            assert (inf["mfs_consumers"], inf["mfs_unit_width"], inf["mfs_stage_width"]) == shapes[n_s], n_s
+            assert inf["mfs_stages"] == 3
+        else:
+            assert inf["mfs_consumers"] == 0
         ens.close()
     for n_s, damping, variant in ((48, "mass", "staged"), (64, "identity", "warp"), (96, "none", "warp")):
         E, h = _mats(m, n_s, 3)
